@@ -1,0 +1,142 @@
+// Internal declarations shared by the host driver (api.cpp) and the CUDA
+// kernels. Not part of the ABI (include/accord.h is).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/accord.h"
+
+namespace accord {
+
+constexpr int kKPad = 64;       // samples padded to a multiple of 64 (one 128-B bf16 TMA row)
+constexpr int kRowPad = 256;    // operand rows padded to the GEMM tile (M and N)
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// ---------------------------------------------------------------------------
+// Device-side views of the per-rank state (plain pointers, no ownership).
+// ---------------------------------------------------------------------------
+struct OmegaView {            // this rank's rows of Omega, CSR, sorted global columns
+  const int64_t* ptr;         // [pk + 1]
+  const int32_t* col;
+  const void* val;            // T
+};
+
+struct PoolView {             // candidate pool written by the GEMM epilogue (unsorted)
+  int32_t* row;               // local row index
+  int32_t* col;               // global column
+  void* g;                    // T: [Omega S]_ik
+  void* w;                    // T: omega_ik^{(t)} (0 if absent)
+  int64_t cap;                // capacity in entries
+  unsigned long long* cursor; // number of entries emitted (may exceed cap)
+  int32_t* row_cnt;           // [pk] entries emitted per row
+};
+
+struct EpiParams {            // candidate rule of the fused epilogue
+  int64_t pk, p, r0;          // local rows, columns, global index of local row 0
+  double inv_n;
+  double lam_cand;            // emit (i,k) iff k == i, or omega_ik != 0, or |g| > lam_cand
+  // BF16_FILTER only: per-entry rigorous error bound of the single-pass bf16
+  // product, n*delta_ik = r1_i * s_k + B_i * D_k (see gemm_tc.cu)
+  const float* row_A;         // ||y_i - bf16(y_i)||       (current Y buffer)
+  const float* row_B;         // ||y_i||
+  const float2* col_sd;       // (||x_k|| + ||x_k - bf16(x_k)||, ||x_k - bf16(x_k)||)
+  float gamma;                // accumulation-error factor
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (kernels.cu, gemm_simt.cu, gemm_tc.cu). All asynchronous
+// on `st`; each returns the number of kernel launches issued.
+// ---------------------------------------------------------------------------
+// X (any layout, f32/f64, device) -> Xt (T, prows x ldk, zero padded). Sets
+// *bad to the first non-finite linear index (init it to INT64_MAX).
+int launch_load_xt(int dtype, const void* X, int64_t ldx, int layout, int64_t n, int64_t p,
+                   void* Xt, int64_t ldk, int64_t prows, unsigned long long* bad,
+                   cudaStream_t st);
+// Xt f32 -> hi = bf16_rn(x), lo = bf16_rn(x - hi) (rows x ldk)
+int launch_split_bf16(const float* src, int64_t elems, __nv_bfloat16* hi,
+                      __nv_bfloat16* lo, cudaStream_t st);
+
+// Power iteration for L = lambda_max(X^T X / n) on Xt (p x ldk). Deterministic.
+// Returns launches; writes the estimate to *L_host (synchronizes).
+int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk,
+                    int max_iter, double tol, double* L_host, cudaStream_t st,
+                    std::string* err);
+
+// Exclusive scan: out[0..N] (out[N] = total) from int32 counts.
+int launch_scan_i32(const int32_t* in, int64_t* out, int64_t N, void* tmp, size_t tmp_bytes,
+                    cudaStream_t st);
+size_t scan_tmp_bytes(int64_t N);
+
+// Finalize the candidate pool into the sorted per-row candidate set C.
+int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* c_ptr,
+                    int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col,
+                    void* c_g, void* c_w, int32_t* long_rows, cudaStream_t st);
+
+// Prox at trial tau over C (Eq. 3.5) with per-row partial sums.
+int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                const void* c_g, const void* c_w, void* c_wn, double tau, double lam,
+                double* row_dd, double* row_l1, double* row_logd, int32_t* row_nnz,
+                cudaStream_t st);
+
+// SpMM Y+ = Omega+ X^T and D = Delta X^T over a CSR (ptr/col/wn/wo); wo may be
+// NULL (Delta = 0). Accumulates in double; writes Y (T), optionally its bf16
+// hi (and lo) copies with the per-row norms ||y||, ||y - bf16(y)||, and the
+// per-row ||D_i||^2, ||Y+_i||^2.
+int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* ptr,
+                const int32_t* col, const void* wn, const void* wo, const void* Xt,
+                void* Yout, __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A,
+                float* row_B, double* row_D2, double* row_Y2, cudaStream_t st);
+
+// Exact candidate values (BF16_FILTER): c_g[e] = (1/n) sum_m Y_im Xt_km in
+// float64 accumulation, for every entry of C (block per row).
+int launch_refine(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
+                  const int32_t* c_col, const float* Y, const float* Xt, float* c_g,
+                  cudaStream_t st);
+
+// Per-column constants of the filter bound from Xt (f32).
+int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st);
+
+// Omega stats over the current CSR: l1, logdiag, nnz, diagonal check.
+int launch_omega_stats(int dtype, int64_t pk, int64_t r0, const int64_t* ptr,
+                       const int32_t* col, const void* val, double* row_l1, double* row_logd,
+                       int32_t* row_nnz, int32_t* bad_diag, cudaStream_t st);
+
+// Fixed-order reduction of the per-row partials into out[8] =
+// {D2, dd, logd, Y2, l1, nnz, ncand, 0}. Any pointer may be NULL (-> 0).
+int launch_reduce_rows(int64_t pk, const double* row_D2, const double* row_dd,
+                       const double* row_logd, const double* row_Y2, const double* row_l1,
+                       const int32_t* row_nnz, const int64_t* c_ptr, double* out,
+                       cudaStream_t st);
+
+// Compaction of C (with new values) into Omega's CSR after acceptance.
+int launch_compact(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr,
+                   const int32_t* c_col, const void* c_wn, const int64_t* om_ptr,
+                   int32_t* om_col, void* om_val, cudaStream_t st);
+
+// Identity Omega^{(0)}.
+int launch_identity(int dtype, int64_t pk, int64_t r0, int64_t* om_ptr, int32_t* om_col,
+                    void* om_val, cudaStream_t st);
+
+// Gradient GEMM + fused candidate epilogue (CUDA cores; T = float or double).
+int launch_gemm_simt(int dtype, const void* Y, const void* Xt, int64_t ldk, int64_t kdim,
+                     const EpiParams& ep, const OmegaView& om, const PoolView& pool,
+                     cudaStream_t st);
+
+// tcgen05 split-bf16 GEMM + fused epilogue (gemm_tc.cu).
+struct TcGemmPlan;   // opaque: tensor maps for both Y buffers
+TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
+                           const __nv_bfloat16* Yhi1, const __nv_bfloat16* Ylo1,
+                           int64_t pk_pad, const __nv_bfloat16* Xhi,
+                           const __nv_bfloat16* Xlo, int64_t p_pad, int64_t ldk,
+                           std::string* err);
+void tc_plan_destroy(TcGemmPlan*);
+int launch_gemm_tc(TcGemmPlan* plan, int mode /* accord_gemm: BF16X3 or BF16_FILTER */,
+                   int ybuf, int64_t kdim, int sm_count, const EpiParams& ep,
+                   const OmegaView& om, const PoolView& pool, cudaStream_t st);
+bool tc_supported(int cc_major, int cc_minor);
+
+}  // namespace accord

@@ -1,0 +1,994 @@
+// HBM-bound kernels of the ACCORD-FBS hot path (everything except the
+// gradient GEMM): data load / operand split (a1), candidate finalize (a4),
+// prox at trial tau (a5), SpMM with fused reductions (a6), fixed-order
+// reductions (a7), compaction of the accepted iterate, power iteration for L.
+//
+// Row r of every per-rank array is the global row r0 + r of Omega.
+#include "accord_internal.h"
+
+#include <cmath>
+#include <cfloat>
+#include <climits>
+#include <vector>
+
+namespace accord {
+
+namespace {
+
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int V = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int V = 2; };
+
+__device__ __forceinline__ float vget(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ double vget(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum with a fixed reduction order (deterministic).
+template <typename T>
+__device__ T block_sum(T v, T* sh /* >= 32 */) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  T r = (threadIdx.x < nw) ? sh[threadIdx.x] : T(0);
+  if (w == 0) r = warp_sum(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// a1: X -> Xt (variable-major, zero padded), finiteness check
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void load_xt_kernel(const T* __restrict__ X, int64_t ldx, int layout, int64_t n,
+                               int64_t p, T* __restrict__ Xt, int64_t ldk, int64_t prows,
+                               unsigned long long* bad) {
+  __shared__ T tile[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t m0 = (int64_t)blockIdx.x * 32;
+  for (int64_t jb = blockIdx.y; jb * 32 < prows; jb += gridDim.y) {
+    const int64_t j0 = jb * 32;
+    if (layout == ACCORD_LAYOUT_VARIABLES_ROW_MAJOR) {
+      for (int jj = ty; jj < 32; jj += 8) {
+        const int64_t j = j0 + jj, m = m0 + tx;
+        T v = T(0);
+        if (j < p && m < n) {
+          v = X[j * ldx + m];
+          if (!isfinite(v)) atomicMin(bad, (unsigned long long)(j * n + m));
+        }
+        Xt[j * ldk + m] = v;
+      }
+    } else {
+      // X is n x p row-major: read with tx along j (coalesced), write with tx along m.
+      for (int mm = ty; mm < 32; mm += 8) {
+        const int64_t m = m0 + mm, j = j0 + tx;
+        T v = T(0);
+        if (j < p && m < n) {
+          v = X[m * ldx + j];
+          if (!isfinite(v)) atomicMin(bad, (unsigned long long)(m * p + j));
+        }
+        tile[mm][tx] = v;
+      }
+      __syncthreads();
+      for (int jj = ty; jj < 32; jj += 8) Xt[(j0 + jj) * ldk + m0 + tx] = tile[tx][jj];
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void split_bf16_kernel(const float4* __restrict__ src, int64_t n4,
+                                  __nv_bfloat162* __restrict__ hi,
+                                  __nv_bfloat162* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = src[i];
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(v.z, v.w);
+    float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+    hi[2 * i] = h0;
+    hi[2 * i + 1] = h1;
+    lo[2 * i] = __floats2bfloat162_rn(v.x - f0.x, v.y - f0.y);
+    lo[2 * i + 1] = __floats2bfloat162_rn(v.z - f1.x, v.w - f1.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan int32 -> int64 (3 phases, fixed order)
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanChunk = kScanThreads * kScanItems;
+
+__device__ int64_t block_excl_scan(int64_t v, int64_t* sh, int64_t* total) {
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (l >= o) x += y;
+  }
+  if (l == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t s = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (l >= o) s += y;
+    }
+    sh[l] = s;  // inclusive warp sums
+  }
+  __syncthreads();
+  int64_t off = (w > 0) ? sh[w - 1] : 0;
+  *total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return off + x - v;
+}
+
+__global__ void __launch_bounds__(1024) scan_phase1(const int32_t* __restrict__ in, int64_t N, int64_t* bsum) {
+  __shared__ int64_t sh[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * kScanItems;
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < N) s += in[base + k];
+  s = block_sum<int64_t>(s, sh);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) scan_phase2(int64_t* bsum, int64_t nb) {
+  __shared__ int64_t sh[32];
+  int64_t carry = 0;
+  for (int64_t c = 0; c < nb; c += blockDim.x) {
+    const int64_t i = c + threadIdx.x;
+    int64_t v = i < nb ? bsum[i] : 0, tot;
+    int64_t e = block_excl_scan(v, sh, &tot);
+    if (i < nb) bsum[i] = carry + e;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+__global__ void __launch_bounds__(1024) scan_phase3(const int32_t* __restrict__ in, int64_t N,
+                            const int64_t* __restrict__ bsum, int64_t nb, int64_t* out) {
+  __shared__ int64_t sh[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * kScanItems;
+  int64_t v[kScanItems], s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (base + k < N) ? in[base + k] : 0;
+    s += v[k];
+  }
+  int64_t tot;
+  int64_t e = block_excl_scan(s, sh, &tot) + bsum[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < N) out[base + k] = e;
+    e += v[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[N] = bsum[nb];
+}
+
+// ---------------------------------------------------------------------------
+// a4: candidate finalize: scatter pool -> per-row key segments, per-row sort
+// by column, gather values in sorted order.
+// key = (col << 32) | pool_index (unique), so sorting keys sorts by column.
+// ---------------------------------------------------------------------------
+constexpr int kWarpSortMax = 1024;     // rows up to this length: one warp, smem bitonic
+constexpr int kBlockSortMax = 16384;   // rows up to this length: one block, smem bitonic
+
+__global__ void scatter_kernel(int64_t pk, const int32_t* __restrict__ prow,
+                               const int32_t* __restrict__ pcol,
+                               const unsigned long long* __restrict__ cursor, int64_t cap,
+                               const int64_t* __restrict__ c_ptr, int32_t* rcur,
+                               uint64_t* __restrict__ keys) {
+  const int64_t cnt = min((int64_t)*cursor, cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = prow[i];
+    const int64_t pos = c_ptr[r] + atomicAdd(&rcur[r], 1);
+    keys[pos] = ((uint64_t)(uint32_t)pcol[i] << 32) | (uint64_t)(uint32_t)i;
+  }
+}
+
+__device__ __forceinline__ void bitonic_warp(uint64_t* s, int n2) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < n2; t += 32) {
+        const int ixj = t ^ j;
+        if (ixj > t) {
+          const bool asc = (t & k) == 0;
+          uint64_t a = s[t], b = s[ixj];
+          if ((a > b) == asc) { s[t] = b; s[ixj] = a; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void rowsort_warp_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
+                                    uint64_t* __restrict__ keys, int32_t* long_rows) {
+  extern __shared__ uint64_t sm_keys[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* s = sm_keys + (size_t)wib * kWarpSortMax;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (r >= pk) return;
+  const int64_t beg = c_ptr[r], len = c_ptr[r + 1] - beg;
+  if (len <= 1) return;
+  if (len > kWarpSortMax) {
+    if (lane == 0) {
+      int slot = atomicAdd(&long_rows[0], 1);
+      long_rows[1 + slot] = (int32_t)r;
+    }
+    return;
+  }
+  int n2 = 32;
+  while (n2 < len) n2 <<= 1;
+  for (int t = lane; t < n2; t += 32) s[t] = t < len ? keys[beg + t] : ~0ull;
+  __syncwarp();
+  bitonic_warp(s, n2);
+  for (int t = lane; t < len; t += 32) keys[beg + t] = s[t];
+}
+
+__global__ void __launch_bounds__(1024) rowsort_block_kernel(const int64_t* __restrict__ c_ptr,
+                                     uint64_t* __restrict__ keys, uint64_t* __restrict__ tmp,
+                                     const int32_t* __restrict__ long_rows) {
+  extern __shared__ uint64_t sm_keys[];
+  const int nlong = long_rows[0];
+  for (int q = blockIdx.x; q < nlong; q += gridDim.x) {
+    const int64_t r = long_rows[1 + q];
+    const int64_t beg = c_ptr[r], len = c_ptr[r + 1] - beg;
+    if (len <= kBlockSortMax) {
+      int n2 = 32;
+      while (n2 < len) n2 <<= 1;
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) sm_keys[t] = t < len ? keys[beg + t] : ~0ull;
+      __syncthreads();
+      for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+            const int ixj = t ^ j;
+            if (ixj > t) {
+              const bool asc = (t & k) == 0;
+              uint64_t a = sm_keys[t], b = sm_keys[ixj];
+              if ((a > b) == asc) { sm_keys[t] = b; sm_keys[ixj] = a; }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int t = threadIdx.x; t < len; t += blockDim.x) keys[beg + t] = sm_keys[t];
+      __syncthreads();
+    } else {
+      // Very long row: rank by counting (keys are unique), O(len^2) but correct.
+      for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
+        const uint64_t ka = keys[beg + a];
+        int64_t rank = 0;
+        for (int64_t b = 0; b < len; ++b) rank += keys[beg + b] < ka;
+        tmp[beg + rank] = ka;
+      }
+      __syncthreads();
+      for (int64_t a = threadIdx.x; a < len; a += blockDim.x) keys[beg + a] = tmp[beg + a];
+      __syncthreads();
+    }
+  }
+}
+
+template <typename T>
+__global__ void gather_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
+                              const uint64_t* __restrict__ keys, const T* __restrict__ pg,
+                              const T* __restrict__ pw, int32_t* __restrict__ c_col,
+                              T* __restrict__ c_g, T* __restrict__ c_w) {
+  const int64_t tot = c_ptr[pk];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    const uint32_t idx = (uint32_t)(k & 0xffffffffu);
+    c_col[e] = (int32_t)(k >> 32);
+    c_g[e] = pg[idx];
+    c_w[e] = pw[idx];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a5: prox at trial tau (Eq. 3.5), warp per row.
+// Forward step and prox are evaluated in double from the stored values; the
+// result is rounded to T. Diagonal root in the cancellation-free branch form.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double prox_diag_d(double y, double tau, double lam) {
+  const double a = y - tau * lam;
+  const double r = sqrt(a * a + 4.0 * tau);
+  return a >= 0.0 ? 0.5 * (a + r) : 2.0 * tau / (r - a);
+}
+
+template <typename T>
+__global__ void prox_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
+                            const int32_t* __restrict__ c_col, const T* __restrict__ c_g,
+                            const T* __restrict__ c_w, T* __restrict__ c_wn, double tau,
+                            double lam, double* __restrict__ row_dd,
+                            double* __restrict__ row_l1, double* __restrict__ row_logd,
+                            int32_t* __restrict__ row_nnz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const int64_t beg = c_ptr[r], end = c_ptr[r + 1];
+  const int64_t gi = r0 + r;
+  const double tl = tau * lam;
+  double dd = 0.0, l1 = 0.0, logd = 0.0;
+  int nnz = 0;
+  for (int64_t e = beg + lane; e < end; e += 32) {
+    const double wo = (double)c_w[e];
+    const double y = wo - tau * (double)c_g[e];       // forward step
+    double w;
+    if (c_col[e] == gi) {
+      w = prox_diag_d(y, tau, lam);
+    } else {
+      const double m = fabs(y) - tl;                   // S_{tau lam}(y)
+      w = m > 0.0 ? copysign(m, y) : 0.0;
+    }
+    const T wt = (T)w;
+    c_wn[e] = wt;
+    const double d = (double)wt - wo;
+    dd += d * d;
+    l1 += fabs((double)wt);
+    nnz += wt != T(0);
+    if (c_col[e] == gi) logd += log((double)wt);
+  }
+  dd = warp_sum(dd);
+  l1 = warp_sum(l1);
+  logd = warp_sum(logd);
+  nnz = warp_sum(nnz);
+  if (lane == 0) {
+    row_dd[r] = dd;
+    row_l1[r] = l1;
+    row_logd[r] = logd;
+    row_nnz[r] = nnz;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a6: SpMM Y+_i = sum_j w+_ij Xt_j and D_i = sum_j Delta_ij Xt_j, block per row,
+// 16-byte coalesced gathers of Xt rows; fused ||D_i||^2 and ||Y+_i||^2.
+// ---------------------------------------------------------------------------
+constexpr int kSpmmMaxThreads = 1024;
+
+template <typename T, bool kSplit>
+__global__ void __launch_bounds__(1024) spmm_kernel(
+    int64_t pk, int64_t n, int64_t ldk, const int64_t* __restrict__ ptr,
+    const int32_t* __restrict__ col, const T* __restrict__ wn, const T* __restrict__ wo,
+    const T* __restrict__ Xt, T* __restrict__ Yout, __nv_bfloat16* __restrict__ Yhi,
+    __nv_bfloat16* __restrict__ Ylo, float* __restrict__ row_A, float* __restrict__ row_B,
+    double* __restrict__ row_D2, double* __restrict__ row_Y2) {
+  using VT = typename Vec<T>::type;
+  constexpr int V = Vec<T>::V;
+  __shared__ int32_t s_col[kSpmmMaxThreads];
+  __shared__ double s_w[kSpmmMaxThreads];
+  __shared__ double s_d[kSpmmMaxThreads];
+  __shared__ int s_wc[32];
+  __shared__ double s_red[32];
+  const int64_t r = blockIdx.x;
+  const int64_t beg = ptr[r], end = ptr[r + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0;
+  for (int64_t c0 = 0; c0 < ldk; c0 += (int64_t)blockDim.x * V) {
+    const int64_t c = c0 + (int64_t)threadIdx.x * V;
+    const bool active = c < ldk;
+    double ay[V], ad[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+    for (int64_t e0 = beg; e0 < end; e0 += blockDim.x) {
+      // stage the next blockDim entries in order, dropping w+ = Delta = 0
+      // (deterministic ballot/prefix compaction)
+      const int64_t e = e0 + threadIdx.x;
+      bool keep = false;
+      double w = 0.0, d = 0.0;
+      int32_t cc = 0;
+      if (e < end) {
+        w = (double)wn[e];
+        d = wo ? w - (double)wo[e] : 0.0;
+        cc = col[e];
+        keep = (w != 0.0) || (d != 0.0);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) s_wc[wid] = __popc(m);
+      __syncthreads();
+      int off = 0, cnt = 0;
+      for (int q = 0; q < nw; ++q) {
+        const int x = s_wc[q];
+        off += q < wid ? x : 0;
+        cnt += x;
+      }
+      if (keep) {
+        const int s = off + __popc(m & ((1u << lane) - 1u));
+        s_col[s] = cc;
+        s_w[s] = w;
+        s_d[s] = d;
+      }
+      __syncthreads();
+      if (active) {
+        int q = 0;
+        for (; q + 4 <= cnt; q += 4) {
+          VT x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            x[u] = __ldg(reinterpret_cast<const VT*>(Xt + (int64_t)s_col[q + u] * ldk + c));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double wv = s_w[q + u], dv = s_d[q + u];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              ay[v] = fma(wv, (double)vget(x[u], v), ay[v]);
+              ad[v] = fma(dv, (double)vget(x[u], v), ad[v]);
+            }
+          }
+        }
+        for (; q < cnt; ++q) {
+          VT x = __ldg(reinterpret_cast<const VT*>(Xt + (int64_t)s_col[q] * ldk + c));
+          const double wv = s_w[q], dv = s_d[q];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            ay[v] = fma(wv, (double)vget(x, v), ay[v]);
+            ad[v] = fma(dv, (double)vget(x, v), ad[v]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (active) {
+      T yt[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        d2 += ad[v] * ad[v];
+        y2 += ay[v] * ay[v];
+        yt[v] = (T)ay[v];
+      }
+      if (Yout) {
+        VT o;
+        if constexpr (V == 4) o = make_float4(yt[0], yt[1], yt[2], yt[3]);
+        else o = make_double2(yt[0], yt[1]);
+        *reinterpret_cast<VT*>(Yout + r * ldk + c) = o;
+      }
+      if constexpr (kSplit) {
+        // GEMM operand copies: hi = bf16(y), lo = bf16(y - hi); norms for the
+        // filter bound: ||y||, ||y - hi||
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float y = (float)yt[v];
+          const __nv_bfloat16 h = __float2bfloat16_rn(y);
+          const float hf = __bfloat162float(h);
+          Yhi[r * ldk + c + v] = h;
+          if (Ylo) Ylo[r * ldk + c + v] = __float2bfloat16_rn(y - hf);
+          const double e = (double)y - (double)hf;
+          a2 += e * e;
+          b2 += (double)y * (double)y;
+        }
+      }
+    }
+  }
+  d2 = block_sum(d2, s_red);
+  y2 = block_sum(y2, s_red);
+  if constexpr (kSplit) {
+    a2 = block_sum(a2, s_red);
+    b2 = block_sum(b2, s_red);
+  }
+  if (threadIdx.x == 0) {
+    if (row_D2) row_D2[r] = d2;
+    if (row_Y2) row_Y2[r] = y2;
+    if constexpr (kSplit) {
+      // rounded up: these enter an upper bound
+      if (row_A) row_A[r] = __double2float_ru(sqrt(a2) * (1.0 + 1e-12));
+      if (row_B) row_B[r] = __double2float_ru(sqrt(b2) * (1.0 + 1e-12));
+    }
+  }
+  (void)n;
+}
+
+// ---------------------------------------------------------------------------
+// BF16_FILTER refinement: exact candidate values, warp per entry, Y_i staged
+// in shared memory, float64 accumulation. c_g[e] = (1/n) <Y_i, Xt_k>.
+// ---------------------------------------------------------------------------
+constexpr int kRefineMaxK = 4096;   // samples per row staged in smem (ldk <= 4096)
+
+__global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
+                                                     const int64_t* __restrict__ c_ptr,
+                                                     const int32_t* __restrict__ c_col,
+                                                     const float* __restrict__ Y,
+                                                     const float* __restrict__ Xt,
+                                                     float* __restrict__ c_g) {
+  __shared__ __align__(16) float ys[kRefineMaxK];
+  const int64_t r = blockIdx.x;
+  const int64_t beg = c_ptr[r], end = c_ptr[r + 1];
+  if (beg == end) return;
+  for (int64_t m = threadIdx.x * 4; m < ldk; m += blockDim.x * 4)
+    *reinterpret_cast<float4*>(ys + m) = *reinterpret_cast<const float4*>(Y + r * ldk + m);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double inv_n = 1.0 / (double)n;
+  for (int64_t e = beg + wid; e < end; e += nw) {
+    const float* xr = Xt + (int64_t)c_col[e] * ldk;
+    double s = 0.0;
+    int64_t m = lane * 4;
+    for (; m + 3 * 128 < ldk; m += 4 * 128) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(xr + m + u * 128));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 yv = *reinterpret_cast<const float4*>(ys + m + u * 128);
+        s = fma((double)yv.x, (double)x[u].x, s);
+        s = fma((double)yv.y, (double)x[u].y, s);
+        s = fma((double)yv.z, (double)x[u].z, s);
+        s = fma((double)yv.w, (double)x[u].w, s);
+      }
+    }
+    for (; m < ldk; m += 128) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(xr + m));
+      const float4 yv = *reinterpret_cast<const float4*>(ys + m);
+      s = fma((double)yv.x, (double)x.x, s);
+      s = fma((double)yv.y, (double)x.y, s);
+      s = fma((double)yv.z, (double)x.z, s);
+      s = fma((double)yv.w, (double)x.w, s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) c_g[e] = (float)(s * inv_n);
+  }
+}
+
+// per-column constants of the filter bound (warp per column of X = row of Xt)
+__global__ void col_norms_kernel(int64_t p, int64_t ldk, const float* __restrict__ Xt,
+                                 float2* __restrict__ col_sd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= p) return;
+  double xx = 0, ee = 0;
+  for (int64_t m = lane; m < ldk; m += 32) {
+    const float x = Xt[k * ldk + m];
+    const double e = (double)x - (double)__bfloat162float(__float2bfloat16_rn(x));
+    xx += (double)x * x;
+    ee += e * e;
+  }
+  xx = warp_sum(xx);
+  ee = warp_sum(ee);
+  if (lane == 0) {
+    const double xn = sqrt(xx) * (1.0 + 1e-12), en = sqrt(ee) * (1.0 + 1e-12);
+    col_sd[k] = make_float2(__double2float_ru(xn + en), __double2float_ru(en));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Omega statistics (l1, log diag, nnz, diagonal present and > 0), warp per row
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void omega_stats_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ ptr,
+                                   const int32_t* __restrict__ col, const T* __restrict__ val,
+                                   double* row_l1, double* row_logd, int32_t* row_nnz,
+                                   int32_t* bad_diag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  double l1 = 0, logd = 0;
+  int nnz = 0, has_diag = 0;
+  for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32) {
+    const double v = (double)val[e];
+    l1 += fabs(v);
+    nnz += v != 0.0;
+    if (col[e] == r0 + r) {
+      has_diag = 1;
+      if (v > 0.0) logd += log(v); else atomicExch(bad_diag, 1);
+    }
+  }
+  l1 = warp_sum(l1);
+  logd = warp_sum(logd);
+  nnz = warp_sum(nnz);
+  has_diag = warp_sum(has_diag);
+  if (lane == 0) {
+    row_l1[r] = l1;
+    row_logd[r] = logd;
+    row_nnz[r] = nnz;
+    if (!has_diag) atomicExch(bad_diag, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a7: fixed-order reduction of per-row partials (one block, deterministic)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) reduce_rows_kernel(int64_t pk, const double* __restrict__ D2,
+                                   const double* __restrict__ dd, const double* __restrict__ logd,
+                                   const double* __restrict__ Y2, const double* __restrict__ l1,
+                                   const int32_t* __restrict__ nnz, const int64_t* __restrict__ c_ptr,
+                                   double* out) {
+  __shared__ double sh[32];
+  double a[5] = {0, 0, 0, 0, 0};
+  long long cnt = 0;
+  for (int64_t r = threadIdx.x; r < pk; r += blockDim.x) {
+    if (D2) a[0] += D2[r];
+    if (dd) a[1] += dd[r];
+    if (logd) a[2] += logd[r];
+    if (Y2) a[3] += Y2[r];
+    if (l1) a[4] += l1[r];
+    if (nnz) cnt += nnz[r];
+  }
+  for (int k = 0; k < 5; ++k) {
+    double s = block_sum(a[k], sh);
+    if (threadIdx.x == 0) out[k] = s;
+  }
+  double s = block_sum((double)cnt, sh);
+  if (threadIdx.x == 0) {
+    out[5] = s;
+    out[6] = c_ptr ? (double)c_ptr[pk] : 0.0;
+    out[7] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Accept: compact C (with new values) into Omega's CSR; warp per row
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void compact_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
+                               const int32_t* __restrict__ c_col, const T* __restrict__ c_wn,
+                               const int64_t* __restrict__ om_ptr, int32_t* __restrict__ om_col,
+                               T* __restrict__ om_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  int64_t out = om_ptr[r];
+  const int64_t end = c_ptr[r + 1];
+  for (int64_t e0 = c_ptr[r]; e0 < end; e0 += 32) {
+    const int64_t e = e0 + lane;
+    bool keep = false;
+    int32_t cc = 0;
+    T v = T(0);
+    if (e < end) {
+      cc = c_col[e];
+      v = c_wn[e];
+      keep = (v != T(0)) || (cc == r0 + r);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int64_t pos = out + __popc(m & ((1u << lane) - 1u));
+      om_col[pos] = cc;
+      om_val[pos] = v;
+    }
+    out += __popc(m);
+  }
+}
+
+template <typename T>
+__global__ void identity_kernel(int64_t pk, int64_t r0, int64_t* om_ptr, int32_t* om_col,
+                                T* om_val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= pk;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    om_ptr[i] = i;
+    if (i < pk) {
+      om_col[i] = (int32_t)(r0 + i);
+      om_val[i] = T(1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Power iteration for L = sigma_max(S), deterministic:
+// u = X v (fixed split partial sums), w = X^T u / n (warp per row),
+// rq = v.w, v <- w / ||w||.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void pi_xv_kernel(const T* __restrict__ Xt, int64_t p, int64_t ldk, int64_t rows_per,
+                             const double* __restrict__ v, double* __restrict__ part) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= ldk) return;
+  const int64_t j0 = blockIdx.y * rows_per, j1 = min(p, j0 + rows_per);
+  double s = 0;
+  for (int64_t j = j0; j < j1; ++j) s += (double)Xt[j * ldk + m] * v[j];
+  part[blockIdx.y * ldk + m] = s;
+}
+
+__global__ void pi_sum_parts(const double* __restrict__ part, int64_t nsplit, int64_t ldk,
+                             double* __restrict__ u) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= ldk) return;
+  double s = 0;
+  for (int64_t q = 0; q < nsplit; ++q) s += part[q * ldk + m];
+  u[m] = s;
+}
+
+template <typename T>
+__global__ void pi_xtu_kernel(const T* __restrict__ Xt, int64_t p, int64_t ldk, int64_t n,
+                              const double* __restrict__ u, double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= p) return;
+  double s = 0;
+  for (int64_t m = lane; m < n; m += 32) s += (double)Xt[j * ldk + m] * u[m];
+  s = warp_sum(s);
+  if (lane == 0) w[j] = s / (double)n;
+}
+
+__global__ void __launch_bounds__(1024) pi_dots(const double* __restrict__ v, const double* __restrict__ w, int64_t p,
+                        double* out) {
+  __shared__ double sh[32];
+  double a = 0, b = 0;
+  for (int64_t j = threadIdx.x; j < p; j += blockDim.x) {
+    a += v[j] * w[j];
+    b += w[j] * w[j];
+  }
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
+}
+
+__global__ void pi_normalize(const double* __restrict__ w, int64_t p, const double* dots,
+                             double* __restrict__ v) {
+  const double inv = dots[1] > 0 ? 1.0 / sqrt(dots[1]) : 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x)
+    v[j] = w[j] * inv;
+}
+
+__global__ void fill_d(double* v, int64_t n, double x) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    v[j] = x;
+}
+
+inline int grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return (int)(g < cap ? g : cap);
+}
+
+}  // namespace
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+int launch_load_xt(int dtype, const void* X, int64_t ldx, int layout, int64_t n, int64_t p,
+                   void* Xt, int64_t ldk, int64_t prows, unsigned long long* bad,
+                   cudaStream_t st) {
+  dim3 blk(32, 8);
+  dim3 grd((unsigned)(ldk / 32), (unsigned)std::min<int64_t>(prows / 32, 65535));
+  if (dtype == ACCORD_F64)
+    load_xt_kernel<double><<<grd, blk, 0, st>>>((const double*)X, ldx, layout, n, p,
+                                                (double*)Xt, ldk, prows, bad);
+  else
+    load_xt_kernel<float><<<grd, blk, 0, st>>>((const float*)X, ldx, layout, n, p, (float*)Xt,
+                                               ldk, prows, bad);
+  return 1;
+}
+
+int launch_split_bf16(const float* src, int64_t elems, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                      cudaStream_t st) {
+  const int64_t n4 = elems / 4;
+  split_bf16_kernel<<<grid_for(n4, 256, 148 * 64), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(src), n4, reinterpret_cast<__nv_bfloat162*>(hi),
+      reinterpret_cast<__nv_bfloat162*>(lo));
+  return 1;
+}
+
+size_t scan_tmp_bytes(int64_t N) {
+  const int64_t nb = (N + kScanChunk - 1) / kScanChunk + 1;
+  return (size_t)(nb + 1) * sizeof(int64_t);
+}
+
+int launch_scan_i32(const int32_t* in, int64_t* out, int64_t N, void* tmp, size_t,
+                    cudaStream_t st) {
+  const int64_t nb = std::max<int64_t>(1, (N + kScanChunk - 1) / kScanChunk);
+  int64_t* bsum = (int64_t*)tmp;
+  scan_phase1<<<(unsigned)nb, kScanThreads, 0, st>>>(in, N, bsum);
+  scan_phase2<<<1, kScanThreads, 0, st>>>(bsum, nb);
+  scan_phase3<<<(unsigned)nb, kScanThreads, 0, st>>>(in, N, bsum, nb, out);
+  return 3;
+}
+
+int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* c_ptr,
+                    int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col, void* c_g,
+                    void* c_w, int32_t* long_rows, cudaStream_t st) {
+  int launches = 0;
+  scatter_kernel<<<148 * 8, 256, 0, st>>>(pk, pool.row, pool.col, pool.cursor, pool.cap, c_ptr,
+                                          rcur, keys);
+  ++launches;
+  {
+    const int warps = 8;
+    const size_t smem = (size_t)warps * kWarpSortMax * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(rowsort_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      cudaFuncSetAttribute(rowsort_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kBlockSortMax * sizeof(uint64_t)));
+      attr = true;
+    }
+    rowsort_warp_kernel<<<(unsigned)((pk + warps - 1) / warps), warps * 32, smem, st>>>(
+        pk, c_ptr, keys, long_rows);
+    rowsort_block_kernel<<<148, 1024, kBlockSortMax * sizeof(uint64_t), st>>>(
+        c_ptr, keys, keys_tmp, long_rows);
+    launches += 2;
+  }
+  if (dtype == ACCORD_F64)
+    gather_kernel<double><<<148 * 8, 256, 0, st>>>(pk, c_ptr, keys, (const double*)pool.g,
+                                                   (const double*)pool.w, c_col, (double*)c_g,
+                                                   (double*)c_w);
+  else
+    gather_kernel<float><<<148 * 8, 256, 0, st>>>(pk, c_ptr, keys, (const float*)pool.g,
+                                                  (const float*)pool.w, c_col, (float*)c_g,
+                                                  (float*)c_w);
+  return launches + 1;
+}
+
+int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                const void* c_g, const void* c_w, void* c_wn, double tau, double lam,
+                double* row_dd, double* row_l1, double* row_logd, int32_t* row_nnz,
+                cudaStream_t st) {
+  const int warps = 8;
+  const unsigned g = (unsigned)((pk + warps - 1) / warps);
+  if (dtype == ACCORD_F64)
+    prox_kernel<double><<<g, warps * 32, 0, st>>>(pk, r0, c_ptr, c_col, (const double*)c_g,
+                                                  (const double*)c_w, (double*)c_wn, tau, lam,
+                                                  row_dd, row_l1, row_logd, row_nnz);
+  else
+    prox_kernel<float><<<g, warps * 32, 0, st>>>(pk, r0, c_ptr, c_col, (const float*)c_g,
+                                                 (const float*)c_w, (float*)c_wn, tau, lam,
+                                                 row_dd, row_l1, row_logd, row_nnz);
+  return 1;
+}
+
+int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* ptr,
+                const int32_t* col, const void* wn, const void* wo, const void* Xt, void* Yout,
+                __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
+                double* row_D2, double* row_Y2, cudaStream_t st) {
+  const int V = dtype == ACCORD_F64 ? 2 : 4;
+  int threads = (int)std::min<int64_t>(kSpmmMaxThreads, round_up(ldk / V, 32));
+  if (pk == 0) return 0;
+  if (dtype == ACCORD_F64) {
+    spmm_kernel<double, false><<<(unsigned)pk, threads, 0, st>>>(
+        pk, n, ldk, ptr, col, (const double*)wn, (const double*)wo, (const double*)Xt,
+        (double*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2);
+  } else if (Yhi) {
+    spmm_kernel<float, true><<<(unsigned)pk, threads, 0, st>>>(
+        pk, n, ldk, ptr, col, (const float*)wn, (const float*)wo, (const float*)Xt,
+        (float*)Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2);
+  } else {
+    spmm_kernel<float, false><<<(unsigned)pk, threads, 0, st>>>(
+        pk, n, ldk, ptr, col, (const float*)wn, (const float*)wo, (const float*)Xt,
+        (float*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2);
+  }
+  return 1;
+}
+
+int launch_refine(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
+                  const float* Y, const float* Xt, float* c_g, cudaStream_t st) {
+  if (pk == 0) return 0;
+  refine_kernel<<<(unsigned)pk, 256, 0, st>>>(pk, n, ldk, c_ptr, c_col, Y, Xt, c_g);
+  return 1;
+}
+
+int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st) {
+  col_norms_kernel<<<(unsigned)((p + 7) / 8), 256, 0, st>>>(p, ldk, Xt, col_sd);
+  return 1;
+}
+
+int launch_omega_stats(int dtype, int64_t pk, int64_t r0, const int64_t* ptr, const int32_t* col,
+                       const void* val, double* row_l1, double* row_logd, int32_t* row_nnz,
+                       int32_t* bad_diag, cudaStream_t st) {
+  const int warps = 8;
+  const unsigned g = (unsigned)((pk + warps - 1) / warps);
+  if (dtype == ACCORD_F64)
+    omega_stats_kernel<double><<<g, warps * 32, 0, st>>>(pk, r0, ptr, col, (const double*)val,
+                                                         row_l1, row_logd, row_nnz, bad_diag);
+  else
+    omega_stats_kernel<float><<<g, warps * 32, 0, st>>>(pk, r0, ptr, col, (const float*)val,
+                                                        row_l1, row_logd, row_nnz, bad_diag);
+  return 1;
+}
+
+int launch_reduce_rows(int64_t pk, const double* row_D2, const double* row_dd,
+                       const double* row_logd, const double* row_Y2, const double* row_l1,
+                       const int32_t* row_nnz, const int64_t* c_ptr, double* out,
+                       cudaStream_t st) {
+  reduce_rows_kernel<<<1, 1024, 0, st>>>(pk, row_D2, row_dd, row_logd, row_Y2, row_l1, row_nnz,
+                                         c_ptr, out);
+  return 1;
+}
+
+int launch_compact(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                   const void* c_wn, const int64_t* om_ptr, int32_t* om_col, void* om_val,
+                   cudaStream_t st) {
+  const int warps = 8;
+  const unsigned g = (unsigned)((pk + warps - 1) / warps);
+  if (dtype == ACCORD_F64)
+    compact_kernel<double><<<g, warps * 32, 0, st>>>(pk, r0, c_ptr, c_col, (const double*)c_wn,
+                                                     om_ptr, om_col, (double*)om_val);
+  else
+    compact_kernel<float><<<g, warps * 32, 0, st>>>(pk, r0, c_ptr, c_col, (const float*)c_wn,
+                                                    om_ptr, om_col, (float*)om_val);
+  return 1;
+}
+
+int launch_identity(int dtype, int64_t pk, int64_t r0, int64_t* om_ptr, int32_t* om_col,
+                    void* om_val, cudaStream_t st) {
+  if (dtype == ACCORD_F64)
+    identity_kernel<double><<<grid_for(pk + 1, 256), 256, 0, st>>>(pk, r0, om_ptr, om_col,
+                                                                   (double*)om_val);
+  else
+    identity_kernel<float><<<grid_for(pk + 1, 256), 256, 0, st>>>(pk, r0, om_ptr, om_col,
+                                                                  (float*)om_val);
+  return 1;
+}
+
+int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk, int max_iter,
+                    double tol, double* L_host, cudaStream_t st, std::string* err) {
+  int launches = 0;
+  const int64_t nsplit = std::min<int64_t>(256, std::max<int64_t>(1, p / 256));
+  const int64_t rows_per = (p + nsplit - 1) / nsplit;
+  double *v = nullptr, *w = nullptr, *u = nullptr, *part = nullptr, *dots = nullptr;
+  cudaError_t e = cudaSuccess;
+  e = cudaMallocAsync(&v, p * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&w, p * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&u, ldk * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&part, nsplit * ldk * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dots, 2 * sizeof(double), st);
+  if (e != cudaSuccess) {
+    *err = std::string("power iteration alloc: ") + cudaGetErrorString(e);
+    return -1;
+  }
+  fill_d<<<grid_for(p, 256), 256, 0, st>>>(v, p, 1.0 / std::sqrt((double)p));
+  ++launches;
+  double rq_prev = -1.0, rq = 0.0, h[2];
+  const int check_every = 10;
+  for (int it = 0; it < max_iter; ++it) {
+    dim3 g1((unsigned)((ldk + 255) / 256), (unsigned)nsplit);
+    if (dtype == ACCORD_F64)
+      pi_xv_kernel<double><<<g1, 256, 0, st>>>((const double*)Xt, p, ldk, rows_per, v, part);
+    else
+      pi_xv_kernel<float><<<g1, 256, 0, st>>>((const float*)Xt, p, ldk, rows_per, v, part);
+    pi_sum_parts<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(part, nsplit, ldk, u);
+    const unsigned g3 = (unsigned)((p + 7) / 8);
+    if (dtype == ACCORD_F64)
+      pi_xtu_kernel<double><<<g3, 256, 0, st>>>((const double*)Xt, p, ldk, n, u, w);
+    else
+      pi_xtu_kernel<float><<<g3, 256, 0, st>>>((const float*)Xt, p, ldk, n, u, w);
+    pi_dots<<<1, 1024, 0, st>>>(v, w, p, dots);
+    pi_normalize<<<grid_for(p, 256), 256, 0, st>>>(w, p, dots, v);
+    launches += 5;
+    if ((it + 1) % check_every == 0 || it + 1 == max_iter) {
+      cudaMemcpyAsync(h, dots, sizeof(h), cudaMemcpyDeviceToHost, st);
+      e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) break;
+      rq = h[0];
+      if (rq_prev > 0 && std::fabs(rq - rq_prev) <= tol * rq) break;
+      rq_prev = rq;
+    }
+  }
+  if (e == cudaSuccess) {
+    cudaMemcpyAsync(h, dots, sizeof(h), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    rq = h[0];
+  }
+  cudaFreeAsync(v, st);
+  cudaFreeAsync(w, st);
+  cudaFreeAsync(u, st);
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(dots, st);
+  if (e != cudaSuccess) {
+    *err = std::string("power iteration: ") + cudaGetErrorString(e);
+    return -1;
+  }
+  *L_host = rq;
+  return launches;
+}
+
+}  // namespace accord

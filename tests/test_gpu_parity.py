@@ -1,0 +1,130 @@
+"""GPU parity: the CUDA path through the C ABI vs the float64 oracle on the
+same seeded inputs (BASELINE.json configs 1-2 in full; small cases of the
+same recipes spanning several tiles and ragged tails)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from accord_inputs import make_problem, get_config   # noqa: E402
+from oracle import accord_oracle as O                 # noqa: E402
+from tests.parity_util import compare_full            # noqa: E402
+import paper_2412_11554_b200 as A                     # noqa: E402
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+
+
+def run_gpu(Xt, lam, T, inv_L, gemm, layout="variables", tau0=0.5, beta=0.5, **kw):
+    X = torch.from_numpy(Xt if layout == "variables" else np.ascontiguousarray(Xt.T)).cuda()
+    with A.AccordSolver(X, lam, layout=layout, tau0=tau0, beta=beta, inv_L=inv_L, gemm=gemm,
+                        **kw) as s:
+        stats = s.step(T)
+        csr = s.export_csr()
+        info = s.info()
+    return csr, stats, info
+
+
+@pytest.mark.parametrize("key", ["t_chain", "t_ba_f64", 1])
+def test_parity_f64_simt(key):
+    _cuda()
+    pr = make_problem(key)
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    for lam in c.lambdas:
+        csr, stats, info = run_gpu(pr.Xt, lam, c.T, inv_L, A.GEMM_SIMT)
+        assert info["gemm"] == A.GEMM_SIMT and info["dtype"] == A.F64
+        rep = compare_full(pr.Xt, lam, c.T, inv_L, csr.to_dense(c.p), stats, "f64")
+        assert not rep["replayed"]
+
+
+@pytest.mark.parametrize("gemm", [A.GEMM_SIMT, A.GEMM_BF16X3, A.GEMM_BF16_FILTER])
+@pytest.mark.parametrize("key", ["t_ba_f32", "t_hubs_f32"])
+def test_parity_f32_small(key, gemm):
+    _cuda()
+    pr = make_problem(key)
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    csr, stats, info = run_gpu(pr.Xt, c.lambdas[0], c.T, inv_L, gemm)
+    assert info["gemm"] == gemm
+    compare_full(pr.Xt, c.lambdas[0], c.T, inv_L, csr.to_dense(c.p), stats, "f32")
+
+
+@pytest.mark.parametrize("lam", [0.05, 0.1, 0.2])
+def test_parity_config2_full(lam):
+    """BASELINE config 2 (p=2000, n=500, f32, BA tree), 100 iterations, all lambdas."""
+    _cuda()
+    pr = make_problem(2)
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    csr, stats, info = run_gpu(pr.Xt, lam, c.T, inv_L, A.GEMM_AUTO)
+    assert info["gemm"] == A.GEMM_BF16_FILTER
+    compare_full(pr.Xt, lam, c.T, inv_L, csr.to_dense(c.p), stats, "f32")
+
+
+def test_sample_major_layout_matches_variable_major():
+    _cuda()
+    pr = make_problem("t_ba_f64")
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    a, sa, _ = run_gpu(pr.Xt, 0.1, 5, inv_L, A.GEMM_SIMT, layout="variables")
+    b, sb, _ = run_gpu(pr.Xt, 0.1, 5, inv_L, A.GEMM_SIMT, layout="samples")
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col, b.col)
+    assert np.array_equal(a.val, b.val)
+
+
+def test_objective_at_identity_and_export_invariants():
+    _cuda()
+    pr = make_problem("t_ba_f32")
+    X = torch.from_numpy(pr.Xt).cuda()
+    lam = 0.1
+    with A.AccordSolver(X, lam, inv_L=0.0) as s:
+        f0, parts = s.objective()
+        Xd = pr.Xt.astype(np.float64)
+        want = (Xd * Xd).sum() / (2 * pr.cfg.n) + lam * pr.cfg.p
+        assert abs(f0 - want) <= 1e-6 * want
+        info = s.info()
+        L = O.spectral_bound(pr.Xt)
+        assert L <= info["L"] <= L * 1.01      # device power iteration, safe side
+        s.step(3)
+        csr = s.export_csr()
+    p = pr.cfg.p
+    for i in range(p):
+        cols = csr.col[csr.row_ptr[i]:csr.row_ptr[i + 1]]
+        vals = csr.val[csr.row_ptr[i]:csr.row_ptr[i + 1]]
+        assert np.all(np.diff(cols) > 0)
+        assert i in cols and vals[list(cols).index(i)] > 0
+        assert np.all((vals != 0) | (cols == i))
+
+
+def test_warm_start_roundtrip():
+    _cuda()
+    pr = make_problem("t_ba_f64")
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    X = torch.from_numpy(pr.Xt).cuda()
+    with A.AccordSolver(X, 0.1, inv_L=inv_L, gemm=A.GEMM_SIMT) as s:
+        s.step(4)
+        mid = s.export_csr()
+        s.step(3)
+        end = s.export_csr()
+    with A.AccordSolver(X, 0.1, inv_L=inv_L, gemm=A.GEMM_SIMT) as s2:
+        s2.set_omega_csr(mid.row_ptr, mid.col, mid.val)
+        s2.step(3)
+        end2 = s2.export_csr()
+    assert np.array_equal(end.col, end2.col) and np.allclose(end.val, end2.val, rtol=0,
+                                                              atol=1e-13)
+
+
+def test_errors_are_loud():
+    _cuda()
+    X = torch.zeros((10, 5), dtype=torch.float32).cuda()
+    with pytest.raises(A.AccordError):
+        A.AccordSolver(X, -1.0)
+    Xn = torch.ones((10, 5), dtype=torch.float32)
+    Xn[3, 2] = float("nan")
+    with pytest.raises(A.AccordError) as e:
+        A.AccordSolver(Xn.cuda(), 0.1)
+    assert "row 3, col 2" in str(e.value)
