@@ -143,6 +143,7 @@ typedef struct {
   float ms_spmm;      /* SpMM kernels, all trials */
   float ms_reduce;    /* reductions + collectives + host decision, all trials */
   float ms_total;     /* whole iteration */
+  int64_t max_row_cand; /* longest candidate row of this rank (diagnostic) */
 } accord_iter_stats;
 
 typedef struct {

@@ -62,6 +62,7 @@ class IterStats(C.Structure):
         ("ms_gemm", C.c_float), ("ms_finalize", C.c_float), ("ms_refine", C.c_float),
         ("ms_prox", C.c_float),
         ("ms_spmm", C.c_float), ("ms_reduce", C.c_float), ("ms_total", C.c_float),
+        ("max_row_cand", C.c_int64),
     ]
 
     def as_dict(self):

@@ -30,8 +30,9 @@ struct PoolView {             // candidate pool written by the GEMM epilogue (un
   int32_t* col;               // global column
   void* g;                    // T: [Omega S]_ik
   void* w;                    // T: omega_ik^{(t)} (0 if absent)
-  int64_t cap;                // capacity in entries
-  unsigned long long* cursor; // number of entries emitted (may exceed cap)
+  int64_t seg_cap;            // entries per segment; segment s = [s*seg_cap, (s+1)*seg_cap)
+  int64_t nseg;               // segments (one per persistent GEMM CTA; 1 for the SIMT GEMM)
+  unsigned long long* seg_cnt;// [nseg] entries emitted per segment (may exceed seg_cap)
   int32_t* row_cnt;           // [pk] entries emitted per row
 };
 
@@ -106,7 +107,8 @@ int launch_omega_stats(int dtype, int64_t pk, int64_t r0, const int64_t* ptr,
                        int32_t* row_nnz, int32_t* bad_diag, cudaStream_t st);
 
 // Fixed-order reduction of the per-row partials into out[8] =
-// {D2, dd, logd, Y2, l1, nnz, ncand, 0}. Any pointer may be NULL (-> 0).
+// {D2, dd, logd, Y2, l1, nnz, ncand, max candidates in a row}. Any pointer may
+// be NULL (-> 0).
 int launch_reduce_rows(int64_t pk, const double* row_D2, const double* row_dd,
                        const double* row_logd, const double* row_Y2, const double* row_l1,
                        const int32_t* row_nnz, const int64_t* c_ptr, double* out,
@@ -134,6 +136,9 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            const __nv_bfloat16* Xlo, int64_t p_pad, int64_t ldk,
                            std::string* err);
 void tc_plan_destroy(TcGemmPlan*);
+// per-256-column maxima of the filter's column constants (after launch_col_norms)
+int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st);
+int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs (= pool segments)
 int launch_gemm_tc(TcGemmPlan* plan, int mode /* accord_gemm: BF16X3 or BF16_FILTER */,
                    int ybuf, int64_t kdim, int sm_count, const EpiParams& ep,
                    const OmegaView& om, const PoolView& pool, cudaStream_t st);

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -119,7 +120,8 @@ struct accord_ctx {
   int32_t *pool_row = nullptr, *pool_col = nullptr;
   void *pool_g = nullptr, *pool_w = nullptr;
   int32_t *row_cnt = nullptr, *rcur = nullptr, *long_rows = nullptr;
-  unsigned long long* cursor = nullptr;
+  unsigned long long* seg_cnt = nullptr;   // [max(sm_count, 1)] pool fill per segment
+  int64_t nseg = 1;
   double *row_D2 = nullptr, *row_Y2 = nullptr, *row_dd = nullptr, *row_l1 = nullptr,
          *row_logd = nullptr;
   int32_t* row_nnz = nullptr;
@@ -128,10 +130,15 @@ struct accord_ctx {
   void* scan_tmp = nullptr;
   size_t scan_tmp_sz = 0;
   double* h_red = nullptr;                 // pinned [16]
-  unsigned long long* h_cursor = nullptr;  // pinned
+  unsigned long long* h_seg = nullptr;     // pinned [max(sm_count, 1)]
   TcGemmPlan* plan = nullptr;
   cudaEvent_t ev[8] = {};
 
+  // optional per-kernel tracing (ACCORD_TRACE=1): events after each launch,
+  // printed to stderr at the end of every iteration
+  bool trace = false;
+  std::vector<cudaEvent_t> tr_pool;
+  std::vector<std::pair<const char*, cudaEvent_t>> tr_marks;
   int64_t launches = 0, gemm_launches = 0, iters = 0, nnz_local = 0;
   double f = 0, parts[3] = {0, 0, 0};
   std::vector<void*> allocs;
@@ -180,7 +187,8 @@ void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
 OmegaView omega_view(accord_ctx* c) { return OmegaView{c->om_ptr, c->om_col, c->om_val}; }
 
 PoolView pool_view(accord_ctx* c) {
-  return PoolView{c->pool_row, c->pool_col, c->pool_g, c->pool_w, c->cap, c->cursor, c->row_cnt};
+  return PoolView{c->pool_row, c->pool_col, c->pool_g, c->pool_w, c->cap / c->nseg, c->nseg,
+                  c->seg_cnt, c->row_cnt};
 }
 
 // (Re)allocate the entry-indexed arrays for capacity `cap`, preserving Omega.
@@ -314,8 +322,12 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     throw Fail{ACCORD_E_UNSUPPORTED, "BF16_FILTER supports n <= 4096"};
 
   for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  {
+    const char* t = std::getenv("ACCORD_TRACE");
+    c->trace = t && t[0] == '1';
+  }
   CK(cudaMallocHost(&c->h_red, 16 * sizeof(double)));
-  CK(cudaMallocHost(&c->h_cursor, sizeof(unsigned long long)));
+  CK(cudaMallocHost(&c->h_seg, std::max(c->sm_count, 1) * sizeof(unsigned long long)));
 
   if (c->comm == ACCORD_COMM_NCCL) {
     NcclApi* api = nccl_api();
@@ -361,10 +373,12 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   } else {
     double L = 0;
     std::string e;
-    int l = power_iteration(c->dtype, c->Xt, c->p, c->n, c->ldk, 3000, 1e-10, &L, c->st, &e);
+    // power iteration from the all-ones start, relative tolerance,
+    // then a safety inflation (overestimating L is safe, underestimating is not)
+    int l = power_iteration(c->dtype, c->Xt, c->p, c->n, c->ldk, 600, 1e-8, &L, c->st, &e);
     if (l < 0) throw Fail{ACCORD_E_CUDA, e};
     c->launches += l;
-    c->L = L * (1.0 + 1e-3);  // safe overestimate
+    c->L = L * (1.0 + 2e-3);
     c->inv_L = c->L > 0 ? 1.0 / c->L : 1e300;
   }
 
@@ -403,6 +417,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
                              x3 ? c->Ylo[1] : c->Yhi[1], c->pk_pad, c->Xhi,
                              x3 ? c->Xlo : c->Xhi, c->p_pad, c->ldk, &e);
     if (!c->plan) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
+    if (filt) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
   }
 
   // ---- per-row and entry-indexed state ----
@@ -411,7 +426,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->row_cnt = c->dalloc<int32_t>(c->pk);
   c->rcur = c->dalloc<int32_t>(c->pk);
   c->long_rows = c->dalloc<int32_t>(c->pk + 1);
-  c->cursor = c->dalloc<unsigned long long>(1);
+  c->seg_cnt = c->dalloc<unsigned long long>(std::max(c->sm_count, 1));
+  c->nseg = c->plan ? tc_grid_size(c->plan, c->sm_count) : 1;
   c->row_D2 = c->dalloc<double>(c->pk);
   c->row_Y2 = c->dalloc<double>(c->pk);
   c->row_dd = c->dalloc<double>(c->pk);
@@ -453,6 +469,32 @@ accord_status guard(accord_ctx* c, F&& fn) {
   }
 }
 
+void TR(accord_ctx* c, const char* name) {
+  if (!c->trace) return;
+  if (c->tr_marks.size() >= c->tr_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->tr_pool.push_back(e);
+  }
+  cudaEvent_t e = c->tr_pool[c->tr_marks.size()];
+  CK(cudaEventRecord(e, c->st));
+  c->tr_marks.emplace_back(name, e);
+}
+
+void TR_flush(accord_ctx* c) {
+  if (!c->trace || c->tr_marks.empty()) return;
+  CK(cudaEventSynchronize(c->tr_marks.back().second));
+  std::fprintf(stderr, "[accord trace] it=%lld maxrow=%.0f ncand=%.0f", (long long)c->iters,
+               c->h_red[7], c->h_red[6]);
+  for (size_t i = 1; i < c->tr_marks.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->tr_marks[i - 1].second, c->tr_marks[i].second);
+    std::fprintf(stderr, " %s=%.3f", c->tr_marks[i].first, ms);
+  }
+  std::fprintf(stderr, "\n");
+  c->tr_marks.clear();
+}
+
 float ev_ms(accord_ctx* c, int a, int b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]);
@@ -463,10 +505,11 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   accord_iter_stats st{};
   cudaStream_t S = c->st;
   CK(cudaEventRecord(c->ev[0], S));
+  TR(c, "start");
   // ---------------- a2 + a3: gradient GEMM with the fused epilogue --------
   for (;;) {
     CK(cudaMemsetAsync(c->row_cnt, 0, c->pk * 4, S));
-    CK(cudaMemsetAsync(c->cursor, 0, 8, S));
+    CK(cudaMemsetAsync(c->seg_cnt, 0, c->nseg * 8, S));
     EpiParams ep{};
     ep.pk = c->pk;
     ep.p = c->p;
@@ -480,30 +523,47 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
     ep.gamma = (float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
     CK(cudaEventRecord(c->ev[1], S));
     if (c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER)
-      c->launches += launch_gemm_tc(c->plan, c->gemm, c->cur, c->ldk, c->sm_count, ep,
-                                    omega_view(c), pool_view(c), S);
+    {
+      const int l = launch_gemm_tc(c->plan, c->gemm, c->cur, c->ldk, c->sm_count, ep,
+                                   omega_view(c), pool_view(c), S);
+      if (l < 0) throw Fail{ACCORD_E_CUDA, "GEMM grid / pool segment mismatch"};
+      c->launches += l;
+    }
     else
       c->launches += launch_gemm_simt(c->dtype, c->Y[c->cur], c->Xt, c->ldk, c->ldk, ep,
                                       omega_view(c), pool_view(c), S);
     c->gemm_launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], S));
-    CK(cudaMemcpyAsync(c->h_cursor, c->cursor, 8, cudaMemcpyDeviceToHost, S));
+    TR(c, "gemm");
+    CK(cudaMemcpyAsync(c->h_seg, c->seg_cnt, c->nseg * 8, cudaMemcpyDeviceToHost, S));
     CK(cudaStreamSynchronize(S));
     st.ms_gemm += ev_ms(c, 1, 2);
-    const int64_t need = (int64_t)*c->h_cursor;
-    if (need <= c->cap) break;
-    if (need >= (int64_t)UINT32_MAX)
-      throw Fail{ACCORD_E_NOMEM, "candidate set exceeds 2^32 entries"};
-    grow(c, std::min<int64_t>((int64_t)UINT32_MAX - 1, need + need / 4 + 1024), c->nnz_local);
+    int64_t need_seg = 0, total = 0;
+    for (int64_t q = 0; q < c->nseg; ++q) {
+      need_seg = std::max<int64_t>(need_seg, (int64_t)c->h_seg[q]);
+      total += (int64_t)c->h_seg[q];
+    }
+    if (need_seg <= c->cap / c->nseg) break;
+    // a pool segment overflowed: grow (every segment to the largest need) and redo
+    const int64_t want = (need_seg + need_seg / 4 + 1024) * c->nseg;
+    if (want >= (int64_t)UINT32_MAX)
+      throw Fail{ACCORD_E_NOMEM, "candidate pool exceeds 2^32 entries"};
+    grow(c, std::max(want, total), c->nnz_local);
   }
   // ---------------- a4: finalize C ----------------
+  TR(c, "host_gap");
   c->launches += launch_scan_i32(c->row_cnt, c->c_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
+  TR(c, "scan");
   CK(cudaMemsetAsync(c->rcur, 0, c->pk * 4, S));
   CK(cudaMemsetAsync(c->long_rows, 0, 4, S));
-  c->launches += launch_finalize(c->dtype, c->pk, pool_view(c), c->c_ptr, c->rcur, c->keys,
+  TR(c, "memset");
+  PoolView pv = pool_view(c);
+  if (c->gemm == ACCORD_GEMM_BF16_FILTER) pv.g = nullptr;   // values come from the refine
+  c->launches += launch_finalize(c->dtype, c->pk, pv, c->c_ptr, c->rcur, c->keys,
                                  c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S);
   CK(cudaEventRecord(c->ev[3], S));
+  TR(c, "finalize");
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) {
     // exact values of the filtered candidates: G_ik = <Y_i, X_k> / n (f64 accumulation)
     c->launches += launch_refine(c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
@@ -511,6 +571,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
                                  (float*)c->c_g, S);
   }
   CK(cudaEventRecord(c->ev[4], S));
+  TR(c, "refine");
   CK(cudaEventSynchronize(c->ev[4]));
   st.ms_finalize = ev_ms(c, 2, 3);
   st.ms_refine = ev_ms(c, 3, 4);
@@ -525,15 +586,18 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
                                c->c_wn, tau, c->lam, c->row_dd, c->row_l1, c->row_logd,
                                c->row_nnz, S);
     CK(cudaEventRecord(c->ev[5], S));
+    TR(c, "prox");
     c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, c->c_wn,
                                c->c_w, c->Xt, c->Y[nb], c->Yhi[nb], c->Ylo[nb], c->row_A[nb],
                                c->row_B[nb], c->row_D2, c->row_Y2, S);
     CK(cudaEventRecord(c->ev[6], S));
+    TR(c, "spmm");
     c->launches += launch_reduce_rows(c->pk, c->row_D2, c->row_dd, c->row_logd, c->row_Y2,
                                       c->row_l1, c->row_nnz, c->c_ptr, c->red_d, S);
     CK(cudaGetLastError());
     allreduce(c, c->red_d, c->h_red, 8);
     CK(cudaEventRecord(c->ev[7], S));
+    TR(c, "reduce+decide");
     CK(cudaEventSynchronize(c->ev[7]));
     st.ms_prox += ev_ms(c, 4, 5);
     st.ms_spmm += ev_ms(c, 5, 6);
@@ -562,6 +626,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   c->launches += launch_scan_i32(c->row_nnz, c->om_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
   c->launches += launch_compact(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_wn, c->om_ptr,
                                 c->om_col, c->om_val, S);
+  TR(c, "compact");
   c->cur = nb;
   int64_t nnz_loc = 0;
   CK(cudaMemcpyAsync(&nnz_loc, c->om_ptr + c->pk, 8, cudaMemcpyDeviceToHost, S));
@@ -582,7 +647,9 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   st.delta_fro = std::sqrt(r[1]);
   st.nnz = (int64_t)r[5];
   st.n_cand = (int64_t)r[6];
+  st.max_row_cand = (int64_t)r[7];
   st.ms_total = ev_ms(c, 0, 7);
+  TR_flush(c);
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
   if (s) *s = st;
 }
@@ -861,8 +928,9 @@ void accord_destroy(accord_ctx* c) {
   for (void* ptr : c->allocs) cudaFree(ptr);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->tr_pool) cudaEventDestroy(e);
   if (c->h_red) cudaFreeHost(c->h_red);
-  if (c->h_cursor) cudaFreeHost(c->h_cursor);
+  if (c->h_seg) cudaFreeHost(c->h_seg);
   if (c->nccl && nccl_api()) nccl_api()->CommDestroy(c->nccl);
   delete c;
 }

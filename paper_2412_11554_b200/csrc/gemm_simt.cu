@@ -86,9 +86,9 @@ gemm_simt_kernel(const T* __restrict__ Y, const T* __restrict__ Xt, int64_t ldk,
       const T w = lookup_omega<T>(om, r, (int32_t)k);
       const bool emit = (k == gi) || (w != T(0)) || (fabs((double)g) > ep.lam_cand);
       if (!emit) continue;
-      const unsigned long long pos = atomicAdd(pool.cursor, 1ull);
+      const unsigned long long pos = atomicAdd(&pool.seg_cnt[0], 1ull);   // one segment
       ++cnt;
-      if ((int64_t)pos < pool.cap) {
+      if ((int64_t)pos < pool.seg_cap) {
         pool.row[pos] = (int32_t)r;
         pool.col[pos] = (int32_t)k;
         ((T*)pool.g)[pos] = g;

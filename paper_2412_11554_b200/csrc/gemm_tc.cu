@@ -1,29 +1,40 @@
 // tcgen05 gradient GEMM with the fused candidate epilogue (SURVEY.md §8(a)
-// rows a2 + a3), sm_100a.
+// rows a2 + a3), sm_100a, CTA pairs (cta_group::2).
 //
-//   G_k = Y_k X / n,  Y_k = Omega_{R_k} X^T  (two-step gradient)
+//   G_k = Y_k X / n,  Y_k = Omega_{R_k} X^T   (two-step gradient)
 //
-// Precision: Y and X^T are each split once into bf16 pairs
-// hi = bf16(v), lo = bf16(v - hi); the tensor cores accumulate
-//   hi*hi + hi*lo + lo*hi      (3 x kind::f16 MMAs, fp32 accumulator in TMEM)
-// which carries ~16 significant bits per operand product instead of 8; the
-// dropped lo*lo term is <= 2^-16 relative. Measured against the float64
-// oracle this is fp32-grade, which the 1e-5 parity budget needs (single-pass
-// bf16 or tf32 is not).
+// Both operands are K-major (Y rows and X^T rows, K = n samples), so the
+// product is a plain "TN" GEMM: D[i,k] = sum_m Y[i,m] Xt[k,m].
 //
-// Structure: persistent kernel, one 128 x 256 output tile per step, 8 warps:
-//   warp 0   TMA producer (lane 0): A_hi, A_lo (Y rows), B_hi, B_lo (X^T rows)
-//            into a 2-stage SMEM ring (SWIZZLE_128B, 96 KB / stage)
-//   warp 1   MMA issuer (lane 0): 4 k-steps x 3 MMAs (M128 N256 K16) per stage
-//   warp 2   TMEM allocator (512 columns = 2 accumulator stages)
-//   warps 4-7 epilogue: TMEM -> registers (32x32b.x32), candidate rule, warp
-//            ballot/prefix compaction into the candidate pool. The p x p
-//            gradient never reaches HBM. The epilogue of tile t overlaps the
-//            mainloop of tile t+1 (double-buffered accumulator).
+// Two arithmetic modes:
+//   kMode 1, BF16_FILTER (default): one bf16 MMA pass; the epilogue emits
+//     (i,k) when |acc| > n*lambda - n*delta_ik, with n*delta_ik a rigorous
+//     bound on |acc - n*G_ik| (bf16 rounding of both operands by
+//     Cauchy-Schwarz on the actual rounding-error vectors, plus the fp32
+//     accumulation). The candidate values are then recomputed exactly by the
+//     refine SDDMM (kernels.cu), so no candidate can be missed and every value
+//     is float64-accumulated.
+//   kMode 0, BF16X3: operands split hi = bf16(v), lo = bf16(v - hi); three
+//     MMA passes hi*hi + hi*lo + lo*hi into the same fp32 accumulator; values
+//     come from TMEM (relative product error ~2^-16).
+//
+// Structure (persistent, one 256 x 256 tile per CTA pair per step):
+//   cluster of 2 CTAs; CTA r holds rows [128r, 128r+128) of the A tile (Y)
+//   and rows [128r, 128r+128) of the B tile (X^T); the leader (r = 0) issues
+//   tcgen05.mma.cta_group::2 (M256 N256 K16), whose accumulator lands half in
+//   each CTA's TMEM (lane = row).
+//   warp 0  TMA producer (both CTAs; the bytes are credited to the leader's
+//           full barrier), SWIZZLE_128B, kStages-deep ring
+//   warp 1  MMA issuer (leader only), commits multicast to both CTAs
+//   warp 2  TMEM allocator (512 columns = 2 accumulator stages)
+//   warps 4-7 epilogue (both CTAs): TMEM -> registers (32x32b), candidate
+//           rule, warp prefix-sum compaction into the candidate pool, one
+//           atomicAdd per warp-chunk. The p x p gradient never reaches HBM;
+//           the epilogue of tile t overlaps the mainloop of tile t+1.
 //
 // Epilogue rule (derived from Eq. 3.5): emit
-// (i, k, g = acc / n, omega_ik) iff k == i, or (i,k) in supp Omega (found by a
-// merge walk of the thread's sorted CSR row), or |acc| > lam_cand * n.
+// (i, k, g, omega_ik) iff k == i, or (i,k) in supp Omega (merge walk of the
+// thread's sorted CSR row), or the |G| > lambda test above passes.
 #include "accord_internal.h"
 #include "tc_ptx.cuh"
 
@@ -37,21 +48,22 @@ namespace accord {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64;     // BK in bf16 elements = 128 B rows
+constexpr int BM = 128;                         // rows of A per CTA (256 per pair)
+constexpr int BN = 256;                         // columns of the tile (N of one MMA)
+constexpr int BNH = BN / 2;                     // rows of B held per CTA
+constexpr int BK = 64;                          // bf16 elements = 128-B rows
 constexpr int kAccStages = 2;
 constexpr int kTmemCols = 512;
-constexpr uint32_t kTileA = BM * BK * 2;       // 16 KB
-constexpr uint32_t kTileB = BN * BK * 2;       // 32 KB
+constexpr uint32_t kTileA = BM * BK * 2;        // 16 KB
+constexpr uint32_t kTileB = BNH * BK * 2;       // 16 KB
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
-constexpr int kGroupM = 16;                    // M-blocks per raster group (L2 reuse)
+constexpr int kGroupM = 16;                     // M-blocks per raster group (L2 reuse)
 
-// kMode 0 = BF16X3 (hi/lo operands, 3 MMAs per k-step, values from TMEM)
-// kMode 1 = BF16_FILTER (hi operands only, 1 MMA per k-step, certified filter)
 template <int kMode> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
-  static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 96 / 48 KB
-  static constexpr int kStages = kMode == 0 ? 2 : 4;
+  static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 64 / 32 KB
+  static constexpr int kStages = kMode == 0 ? 3 : 6;
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
 };
 
@@ -67,67 +79,77 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int num_m, int num_n) {
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
-                   const __grid_constant__ CUtensorMap mA_lo,
-                   const __grid_constant__ CUtensorMap mB_hi,
-                   const __grid_constant__ CUtensorMap mB_lo, int num_kb, int num_m, int num_n,
-                   EpiParams ep, OmegaView om, PoolView pool) {
+               const __grid_constant__ CUtensorMap mA_lo,
+               const __grid_constant__ CUtensorMap mB_hi,
+               const __grid_constant__ CUtensorMap mB_lo, int num_kb, int num_m, int num_n,
+               EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
+               PoolView pool) {
   constexpr int kStages = Cfg<kMode>::kStages;
   constexpr uint32_t kStageBytes = Cfg<kMode>::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for SWIZZLE_128B atoms
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + kStages * kStageBytes);
-  uint64_t* full = bars;                         // [kStages]
-  uint64_t* empty = bars + kStages;              // [kStages]
-  uint64_t* tfull = bars + 2 * kStages;          // [kAccStages]
-  uint64_t* tempty = bars + 2 * kStages + kAccStages;
+  uint64_t* full = bars;                          // [kStages]   (leader's is used)
+  uint64_t* empty = bars + kStages;               // [kStages]   (each CTA's own)
+  uint64_t* tfull = bars + 2 * kStages;           // [kAccStages] (each CTA's own)
+  uint64_t* tempty = bars + 2 * kStages + kAccStages;   // (leader's is used)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kStages + 2 * kAccStages);
+  unsigned long long* seg_cur = (unsigned long long*)(tmem_slot + 2);   // this CTA's pool cursor
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
   const int num_tiles = num_m * num_n;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&mA_hi);
-    tc::tma_prefetch(&mA_lo);
     tc::tma_prefetch(&mB_hi);
-    tc::tma_prefetch(&mB_lo);
+    if (kMode == 0) {
+      tc::tma_prefetch(&mA_lo);
+      tc::tma_prefetch(&mB_lo);
+    }
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(tc::smem_u32(&full[s]), 1);
       tc::mbar_init(tc::smem_u32(&empty[s]), 1);
     }
     for (int a = 0; a < kAccStages; ++a) {
       tc::mbar_init(tc::smem_u32(&tfull[a]), 1);
-      tc::mbar_init(tc::smem_u32(&tempty[a]), 4);   // one arrive per epilogue warp
+      tc::mbar_init(tc::smem_u32(&tempty[a]), 8);   // 4 epilogue warps x 2 CTAs
     }
     tc::fence_mbar_init();
+    *seg_cur = 0;
   }
-  if (warp == 2) tc::tmem_alloc<kTmemCols, 1>(tc::smem_u32(tmem_slot));
+  if (warp == 2) tc::tmem_alloc<kTmemCols, 2>(tc::smem_u32(tmem_slot));
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ============================ TMA producer ============================
+    // ============================ TMA producer (both CTAs) ================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = cluster; t < num_tiles; t += nclusters) {
         const TileCoord tc_ = tile_coord(t, num_m, num_n);
+        const int ya = tc_.m * (2 * BM) + (int)rank * BM;
+        const int yb = tc_.n * BN + (int)rank * BNH;
         for (int kb = 0; kb < num_kb; ++kb) {
           tc::mbar_wait(tc::smem_u32(&empty[stage]), phase ^ 1);
           uint8_t* s = smem + stage * kStageBytes;
-          const uint32_t fb = tc::smem_u32(&full[stage]);
-          tc::mbar_arrive_expect_tx(fb, kStageBytes);
+          const uint32_t fb_local = tc::smem_u32(&full[stage]);
+          if (leader) tc::mbar_arrive_expect_tx(fb_local, 2 * kStageBytes);   // both CTAs' bytes
+          const uint32_t fb = tc::mapa_shared(fb_local, 0);                  // leader's barrier
           const int kx = kb * BK;
           // stage layout: A_hi | B_hi | (A_lo | B_lo)
-          tc::tma_load_2d(tc::smem_u32(s), &mA_hi, fb, kx, tc_.m * BM);
-          tc::tma_load_2d(tc::smem_u32(s + kTileA), &mB_hi, fb, kx, tc_.n * BN);
+          tc::tma_load_2d_cg2(tc::smem_u32(s), &mA_hi, fb, kx, ya);
+          tc::tma_load_2d_cg2(tc::smem_u32(s + kTileA), &mB_hi, fb, kx, yb);
           if constexpr (kMode == 0) {
-            tc::tma_load_2d(tc::smem_u32(s + kTileA + kTileB), &mA_lo, fb, kx, tc_.m * BM);
-            tc::tma_load_2d(tc::smem_u32(s + 2 * kTileA + kTileB), &mB_lo, fb, kx, tc_.n * BN);
+            tc::tma_load_2d_cg2(tc::smem_u32(s + kTileA + kTileB), &mA_lo, fb, kx, ya);
+            tc::tma_load_2d_cg2(tc::smem_u32(s + 2 * kTileA + kTileB), &mB_lo, fb, kx, yb);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -135,14 +157,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ============================ MMA issuer ==============================
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+    // ============================ MMA issuer (leader) =====================
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(2 * BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = cluster; t < num_tiles; t += nclusters) {
         tc::mbar_wait(tc::smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * BN);
@@ -158,38 +180,41 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 = 32 B along K
             const uint32_t accum = (kb | kk) != 0;
-            tc::mma_bf16<1>(d, a_hi + off, b_hi + off, idesc, accum);
+            tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
             if constexpr (kMode == 0) {
-              tc::mma_bf16<1>(d, a_hi + off, b_lo + off, idesc, 1);
-              tc::mma_bf16<1>(d, a_lo + off, b_hi + off, idesc, 1);
+              tc::mma_bf16<2>(d, a_hi + off, b_lo + off, idesc, 1);
+              tc::mma_bf16<2>(d, a_lo + off, b_hi + off, idesc, 1);
             }
           }
-          tc::mma_commit(tc::smem_u32(&empty[stage]));
+          tc::mma_commit_mc(tc::smem_u32(&empty[stage]), 0x3);   // free the slot in both CTAs
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc::mma_commit(tc::smem_u32(&tfull[acc]));
+        tc::mma_commit_mc(tc::smem_u32(&tfull[acc]), 0x3);       // accumulator ready
         if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
       }
     }
     __syncwarp();
   } else if (warp >= kEpiWarp0) {
-    // ============================ epilogue ================================
+    // ============================ epilogue (both CTAs) ====================
     const int q = warp - kEpiWarp0;                 // TMEM lane quarter (= warp % 4)
-    const float thr = (float)(ep.lam_cand / ep.inv_n);   // |acc| > lam * n
+    const float thr = (float)(ep.lam_cand / ep.inv_n);   // n * lambda
+    const float inv_nf = (float)ep.inv_n;
     const float gam = ep.gamma;
-    const float nf = (float)(1.0 / ep.inv_n);
     const float* omv = (const float*)om.val;
+    const uint32_t tempty_leader = tc::smem_u32(&tempty[0]);
+    const int64_t seg_base = (int64_t)blockIdx.x * pool.seg_cap;   // this CTA's pool segment
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cluster; t < num_tiles; t += nclusters) {
       const TileCoord tc_ = tile_coord(t, num_m, num_n);
-      const int64_t r = (int64_t)tc_.m * BM + q * 32 + lane;     // local row
+      const int64_t r = (int64_t)tc_.m * (2 * BM) + (int64_t)rank * BM + q * 32 + lane;
       const bool row_ok = r < ep.pk;
       const int64_t gi = ep.r0 + r;
       const int n0 = tc_.n * BN;
-      // support walk setup (before waiting: overlaps the mainloop)
+      // support walk setup and per-row filter constants (overlap the mainloop)
       int64_t sp = 0, se = 0;
       int32_t nxt = INT_MAX;
+      float r1 = 0.f, Bn = 0.f, tfast = thr;
       if (row_ok) {
         int64_t lo = om.ptr[r], hi = om.ptr[r + 1];
         se = hi;
@@ -199,96 +224,144 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
         }
         sp = lo;
         nxt = sp < se ? om.col[sp] : INT_MAX;
-      }
-      // BF16_FILTER: n*delta_ik = r1 * s_k + Bn * D_k, a rigorous bound on
-      // |acc - n*G_ik| (bf16 rounding of both operands by Cauchy-Schwarz on
-      // the actual rounding-error vectors, plus fp32 accumulation), inflated
-      // by 1.0625 for the float evaluation of the bound itself.
-      float r1 = 0.f, Bn = 0.f;
-      if (kMode == 1 && row_ok) {
-        const float A = ep.row_A[r], B = ep.row_B[r];
-        r1 = (A + gam * (A + B)) * 1.0625f;
-        Bn = B * 1.0625f;
+        if constexpr (kMode == 1) {
+          // n*delta_ik = r1 * s_k + Bn * D_k, inflated by 1.0625 for the
+          // float evaluation of the bound; tfast uses the tile's max s_k, D_k
+          const float A = ep.row_A[r], B = ep.row_B[r];
+          r1 = (A + gam * (A + B)) * 1.0625f;
+          Bn = B * 1.0625f;
+          const float2 mx = blk_sdmax[tc_.n];
+          tfast = thr - fmaf(r1, mx.x, Bn * mx.y);
+        }
       }
       tc::mbar_wait(tc::smem_u32(&tfull[acc]), acc_phase);
       tc::tc_fence_after();
       int row_count = 0;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t v[32];
-        tc::tmem_ld32(tbase + ch * 32, v);
+      for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
+        uint32_t v2[2][32];
+        tc::tmem_ld32(tbase + ch2 * 64, v2[0]);
+        tc::tmem_ld32(tbase + ch2 * 64 + 32, v2[1]);
         tc::tmem_ld_wait();
-        const int c0 = n0 + ch * 32;
-        const int64_t sp0 = sp;
-        uint32_t mask = 0;
-        if (row_ok) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int col = c0 + c;
-            const bool hit = col == nxt;
-            if (hit) {
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* v = v2[h];
+          const int c0 = n0 + ch2 * 64 + h * 32;
+          const int64_t sp0 = sp;
+          uint32_t mask = 0, sup = 0;
+          if (row_ok) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
+            if (kMode == 1 && mask) {
+              // exact per-column bound for the (rare) survivors of the fast test
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                if (mask & (1u << c)) {
+                  const float2 sd = __ldg(&ep.col_sd[min(c0 + c, (int)ep.p - 1)]);
+                  if (!(fabsf(__uint_as_float(v[c])) > thr - fmaf(r1, sd.x, Bn * sd.y)))
+                    mask &= ~(1u << c);
+                }
+              }
+            }
+            if (gi >= c0 && gi < c0 + 32) mask |= 1u << (gi - c0);    // diagonal
+            while (nxt < c0 + 32) {                                   // support of Omega
+              sup |= 1u << (nxt - c0);
               ++sp;
               nxt = sp < se ? om.col[sp] : INT_MAX;
             }
-            float t = thr;
-            if constexpr (kMode == 1) {
-              const float2 sd = __ldg(&ep.col_sd[col < ep.p ? col : 0]);
-              t = thr - fmaf(r1, sd.x, Bn * sd.y);
-            }
-            const bool cand = hit || (col == gi) || (fabsf(__uint_as_float(v[c])) > t);
-            mask |= (cand && col < ep.p) ? (1u << c) : 0u;
+            mask |= sup;
+            const int64_t left = ep.p - c0;                           // ragged p
+            if (left < 32) mask &= left <= 0 ? 0u : ((1u << left) - 1u);
           }
-        }
-        const int cnt = __popc(mask);
-        const int total = __reduce_add_sync(0xffffffffu, cnt);
-        if (total == 0) continue;
-        int incl = cnt;
+          const int cnt = __popc(mask);
+          const int total = __reduce_add_sync(0xffffffffu, cnt);
+          if (total == 0) continue;
+          int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(pool.cursor, (unsigned long long)incl);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long pos = base + (unsigned long long)(incl - cnt);
-        row_count += cnt;
-        if (cnt) {
-          int64_t s2 = sp0;
-          int32_t n2 = s2 < se ? om.col[s2] : INT_MAX;
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int col = c0 + c;
-            float w = 0.f;
-            if (col == n2) {
-              w = omv[s2];
-              ++s2;
-              n2 = s2 < se ? om.col[s2] : INT_MAX;
-            }
-            if (mask & (1u << c)) {
-              if ((int64_t)pos < pool.cap) {
-                pool.row[pos] = (int32_t)r;
-                pool.col[pos] = col;
-                ((float*)pool.g)[pos] = __uint_as_float(v[c]) / nf;
-                ((float*)pool.w)[pos] = w;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          unsigned long long base = 0;
+          if (lane == 31) base = atomicAdd(seg_cur, (unsigned long long)incl);   // shared memory
+          base = __shfl_sync(0xffffffffu, base, 31);
+          unsigned long long pos = base + (unsigned long long)(incl - cnt);
+          row_count += cnt;
+          if constexpr (kMode == 1) {
+            // candidate positions only; the exact values come from the refine SDDMM
+            uint32_t m = mask;
+            while (m) {
+              const int c = __ffs(m) - 1;
+              m &= m - 1;
+              float w = 0.f;
+              if (sup & (1u << c)) w = omv[sp0 + __popc(sup & ((1u << c) - 1u))];
+              if ((int64_t)pos < pool.seg_cap) {
+                const int64_t gp = seg_base + (int64_t)pos;
+                pool.row[gp] = (int32_t)r;
+                pool.col[gp] = c0 + c;
+                ((float*)pool.w)[gp] = w;
               }
               ++pos;
+            }
+          } else if (cnt) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              if (mask & (1u << c)) {
+                float w = 0.f;
+                if (sup & (1u << c)) w = omv[sp0 + __popc(sup & ((1u << c) - 1u))];
+                if ((int64_t)pos < pool.seg_cap) {
+                  const int64_t gp = seg_base + (int64_t)pos;
+                  pool.row[gp] = (int32_t)r;
+                  pool.col[gp] = c0 + c;
+                  ((float*)pool.g)[gp] = __uint_as_float(v[c]) * inv_nf;
+                  ((float*)pool.w)[gp] = w;
+                }
+                ++pos;
+              }
             }
           }
         }
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&tempty[acc]));
+      if (lane == 0) tc::mbar_arrive_cluster(tempty_leader + acc * 8, 0);
       if (row_count) atomicAdd(&pool.row_cnt[r], row_count);
       if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();
   tc::tc_fence_after();
-  if (warp == 2) tc::tmem_dealloc<kTmemCols, 1>(tmem_base);
+  if (warp == 2) tc::tmem_dealloc<kTmemCols, 2>(tmem_base);
+  if (threadIdx.x == 0) pool.seg_cnt[blockIdx.x] = *seg_cur;
+}
+
+// per-256-column-block maxima of the filter's column constants
+__global__ void blk_max_kernel(const float2* __restrict__ col_sd, int64_t p, int nblk,
+                               float2* __restrict__ out) {
+  const int b = blockIdx.x;
+  float mx = 0.f, my = 0.f;
+  for (int j = threadIdx.x; j < BN; j += blockDim.x) {
+    const int64_t k = (int64_t)b * BN + j;
+    if (k < p) {
+      mx = fmaxf(mx, col_sd[k].x);
+      my = fmaxf(my, col_sd[k].y);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
+  }
+  __shared__ float sx[32], sy[32];
+  if ((threadIdx.x & 31) == 0) { sx[threadIdx.x >> 5] = mx; sy[threadIdx.x >> 5] = my; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { mx = fmaxf(mx, sx[w]); my = fmaxf(my, sy[w]); }
+    out[b] = make_float2(mx, my);
+  }
+  (void)nblk;
 }
 
 // ---- host: tensor maps ----------------------------------------------------
@@ -331,6 +404,7 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ldk, int b
 struct TcGemmPlan {
   CUtensorMap a_hi[2], a_lo[2], b_hi, b_lo;
   int64_t pk_pad = 0, p_pad = 0, ldk = 0;
+  float2* blk_sdmax = nullptr;   // [p_pad / 256] (BF16_FILTER)
 };
 
 bool tc_supported(int cc_major, int cc_minor) { return cc_major == 10 && cc_minor == 0; }
@@ -347,12 +421,17 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
             make_map(&p->a_lo[0], Ylo0, pk_pad, ldk, BM, err) &&
             make_map(&p->a_hi[1], Yhi1, pk_pad, ldk, BM, err) &&
             make_map(&p->a_lo[1], Ylo1, pk_pad, ldk, BM, err) &&
-            make_map(&p->b_hi, Xhi, p_pad, ldk, BN, err) &&
-            make_map(&p->b_lo, Xlo, p_pad, ldk, BN, err);
+            make_map(&p->b_hi, Xhi, p_pad, ldk, BNH, err) &&
+            make_map(&p->b_lo, Xlo, p_pad, ldk, BNH, err);
+  if (ok && cudaMalloc(&p->blk_sdmax, (p_pad / BN) * sizeof(float2)) != cudaSuccess) {
+    *err = "alloc";
+    ok = false;
+  }
   if (!ok) {
     delete p;
     return nullptr;
   }
+  cudaMemset(p->blk_sdmax, 0, (p_pad / BN) * sizeof(float2));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -364,24 +443,40 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
   return p;
 }
 
-void tc_plan_destroy(TcGemmPlan* p) { delete p; }
+int tc_plan_set_col_norms(TcGemmPlan* p, const float2* col_sd, int64_t pcols, cudaStream_t st) {
+  const int nblk = (int)(p->p_pad / BN);
+  blk_max_kernel<<<nblk, 256, 0, st>>>(col_sd, pcols, nblk, p->blk_sdmax);
+  return 1;
+}
+
+void tc_plan_destroy(TcGemmPlan* p) {
+  if (!p) return;
+  if (p->blk_sdmax) cudaFree(p->blk_sdmax);
+  delete p;
+}
+
+int tc_grid_size(const TcGemmPlan* plan, int sm_count) {
+  const int64_t tiles = (plan->pk_pad / (2 * BM)) * (plan->p_pad / BN);
+  const int64_t clusters = tiles < sm_count / 2 ? tiles : sm_count / 2;
+  return (int)(2 * clusters);
+}
 
 int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int64_t kdim, int sm_count,
                    const EpiParams& ep, const OmegaView& om, const PoolView& pool,
                    cudaStream_t st) {
-  const int num_m = (int)(plan->pk_pad / BM);
+  const int num_m = (int)(plan->pk_pad / (2 * BM));
   const int num_n = (int)(plan->p_pad / BN);
   const int num_kb = (int)((kdim + BK - 1) / BK);
-  const int tiles = num_m * num_n;
-  const int grid = tiles < sm_count ? tiles : sm_count;
+  const int grid = tc_grid_size(plan, sm_count);
+  if (pool.nseg != grid) return -1;
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0><<<grid, kThreads, Cfg<0>::kSmemBytes, st>>>(
         plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, ep,
-        om, pool);
+        plan->blk_sdmax, om, pool);
   else
     gemm_tc_kernel<1><<<grid, kThreads, Cfg<1>::kSmemBytes, st>>>(
         plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, ep,
-        om, pool);
+        plan->blk_sdmax, om, pool);
   return 1;
 }
 

@@ -191,14 +191,16 @@ __global__ void __launch_bounds__(1024) scan_phase3(const int32_t* __restrict__ 
 constexpr int kWarpSortMax = 1024;     // rows up to this length: one warp, smem bitonic
 constexpr int kBlockSortMax = 16384;   // rows up to this length: one block, smem bitonic
 
-__global__ void scatter_kernel(int64_t pk, const int32_t* __restrict__ prow,
-                               const int32_t* __restrict__ pcol,
-                               const unsigned long long* __restrict__ cursor, int64_t cap,
+// grid: (8 blocks per segment) x nseg
+__global__ void scatter_kernel(const int32_t* __restrict__ prow, const int32_t* __restrict__ pcol,
+                               const unsigned long long* __restrict__ seg_cnt, int64_t seg_cap,
                                const int64_t* __restrict__ c_ptr, int32_t* rcur,
                                uint64_t* __restrict__ keys) {
-  const int64_t cnt = min((int64_t)*cursor, cap);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t seg = blockIdx.y;
+  const int64_t cnt = min((int64_t)seg_cnt[seg], seg_cap);
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < cnt;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = seg * seg_cap + o;
     const int32_t r = prow[i];
     const int64_t pos = c_ptr[r] + atomicAdd(&rcur[r], 1);
     keys[pos] = ((uint64_t)(uint32_t)pcol[i] << 32) | (uint64_t)(uint32_t)i;
@@ -246,18 +248,24 @@ __global__ void rowsort_warp_kernel(int64_t pk, const int64_t* __restrict__ c_pt
   for (int t = lane; t < len; t += 32) keys[beg + t] = s[t];
 }
 
+// Rows longer than kWarpSortMax: one block per row. Runs of kBlockSortMax are
+// sorted in shared memory (bitonic), then merged pairwise in global memory
+// (merge path: each output position finds its split by binary search).
 __global__ void __launch_bounds__(1024) rowsort_block_kernel(const int64_t* __restrict__ c_ptr,
-                                     uint64_t* __restrict__ keys, uint64_t* __restrict__ tmp,
-                                     const int32_t* __restrict__ long_rows) {
+                                                             uint64_t* __restrict__ keys,
+                                                             uint64_t* __restrict__ tmp,
+                                                             const int32_t* __restrict__ long_rows) {
   extern __shared__ uint64_t sm_keys[];
   const int nlong = long_rows[0];
   for (int q = blockIdx.x; q < nlong; q += gridDim.x) {
     const int64_t r = long_rows[1 + q];
     const int64_t beg = c_ptr[r], len = c_ptr[r + 1] - beg;
-    if (len <= kBlockSortMax) {
+    for (int64_t run0 = 0; run0 < len; run0 += kBlockSortMax) {
+      const int64_t rl = min((int64_t)kBlockSortMax, len - run0);
       int n2 = 32;
-      while (n2 < len) n2 <<= 1;
-      for (int t = threadIdx.x; t < n2; t += blockDim.x) sm_keys[t] = t < len ? keys[beg + t] : ~0ull;
+      while (n2 < rl) n2 <<= 1;
+      uint64_t* g = keys + beg + run0;
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) sm_keys[t] = t < rl ? g[t] : ~0ull;
       __syncthreads();
       for (int k = 2; k <= n2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
@@ -265,27 +273,41 @@ __global__ void __launch_bounds__(1024) rowsort_block_kernel(const int64_t* __re
             const int ixj = t ^ j;
             if (ixj > t) {
               const bool asc = (t & k) == 0;
-              uint64_t a = sm_keys[t], b = sm_keys[ixj];
-              if ((a > b) == asc) { sm_keys[t] = b; sm_keys[ixj] = a; }
+              uint64_t x = sm_keys[t], y = sm_keys[ixj];
+              if ((x > y) == asc) { sm_keys[t] = y; sm_keys[ixj] = x; }
             }
           }
           __syncthreads();
         }
       }
-      for (int t = threadIdx.x; t < len; t += blockDim.x) keys[beg + t] = sm_keys[t];
-      __syncthreads();
-    } else {
-      // Very long row: rank by counting (keys are unique), O(len^2) but correct.
-      for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-        const uint64_t ka = keys[beg + a];
-        int64_t rank = 0;
-        for (int64_t b = 0; b < len; ++b) rank += keys[beg + b] < ka;
-        tmp[beg + rank] = ka;
-      }
-      __syncthreads();
-      for (int64_t a = threadIdx.x; a < len; a += blockDim.x) keys[beg + a] = tmp[beg + a];
+      for (int t = threadIdx.x; t < rl; t += blockDim.x) g[t] = sm_keys[t];
       __syncthreads();
     }
+    uint64_t* src = keys + beg;
+    uint64_t* dst = tmp + beg;
+    for (int64_t w = kBlockSortMax; w < len; w *= 2) {
+      for (int64_t s0 = 0; s0 < len; s0 += 2 * w) {
+        const uint64_t* A = src + s0;
+        const int64_t la = min(w, len - s0);
+        const uint64_t* B = A + la;
+        const int64_t lb = max((int64_t)0, min(w, len - s0 - la));
+        for (int64_t k = threadIdx.x; k < la + lb; k += blockDim.x) {
+          int64_t lo = max((int64_t)0, k - lb), hi = min(k, la);
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (A[mid] < B[k - mid - 1]) lo = mid + 1; else hi = mid;
+          }
+          const int64_t i = lo, j = k - lo;
+          dst[s0 + k] = (j >= lb || (i < la && A[i] < B[j])) ? A[i] : B[j];
+        }
+      }
+      __syncthreads();
+      uint64_t* t2 = src; src = dst; dst = t2;
+    }
+    if (src != keys + beg) {
+      for (int64_t t = threadIdx.x; t < len; t += blockDim.x) keys[beg + t] = src[t];
+    }
+    __syncthreads();
   }
 }
 
@@ -300,7 +322,7 @@ __global__ void gather_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
     const uint64_t k = keys[e];
     const uint32_t idx = (uint32_t)(k & 0xffffffffu);
     c_col[e] = (int32_t)(k >> 32);
-    c_g[e] = pg[idx];
+    if (pg) c_g[e] = pg[idx];   // NULL for BF16_FILTER: the refine SDDMM writes c_g
     c_w[e] = pw[idx];
   }
 }
@@ -615,7 +637,9 @@ __global__ void __launch_bounds__(1024) reduce_rows_kernel(int64_t pk, const dou
   __shared__ double sh[32];
   double a[5] = {0, 0, 0, 0, 0};
   long long cnt = 0;
+  double mx = 0;
   for (int64_t r = threadIdx.x; r < pk; r += blockDim.x) {
+    if (c_ptr) mx = fmax(mx, (double)(c_ptr[r + 1] - c_ptr[r]));
     if (D2) a[0] += D2[r];
     if (dd) a[1] += dd[r];
     if (logd) a[2] += logd[r];
@@ -631,7 +655,14 @@ __global__ void __launch_bounds__(1024) reduce_rows_kernel(int64_t pk, const dou
   if (threadIdx.x == 0) {
     out[5] = s;
     out[6] = c_ptr ? (double)c_ptr[pk] : 0.0;
-    out[7] = 0.0;
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+    out[7] = mx;
   }
 }
 
@@ -798,8 +829,8 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
                     int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col, void* c_g,
                     void* c_w, int32_t* long_rows, cudaStream_t st) {
   int launches = 0;
-  scatter_kernel<<<148 * 8, 256, 0, st>>>(pk, pool.row, pool.col, pool.cursor, pool.cap, c_ptr,
-                                          rcur, keys);
+  scatter_kernel<<<dim3(pool.nseg == 1 ? 148 * 8 : 8, (unsigned)pool.nseg), 256, 0, st>>>(
+      pool.row, pool.col, pool.seg_cnt, pool.seg_cap, c_ptr, rcur, keys);
   ++launches;
   {
     const int warps = 8;

@@ -69,14 +69,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y)
       : "memory");
 }
-// 2-CTA variant: both CTAs of the pair issue it for their half; the
-// transaction bytes are credited to the leader CTA's mbarrier (peer bit 0).
-__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* m, uint32_t bar,
-                                                int32_t x, int32_t y) {
+// Address of the same shared-memory location in CTA `cta` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(cta));
+  return r;
+}
+// 2-CTA variant: both CTAs of the pair issue it for their half of the tile;
+// `bar_cluster` is the leader CTA's mbarrier (shared::cluster address), which
+// receives the transaction bytes of both CTAs.
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* m,
+                                                uint32_t bar_cluster, int32_t x, int32_t y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(x), "r"(y)
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y)
       : "memory");
 }
 

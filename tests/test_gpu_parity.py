@@ -128,3 +128,18 @@ def test_errors_are_loud():
     with pytest.raises(A.AccordError) as e:
         A.AccordSolver(Xn.cuda(), 0.1)
     assert "row 3, col 2" in str(e.value)
+
+
+@pytest.mark.parametrize("p,n,lam,T", [(4000, 60, 0.05, 2), (17000, 40, 0.02, 1)])
+def test_parity_dense_candidate_rows(p, n, lam, T):
+    """Rows with thousands (block bitonic) and > 16384 (runs + merge path)
+    candidates: small n makes |S_ik| > lambda for most pairs."""
+    _cuda()
+    from accord_inputs import Config
+    cfg = Config(name=f"dense_p{p}", p=p, n=n, dtype="f32", structure="ba", block=p // 4,
+                 lambdas=(lam,), T=T, graph_seed=61, sample_seed=62)
+    pr = make_problem(cfg)
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    csr, stats, info = run_gpu(pr.Xt, lam, T, inv_L, A.GEMM_AUTO)
+    assert stats[-1]["max_row_cand"] > (16384 if p > 16384 else 1024)
+    compare_full(pr.Xt, lam, T, inv_L, csr.to_dense(p), stats, "f32")
