@@ -58,7 +58,6 @@ constexpr uint32_t kTileA = BM * BK * 2;        // 16 KB
 constexpr uint32_t kTileB = BNH * BK * 2;       // 16 KB
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
-constexpr int kGroupM = 16;                     // M-blocks per raster group (L2 reuse)
 
 template <int kMode> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
@@ -67,16 +66,63 @@ template <int kMode> struct Cfg {
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
 };
 
-struct TileCoord { int m, n; };
+// Tile order. Work unit = up to `U` consecutive M-blocks at a fixed N-block,
+// inside a group of `GM` M-blocks; units are enumerated group-major, then by
+// N-block, and dealt round-robin to the clusters. All clusters therefore work
+// on one A group at a time (GM x 256 rows of Y stay L2-resident) and each
+// cluster reuses its B block (256 rows of X^T) across its unit, so X^T is
+// streamed from HBM about once per group instead of once per tile,
+// independently of how far the persistent clusters drift apart.
+struct Sched {
+  int num_m, num_n, GM, U;
+  int full_groups, rem, spu, spu_last;
+  long long units_full, units;
+  __device__ Sched(int nm, int nn, int gm, int u) : num_m(nm), num_n(nn), GM(gm), U(u) {
+    full_groups = num_m / GM;
+    rem = num_m - full_groups * GM;
+    spu = (GM + U - 1) / U;
+    spu_last = (rem + U - 1) / U;
+    units_full = (long long)full_groups * num_n * spu;
+    units = units_full + (long long)num_n * spu_last;
+  }
+  // unit -> (first M-block, count, N-block)
+  __device__ void unit(long long u, int& m0, int& cnt, int& n) const {
+    if (u < units_full) {
+      const long long per_g = (long long)num_n * spu;
+      const int g = (int)(u / per_g);
+      const int r = (int)(u - (long long)g * per_g);
+      n = r / spu;
+      const int s = r - n * spu;
+      m0 = g * GM + s * U;
+      cnt = min(U, GM - s * U);
+    } else {
+      const int r = (int)(u - units_full);
+      n = r / spu_last;
+      const int s = r - n * spu_last;
+      m0 = full_groups * GM + s * U;
+      cnt = min(U, rem - s * U);
+    }
+  }
+};
 
-__device__ __forceinline__ TileCoord tile_coord(int t, int num_m, int num_n) {
-  const int per_group = kGroupM * num_n;
-  const int g = t / per_group;
-  const int first = g * kGroupM;
-  const int gm = min(kGroupM, num_m - first);
-  const int l = t - g * per_group;
-  return TileCoord{first + l % gm, l / gm};
-}
+// Iterate this cluster's tiles in schedule order: for (TileIt it(...); it.ok; it.next())
+struct TileIt {
+  const Sched& S;
+  long long u;
+  int stride, m0, cnt, mi, n;
+  bool ok;
+  __device__ TileIt(const Sched& s, int cluster, int nclusters)
+      : S(s), u(cluster), stride(nclusters), mi(0) { load(); }
+  __device__ void load() {
+    ok = u < S.units;
+    if (ok) S.unit(u, m0, cnt, n);
+    mi = 0;
+  }
+  __device__ void next() {
+    if (++mi == cnt) { u += stride; load(); }
+  }
+  __device__ int m() const { return m0 + mi; }
+};
 
 template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -84,7 +130,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
                const __grid_constant__ CUtensorMap mB_hi,
                const __grid_constant__ CUtensorMap mB_lo, int num_kb, int num_m, int num_n,
-               EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
+               int group_m, int unit_m, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
   constexpr int kStages = Cfg<kMode>::kStages;
   constexpr uint32_t kStageBytes = Cfg<kMode>::kStageBytes;
@@ -101,8 +147,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
-  const int num_tiles = num_m * num_n;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const Sched sched(num_m, num_n, group_m, unit_m);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&mA_hi);
@@ -133,10 +179,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
-        const TileCoord tc_ = tile_coord(t, num_m, num_n);
-        const int ya = tc_.m * (2 * BM) + (int)rank * BM;
-        const int yb = tc_.n * BN + (int)rank * BNH;
+      for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
+        const int ya = it.m() * (2 * BM) + (int)rank * BM;
+        const int yb = it.n * BN + (int)rank * BNH;
         for (int kb = 0; kb < num_kb; ++kb) {
           tc::mbar_wait(tc::smem_u32(&empty[stage]), phase ^ 1);
           uint8_t* s = smem + stage * kStageBytes;
@@ -164,7 +209,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
         tc::mbar_wait(tc::smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * BN);
@@ -205,12 +250,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     const int64_t seg_base = (int64_t)blockIdx.x * pool.seg_cap;   // this CTA's pool segment
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cluster; t < num_tiles; t += nclusters) {
-      const TileCoord tc_ = tile_coord(t, num_m, num_n);
-      const int64_t r = (int64_t)tc_.m * (2 * BM) + (int64_t)rank * BM + q * 32 + lane;
+    for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
+      const int64_t r = (int64_t)it.m() * (2 * BM) + (int64_t)rank * BM + q * 32 + lane;
       const bool row_ok = r < ep.pk;
       const int64_t gi = ep.r0 + r;
-      const int n0 = tc_.n * BN;
+      const int n0 = it.n * BN;
       // support walk setup and per-row filter constants (overlap the mainloop)
       int64_t sp = 0, se = 0;
       int32_t nxt = INT_MAX;
@@ -230,7 +274,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           const float A = ep.row_A[r], B = ep.row_B[r];
           r1 = (A + gam * (A + B)) * 1.0625f;
           Bn = B * 1.0625f;
-          const float2 mx = blk_sdmax[tc_.n];
+          const float2 mx = blk_sdmax[it.n];
           tfast = thr - fmaf(r1, mx.x, Bn * mx.y);
         }
       }
@@ -469,14 +513,20 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int64_t kdim, int sm_co
   const int num_kb = (int)((kdim + BK - 1) / BK);
   const int grid = tc_grid_size(plan, sm_count);
   if (pool.nseg != grid) return -1;
+  // A group of <= 64 M-blocks (<= 32 MB of Y_hi at n = 1000) stays in L2; units
+  // small enough that the per-cluster imbalance is <= ~6% of its work
+  const int group_m = num_m < 64 ? num_m : 64;
+  const long long tiles = (long long)num_m * num_n;
+  long long u = tiles / ((long long)(grid / 2) * 16);
+  const int unit_m = (int)(u < 1 ? 1 : (u > group_m ? group_m : u));
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0><<<grid, kThreads, Cfg<0>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, ep,
-        plan->blk_sdmax, om, pool);
+        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, group_m, unit_m,
+        ep, plan->blk_sdmax, om, pool);
   else
     gemm_tc_kernel<1><<<grid, kThreads, Cfg<1>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, ep,
-        plan->blk_sdmax, om, pool);
+        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, group_m, unit_m,
+        ep, plan->blk_sdmax, om, pool);
   return 1;
 }
 
