@@ -66,40 +66,43 @@ template <int kMode> struct Cfg {
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
 };
 
-// Tile order. Work unit = up to `U` consecutive M-blocks at a fixed N-block,
-// inside a group of `GM` M-blocks; units are enumerated group-major, then by
-// N-block, and dealt round-robin to the clusters. All clusters therefore work
-// on one A group at a time (GM x 256 rows of Y stay L2-resident) and each
-// cluster reuses its B block (256 rows of X^T) across its unit, so X^T is
-// streamed from HBM about once per group instead of once per tile,
-// independently of how far the persistent clusters drift apart.
+// Tile order. Work unit = up to `U` consecutive N-blocks at a fixed M-block,
+// inside a group of `GN` N-blocks; units are enumerated group-major, then by
+// M-block, and dealt round-robin to the clusters. All clusters therefore work
+// on one X^T group at a time (GN x 256 rows, <= 32 MB, stay L2-resident, so
+// X^T crosses HBM once per launch and Y once per group), each cluster reuses
+// its Y block across its unit, and inside a unit a thread's row stays the
+// same, so the epilogue's walk through the sorted CSR row of Omega continues
+// from tile to tile (one binary search per unit instead of per tile). This
+// keeps the schedule's L2 footprint bounded however far the persistent
+// clusters drift apart.
 struct Sched {
-  int num_m, num_n, GM, U;
+  int num_m, num_n, GN, U;
   int full_groups, rem, spu, spu_last;
   long long units_full, units;
-  __device__ Sched(int nm, int nn, int gm, int u) : num_m(nm), num_n(nn), GM(gm), U(u) {
-    full_groups = num_m / GM;
-    rem = num_m - full_groups * GM;
-    spu = (GM + U - 1) / U;
+  __device__ Sched(int nm, int nn, int gn, int u) : num_m(nm), num_n(nn), GN(gn), U(u) {
+    full_groups = num_n / GN;
+    rem = num_n - full_groups * GN;
+    spu = (GN + U - 1) / U;
     spu_last = (rem + U - 1) / U;
-    units_full = (long long)full_groups * num_n * spu;
-    units = units_full + (long long)num_n * spu_last;
+    units_full = (long long)full_groups * num_m * spu;
+    units = units_full + (long long)num_m * spu_last;
   }
-  // unit -> (first M-block, count, N-block)
-  __device__ void unit(long long u, int& m0, int& cnt, int& n) const {
+  // unit -> (M-block, first N-block, count)
+  __device__ void unit(long long u, int& m, int& n0, int& cnt) const {
     if (u < units_full) {
-      const long long per_g = (long long)num_n * spu;
+      const long long per_g = (long long)num_m * spu;
       const int g = (int)(u / per_g);
       const int r = (int)(u - (long long)g * per_g);
-      n = r / spu;
-      const int s = r - n * spu;
-      m0 = g * GM + s * U;
-      cnt = min(U, GM - s * U);
+      m = r / spu;
+      const int s = r - m * spu;
+      n0 = g * GN + s * U;
+      cnt = min(U, GN - s * U);
     } else {
       const int r = (int)(u - units_full);
-      n = r / spu_last;
-      const int s = r - n * spu_last;
-      m0 = full_groups * GM + s * U;
+      m = r / spu_last;
+      const int s = r - m * spu_last;
+      n0 = full_groups * GN + s * U;
       cnt = min(U, rem - s * U);
     }
   }
@@ -109,19 +112,20 @@ struct Sched {
 struct TileIt {
   const Sched& S;
   long long u;
-  int stride, m0, cnt, mi, n;
+  int stride, m, n0, cnt, ni;
   bool ok;
   __device__ TileIt(const Sched& s, int cluster, int nclusters)
-      : S(s), u(cluster), stride(nclusters), mi(0) { load(); }
+      : S(s), u(cluster), stride(nclusters), ni(0) { load(); }
   __device__ void load() {
     ok = u < S.units;
-    if (ok) S.unit(u, m0, cnt, n);
-    mi = 0;
+    if (ok) S.unit(u, m, n0, cnt);
+    ni = 0;
   }
   __device__ void next() {
-    if (++mi == cnt) { u += stride; load(); }
+    if (++ni == cnt) { u += stride; load(); }
   }
-  __device__ int m() const { return m0 + mi; }
+  __device__ int n() const { return n0 + ni; }
+  __device__ bool unit_start() const { return ni == 0; }
 };
 
 template <int kMode>
@@ -130,7 +134,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
                const __grid_constant__ CUtensorMap mB_hi,
                const __grid_constant__ CUtensorMap mB_lo, int num_kb, int num_m, int num_n,
-               int group_m, int unit_m, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
+               int group_n, int unit_n, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
   constexpr int kStages = Cfg<kMode>::kStages;
   constexpr uint32_t kStageBytes = Cfg<kMode>::kStageBytes;
@@ -148,7 +152,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const Sched sched(num_m, num_n, group_m, unit_m);
+  const Sched sched(num_m, num_n, group_n, unit_n);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&mA_hi);
@@ -180,8 +184,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       int stage = 0;
       uint32_t phase = 0;
       for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
-        const int ya = it.m() * (2 * BM) + (int)rank * BM;
-        const int yb = it.n * BN + (int)rank * BNH;
+        const int ya = it.m * (2 * BM) + (int)rank * BM;
+        const int yb = it.n() * BN + (int)rank * BNH;
         for (int kb = 0; kb < num_kb; ++kb) {
           tc::mbar_wait(tc::smem_u32(&empty[stage]), phase ^ 1);
           uint8_t* s = smem + stage * kStageBytes;
@@ -250,33 +254,41 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     const int64_t seg_base = (int64_t)blockIdx.x * pool.seg_cap;   // this CTA's pool segment
     int acc = 0;
     uint32_t acc_phase = 0;
+    int64_t r = 0, gi = 0, sp = 0, se = 0;
+    bool row_ok = false;
+    int32_t nxt = INT_MAX;
+    float r1 = 0.f, Bn = 0.f;
     for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
-      const int64_t r = (int64_t)it.m() * (2 * BM) + (int64_t)rank * BM + q * 32 + lane;
-      const bool row_ok = r < ep.pk;
-      const int64_t gi = ep.r0 + r;
-      const int n0 = it.n * BN;
-      // support walk setup and per-row filter constants (overlap the mainloop)
-      int64_t sp = 0, se = 0;
-      int32_t nxt = INT_MAX;
-      float r1 = 0.f, Bn = 0.f, tfast = thr;
-      if (row_ok) {
-        int64_t lo = om.ptr[r], hi = om.ptr[r + 1];
-        se = hi;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (om.col[mid] < n0) lo = mid + 1; else hi = mid;
+      const int n0 = it.n() * BN;
+      if (it.unit_start()) {
+        // new row block: row constants and the start of the CSR walk (the
+        // walk then continues across the unit's consecutive column tiles)
+        r = (int64_t)it.m * (2 * BM) + (int64_t)rank * BM + q * 32 + lane;
+        row_ok = r < ep.pk;
+        gi = ep.r0 + r;
+        nxt = INT_MAX;
+        if (row_ok) {
+          int64_t lo = om.ptr[r], hi = om.ptr[r + 1];
+          se = hi;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (om.col[mid] < n0) lo = mid + 1; else hi = mid;
+          }
+          sp = lo;
+          nxt = sp < se ? om.col[sp] : INT_MAX;
+          if constexpr (kMode == 1) {
+            // n*delta_ik = r1 * s_k + Bn * D_k, inflated by 1.0625 for the
+            // float evaluation of the bound
+            const float A = ep.row_A[r], B = ep.row_B[r];
+            r1 = (A + gam * (A + B)) * 1.0625f;
+            Bn = B * 1.0625f;
+          }
         }
-        sp = lo;
-        nxt = sp < se ? om.col[sp] : INT_MAX;
-        if constexpr (kMode == 1) {
-          // n*delta_ik = r1 * s_k + Bn * D_k, inflated by 1.0625 for the
-          // float evaluation of the bound; tfast uses the tile's max s_k, D_k
-          const float A = ep.row_A[r], B = ep.row_B[r];
-          r1 = (A + gam * (A + B)) * 1.0625f;
-          Bn = B * 1.0625f;
-          const float2 mx = blk_sdmax[it.n];
-          tfast = thr - fmaf(r1, mx.x, Bn * mx.y);
-        }
+      }
+      float tfast = thr;
+      if (kMode == 1 && row_ok) {
+        const float2 mx = blk_sdmax[it.n()];     // tile max of the column constants
+        tfast = thr - fmaf(r1, mx.x, Bn * mx.y);
       }
       tc::mbar_wait(tc::smem_u32(&tfull[acc]), acc_phase);
       tc::tc_fence_after();
@@ -370,7 +382,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(tempty_leader + acc * 8, 0);
+      if (lane == 0) tc::mbar_arrive_remote(tempty_leader + acc * 8, 0);
       if (row_count) atomicAdd(&pool.row_cnt[r], row_count);
       if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
     }
@@ -513,19 +525,19 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int64_t kdim, int sm_co
   const int num_kb = (int)((kdim + BK - 1) / BK);
   const int grid = tc_grid_size(plan, sm_count);
   if (pool.nseg != grid) return -1;
-  // A group of <= 64 M-blocks (<= 32 MB of Y_hi at n = 1000) stays in L2; units
-  // small enough that the per-cluster imbalance is <= ~6% of its work
-  const int group_m = num_m < 64 ? num_m : 64;
+  // A group of <= 64 N-blocks (<= 32 MB of X^T_hi at n = 1000) stays in L2;
+  // units small enough that the per-cluster imbalance is <= ~6% of its work
+  const int group_n = num_n < 64 ? num_n : 64;
   const long long tiles = (long long)num_m * num_n;
   long long u = tiles / ((long long)(grid / 2) * 16);
-  const int unit_m = (int)(u < 1 ? 1 : (u > group_m ? group_m : u));
+  const int unit_n = (int)(u < 1 ? 1 : (u > group_n ? group_n : u));
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0><<<grid, kThreads, Cfg<0>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, group_m, unit_m,
+        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, group_n, unit_n,
         ep, plan->blk_sdmax, om, pool);
   else
     gemm_tc_kernel<1><<<grid, kThreads, Cfg<1>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, group_m, unit_m,
+        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, group_n, unit_n,
         ep, plan->blk_sdmax, om, pool);
   return 1;
 }
