@@ -30,9 +30,15 @@ struct PoolView {             // candidate pool written by the GEMM epilogue (un
   int32_t* col;               // global column
   void* g;                    // T: [Omega S]_ik
   void* w;                    // T: omega_ik^{(t)} (0 if absent)
-  int64_t seg_cap;            // entries per segment; segment s = [s*seg_cap, (s+1)*seg_cap)
-  int64_t nseg;               // segments (one per persistent GEMM CTA; 1 for the SIMT GEMM)
-  unsigned long long* seg_cnt;// [nseg] entries emitted per segment (may exceed seg_cap)
+  // The pool is handed out in chunks of `chunk` entries: chunk c is
+  // [c*chunk, (c+1)*chunk). Each tcgen05 epilogue warp fills a private chunk
+  // and takes the next one with one atomicAdd on *chunk_next (no contention on
+  // a single cursor, no per-CTA imbalance). The SIMT GEMM uses one chunk of
+  // the whole capacity with an atomic cursor in chunk_fill[0].
+  int64_t chunk;              // entries per chunk
+  int64_t nchunks;            // chunks available
+  unsigned int* chunk_next;   // chunks handed out (may exceed nchunks: overflow)
+  unsigned long long* chunk_fill;   // [nchunks] entries written into each chunk
   int32_t* row_cnt;           // [pk] entries emitted per row
 };
 
@@ -138,7 +144,7 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
 void tc_plan_destroy(TcGemmPlan*);
 // per-256-column maxima of the filter's column constants (after launch_col_norms)
 int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st);
-int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs (= pool segments)
+int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs
 int launch_gemm_tc(TcGemmPlan* plan, int mode /* accord_gemm: BF16X3 or BF16_FILTER */,
                    int ybuf, int64_t kdim, int sm_count, const EpiParams& ep,
                    const OmegaView& om, const PoolView& pool, cudaStream_t st);

@@ -120,8 +120,10 @@ struct accord_ctx {
   int32_t *pool_row = nullptr, *pool_col = nullptr;
   void *pool_g = nullptr, *pool_w = nullptr;
   int32_t *row_cnt = nullptr, *rcur = nullptr, *long_rows = nullptr;
-  unsigned long long* seg_cnt = nullptr;   // [max(sm_count, 1)] pool fill per segment
-  int64_t nseg = 1;
+  unsigned int* chunk_next = nullptr;      // pool chunks handed out (device counter)
+  unsigned long long* chunk_fill = nullptr;   // [nchunks] entries per chunk
+  int64_t chunk = 0, nchunks = 0;          // pool chunking (see PoolView)
+  int gemm_warps = 0;                      // epilogue warps of the tcgen05 GEMM (0 = SIMT)
   double *row_D2 = nullptr, *row_Y2 = nullptr, *row_dd = nullptr, *row_l1 = nullptr,
          *row_logd = nullptr;
   int32_t* row_nnz = nullptr;
@@ -130,7 +132,7 @@ struct accord_ctx {
   void* scan_tmp = nullptr;
   size_t scan_tmp_sz = 0;
   double* h_red = nullptr;                 // pinned [16]
-  unsigned long long* h_seg = nullptr;     // pinned [max(sm_count, 1)]
+  unsigned long long* h_seg = nullptr;     // pinned [2]: chunks handed out, chunk_fill[0]
   TcGemmPlan* plan = nullptr;
   cudaEvent_t ev[8] = {};
 
@@ -187,8 +189,8 @@ void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
 OmegaView omega_view(accord_ctx* c) { return OmegaView{c->om_ptr, c->om_col, c->om_val}; }
 
 PoolView pool_view(accord_ctx* c) {
-  return PoolView{c->pool_row, c->pool_col, c->pool_g, c->pool_w, c->cap / c->nseg, c->nseg,
-                  c->seg_cnt, c->row_cnt};
+  return PoolView{c->pool_row, c->pool_col, c->pool_g, c->pool_w, c->chunk, c->nchunks,
+                  c->chunk_next, c->chunk_fill, c->row_cnt};
 }
 
 // (Re)allocate the entry-indexed arrays for capacity `cap`, preserving Omega.
@@ -217,6 +219,19 @@ void grow(accord_ctx* c, int64_t cap, int64_t keep_nnz) {
   c->dfree(c->pool_g, oc * T);  c->pool_g = c->dalloc_bytes(cap * T);
   c->dfree(c->pool_w, oc * T);  c->pool_w = c->dalloc_bytes(cap * T);
   c->cap = cap;
+  // chunking: the SIMT GEMM uses one chunk; the tcgen05 epilogue warps take
+  // private chunks of 1024..8192 entries (>= one 32x32 emission batch)
+  c->dfree(c->chunk_fill, c->nchunks * 8);
+  if (c->gemm_warps == 0) {
+    c->chunk = cap;
+    c->nchunks = 1;
+  } else {
+    int64_t ch = 8192;
+    while (ch > 1024 && cap / ch < 4 * (int64_t)c->gemm_warps) ch >>= 1;
+    c->chunk = ch;
+    c->nchunks = std::max<int64_t>(1, cap / ch);
+  }
+  c->chunk_fill = c->dalloc<unsigned long long>(c->nchunks);
 }
 
 // Objective and nnz of the current Omega (collective). Y[cur] must be current
@@ -327,7 +342,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     c->trace = t && t[0] == '1';
   }
   CK(cudaMallocHost(&c->h_red, 16 * sizeof(double)));
-  CK(cudaMallocHost(&c->h_seg, std::max(c->sm_count, 1) * sizeof(unsigned long long)));
+  CK(cudaMallocHost(&c->h_seg, 2 * sizeof(unsigned long long)));
 
   if (c->comm == ACCORD_COMM_NCCL) {
     NcclApi* api = nccl_api();
@@ -426,8 +441,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->row_cnt = c->dalloc<int32_t>(c->pk);
   c->rcur = c->dalloc<int32_t>(c->pk);
   c->long_rows = c->dalloc<int32_t>(c->pk + 1);
-  c->seg_cnt = c->dalloc<unsigned long long>(std::max(c->sm_count, 1));
-  c->nseg = c->plan ? tc_grid_size(c->plan, c->sm_count) : 1;
+  c->chunk_next = c->dalloc<unsigned int>(1);
+  c->gemm_warps = c->plan ? 4 * tc_grid_size(c->plan, c->sm_count) : 0;
   c->row_D2 = c->dalloc<double>(c->pk);
   c->row_Y2 = c->dalloc<double>(c->pk);
   c->row_dd = c->dalloc<double>(c->pk);
@@ -440,8 +455,15 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->scan_tmp = c->dalloc_bytes(c->scan_tmp_sz);
   int64_t cap = prm->cand_capacity;
   if (cap <= 0) {
+    // The first iteration (G = S) has the most candidates (config 5: ~365 per
+    // row); size for it so that it is not recomputed, within 40% of the free
+    // device memory (~52 B per entry across pool, C, keys and Omega arrays).
     const int64_t dense = c->pk * c->p;
-    cap = std::min<int64_t>(dense, std::max<int64_t>(c->pk * 128, 1 << 20));
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const int64_t mem_cap = (int64_t)(0.4 * (double)fr / 52.0);
+    cap = std::min<int64_t>(dense, std::max<int64_t>(c->pk * 512, 1 << 20));
+    cap = std::max<int64_t>(std::min(cap, mem_cap), std::min<int64_t>(dense, c->pk * 16));
   }
   cap = std::max<int64_t>(cap, c->pk);
   grow(c, std::min<int64_t>(cap, (int64_t)UINT32_MAX), 0);
@@ -509,7 +531,13 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   // ---------------- a2 + a3: gradient GEMM with the fused epilogue --------
   for (;;) {
     CK(cudaMemsetAsync(c->row_cnt, 0, c->pk * 4, S));
-    CK(cudaMemsetAsync(c->seg_cnt, 0, c->nseg * 8, S));
+    CK(cudaMemsetAsync(c->chunk_fill, 0, c->nchunks * 8, S));
+    if (c->gemm_warps == 0) {   // SIMT: one chunk, handed out up front
+      static const unsigned int one = 1;
+      CK(cudaMemcpyAsync(c->chunk_next, &one, 4, cudaMemcpyHostToDevice, S));
+    } else {
+      CK(cudaMemsetAsync(c->chunk_next, 0, 4, S));
+    }
     EpiParams ep{};
     ep.pk = c->pk;
     ep.p = c->p;
@@ -536,20 +564,23 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], S));
     TR(c, "gemm");
-    CK(cudaMemcpyAsync(c->h_seg, c->seg_cnt, c->nseg * 8, cudaMemcpyDeviceToHost, S));
-    CK(cudaStreamSynchronize(S));
-    st.ms_gemm += ev_ms(c, 1, 2);
-    int64_t need_seg = 0, total = 0;
-    for (int64_t q = 0; q < c->nseg; ++q) {
-      need_seg = std::max<int64_t>(need_seg, (int64_t)c->h_seg[q]);
-      total += (int64_t)c->h_seg[q];
+    {
+      unsigned int used = 0;
+      CK(cudaMemcpyAsync(&used, c->chunk_next, 4, cudaMemcpyDeviceToHost, S));
+      CK(cudaMemcpyAsync(c->h_seg, c->chunk_fill, 8, cudaMemcpyDeviceToHost, S));
+      CK(cudaStreamSynchronize(S));
+      c->h_seg[1] = used;
     }
-    if (need_seg <= c->cap / c->nseg) break;
-    // a pool segment overflowed: grow (every segment to the largest need) and redo
-    const int64_t want = (need_seg + need_seg / 4 + 1024) * c->nseg;
+    st.ms_gemm += ev_ms(c, 1, 2);
+    // overflow: SIMT counts entries in chunk_fill[0]; tcgen05 counts chunks
+    const int64_t need = c->gemm_warps == 0 ? (int64_t)c->h_seg[0]
+                                            : (int64_t)c->h_seg[1] * c->chunk;
+    const bool ovf = c->gemm_warps == 0 ? need > c->chunk : (int64_t)c->h_seg[1] > c->nchunks;
+    if (!ovf) break;
+    const int64_t want = need + need / 4 + (1 << 20);
     if (want >= (int64_t)UINT32_MAX)
       throw Fail{ACCORD_E_NOMEM, "candidate pool exceeds 2^32 entries"};
-    grow(c, std::max(want, total), c->nnz_local);
+    grow(c, want, c->nnz_local);
   }
   // ---------------- a4: finalize C ----------------
   TR(c, "host_gap");

@@ -86,9 +86,9 @@ gemm_simt_kernel(const T* __restrict__ Y, const T* __restrict__ Xt, int64_t ldk,
       const T w = lookup_omega<T>(om, r, (int32_t)k);
       const bool emit = (k == gi) || (w != T(0)) || (fabs((double)g) > ep.lam_cand);
       if (!emit) continue;
-      const unsigned long long pos = atomicAdd(&pool.seg_cnt[0], 1ull);   // one segment
+      const unsigned long long pos = atomicAdd(&pool.chunk_fill[0], 1ull);   // one chunk
       ++cnt;
-      if ((int64_t)pos < pool.seg_cap) {
+      if ((int64_t)pos < pool.chunk) {
         pool.row[pos] = (int32_t)r;
         pool.col[pos] = (int32_t)k;
         ((T*)pool.g)[pos] = g;

@@ -42,6 +42,7 @@
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 namespace accord {
@@ -134,7 +135,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
                const __grid_constant__ CUtensorMap mB_hi,
                const __grid_constant__ CUtensorMap mB_lo, int num_kb, int num_m, int num_n,
-               int group_n, int unit_n, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
+               int group_n, int unit_n, int dbg, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
   constexpr int kStages = Cfg<kMode>::kStages;
   constexpr uint32_t kStageBytes = Cfg<kMode>::kStageBytes;
@@ -146,7 +147,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
   uint64_t* tfull = bars + 2 * kStages;           // [kAccStages] (each CTA's own)
   uint64_t* tempty = bars + 2 * kStages + kAccStages;   // (leader's is used)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kStages + 2 * kAccStages);
-  unsigned long long* seg_cur = (unsigned long long*)(tmem_slot + 2);   // this CTA's pool cursor
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -170,7 +170,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       tc::mbar_init(tc::smem_u32(&tempty[a]), 8);   // 4 epilogue warps x 2 CTAs
     }
     tc::fence_mbar_init();
-    *seg_cur = 0;
   }
   if (warp == 2) tc::tmem_alloc<kTmemCols, 2>(tc::smem_u32(tmem_slot));
   tc::tc_fence_before();
@@ -229,7 +228,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 = 32 B along K
             const uint32_t accum = (kb | kk) != 0;
-            tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
+            if (dbg != 2) tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
             if constexpr (kMode == 0) {
               tc::mma_bf16<2>(d, a_hi + off, b_lo + off, idesc, 1);
               tc::mma_bf16<2>(d, a_lo + off, b_hi + off, idesc, 1);
@@ -251,7 +250,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     const float gam = ep.gamma;
     const float* omv = (const float*)om.val;
     const uint32_t tempty_leader = tc::smem_u32(&tempty[0]);
-    const int64_t seg_base = (int64_t)blockIdx.x * pool.seg_cap;   // this CTA's pool segment
+    // this warp's private pool chunk (warp-uniform); taken on first use
+    long long chunk_id = -1;
+    int64_t fill = pool.chunk;
     int acc = 0;
     uint32_t acc_phase = 0;
     int64_t r = 0, gi = 0, sp = 0, se = 0;
@@ -293,6 +294,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       tc::mbar_wait(tc::smem_u32(&tfull[acc]), acc_phase);
       tc::tc_fence_after();
       int row_count = 0;
+      if (dbg == 1) {   // diagnostic: release the accumulator without reading it
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_remote(tempty_leader + acc * 8, 0);
+        if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
       for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
@@ -340,10 +348,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             const int y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
           }
-          unsigned long long base = 0;
-          if (lane == 31) base = atomicAdd(seg_cur, (unsigned long long)incl);   // shared memory
-          base = __shfl_sync(0xffffffffu, base, 31);
-          unsigned long long pos = base + (unsigned long long)(incl - cnt);
+          if (fill + total > pool.chunk) {   // chunk full: record it, take the next one
+            if (lane == 0 && chunk_id >= 0 && chunk_id < pool.nchunks)
+              pool.chunk_fill[chunk_id] = (unsigned long long)fill;
+            unsigned int nc = 0;
+            if (lane == 0) nc = atomicAdd(pool.chunk_next, 1u);
+            chunk_id = (long long)__shfl_sync(0xffffffffu, nc, 0);
+            fill = 0;
+          }
+          const bool writable = chunk_id < pool.nchunks;
+          int64_t pos = chunk_id * pool.chunk + fill + (incl - cnt);
+          fill += total;
           row_count += cnt;
           if constexpr (kMode == 1) {
             // candidate positions only; the exact values come from the refine SDDMM
@@ -353,11 +368,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               m &= m - 1;
               float w = 0.f;
               if (sup & (1u << c)) w = omv[sp0 + __popc(sup & ((1u << c) - 1u))];
-              if ((int64_t)pos < pool.seg_cap) {
-                const int64_t gp = seg_base + (int64_t)pos;
-                pool.row[gp] = (int32_t)r;
-                pool.col[gp] = c0 + c;
-                ((float*)pool.w)[gp] = w;
+              if (writable) {
+                pool.row[pos] = (int32_t)r;
+                pool.col[pos] = c0 + c;
+                ((float*)pool.w)[pos] = w;
               }
               ++pos;
             }
@@ -367,12 +381,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               if (mask & (1u << c)) {
                 float w = 0.f;
                 if (sup & (1u << c)) w = omv[sp0 + __popc(sup & ((1u << c) - 1u))];
-                if ((int64_t)pos < pool.seg_cap) {
-                  const int64_t gp = seg_base + (int64_t)pos;
-                  pool.row[gp] = (int32_t)r;
-                  pool.col[gp] = c0 + c;
-                  ((float*)pool.g)[gp] = __uint_as_float(v[c]) * inv_nf;
-                  ((float*)pool.w)[gp] = w;
+                if (writable) {
+                  pool.row[pos] = (int32_t)r;
+                  pool.col[pos] = c0 + c;
+                  ((float*)pool.g)[pos] = __uint_as_float(v[c]) * inv_nf;
+                  ((float*)pool.w)[pos] = w;
                 }
                 ++pos;
               }
@@ -386,12 +399,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       if (row_count) atomicAdd(&pool.row_cnt[r], row_count);
       if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0 && chunk_id >= 0 && chunk_id < pool.nchunks)
+      pool.chunk_fill[chunk_id] = (unsigned long long)fill;
   }
   tc::tc_fence_before();
   tc::cluster_sync();
   tc::tc_fence_after();
   if (warp == 2) tc::tmem_dealloc<kTmemCols, 2>(tmem_base);
-  if (threadIdx.x == 0) pool.seg_cnt[blockIdx.x] = *seg_cur;
 }
 
 // per-256-column-block maxima of the filter's column constants
@@ -524,20 +538,23 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int64_t kdim, int sm_co
   const int num_n = (int)(plan->p_pad / BN);
   const int num_kb = (int)((kdim + BK - 1) / BK);
   const int grid = tc_grid_size(plan, sm_count);
-  if (pool.nseg != grid) return -1;
   // A group of <= 64 N-blocks (<= 32 MB of X^T_hi at n = 1000) stays in L2;
   // units small enough that the per-cluster imbalance is <= ~6% of its work
   const int group_n = num_n < 64 ? num_n : 64;
   const long long tiles = (long long)num_m * num_n;
   long long u = tiles / ((long long)(grid / 2) * 16);
   const int unit_n = (int)(u < 1 ? 1 : (u > group_n ? group_n : u));
+  // ACCORD_DEBUG_GEMM (diagnostics only; results are wrong when set):
+  // 1 = skip the epilogue, 2 = skip the MMAs
+  const char* dbg_env = std::getenv("ACCORD_DEBUG_GEMM");
+  const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0><<<grid, kThreads, Cfg<0>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, group_n, unit_n,
+        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, group_n, unit_n, dbg,
         ep, plan->blk_sdmax, om, pool);
   else
     gemm_tc_kernel<1><<<grid, kThreads, Cfg<1>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, group_n, unit_n,
+        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, group_n, unit_n, dbg,
         ep, plan->blk_sdmax, om, pool);
   return 1;
 }

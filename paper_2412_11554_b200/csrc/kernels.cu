@@ -191,19 +191,23 @@ __global__ void __launch_bounds__(1024) scan_phase3(const int32_t* __restrict__ 
 constexpr int kWarpSortMax = 1024;     // rows up to this length: one warp, smem bitonic
 constexpr int kBlockSortMax = 16384;   // rows up to this length: one block, smem bitonic
 
-// grid: (8 blocks per segment) x nseg
+// grid: (blocks per chunk) x chunks handed out
 __global__ void scatter_kernel(const int32_t* __restrict__ prow, const int32_t* __restrict__ pcol,
-                               const unsigned long long* __restrict__ seg_cnt, int64_t seg_cap,
+                               int64_t chunk, int64_t nchunks,
+                               const unsigned int* __restrict__ chunk_next,
+                               const unsigned long long* __restrict__ chunk_fill,
                                const int64_t* __restrict__ c_ptr, int32_t* rcur,
                                uint64_t* __restrict__ keys) {
-  const int64_t seg = blockIdx.y;
-  const int64_t cnt = min((int64_t)seg_cnt[seg], seg_cap);
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < cnt;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = seg * seg_cap + o;
-    const int32_t r = prow[i];
-    const int64_t pos = c_ptr[r] + atomicAdd(&rcur[r], 1);
-    keys[pos] = ((uint64_t)(uint32_t)pcol[i] << 32) | (uint64_t)(uint32_t)i;
+  const int64_t used = min((int64_t)*chunk_next, nchunks);
+  for (int64_t ch = blockIdx.y; ch < used; ch += gridDim.y) {
+    const int64_t cnt = min((int64_t)chunk_fill[ch], chunk);
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < cnt;
+         o += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = ch * chunk + o;
+      const int32_t r = prow[i];
+      const int64_t pos = c_ptr[r] + atomicAdd(&rcur[r], 1);
+      keys[pos] = ((uint64_t)(uint32_t)pcol[i] << 32) | (uint64_t)(uint32_t)i;
+    }
   }
 }
 
@@ -829,8 +833,13 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
                     int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col, void* c_g,
                     void* c_w, int32_t* long_rows, cudaStream_t st) {
   int launches = 0;
-  scatter_kernel<<<dim3(pool.nseg == 1 ? 148 * 8 : 8, (unsigned)pool.nseg), 256, 0, st>>>(
-      pool.row, pool.col, pool.seg_cnt, pool.seg_cap, c_ptr, rcur, keys);
+  {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(pool.chunk / 256, 148 * 8));
+    const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(pool.nchunks, 65535));
+    scatter_kernel<<<dim3(gx, gy), 256, 0, st>>>(pool.row, pool.col, pool.chunk, pool.nchunks,
+                                                 pool.chunk_next, pool.chunk_fill, c_ptr, rcur,
+                                                 keys);
+  }
   ++launches;
   {
     const int warps = 8;
