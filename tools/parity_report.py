@@ -1,0 +1,82 @@
+"""Parity report (test infrastructure): GPU path vs the float64 oracle on every
+BASELINE config, printed as one JSON document.
+
+  configs 1-2: full oracle (Algorithm 1 in float64), T from BASELINE.json
+  configs 3-5: sampled-row replay with the GPU's step schedule
+
+Run on the GPU box: python tools/parity_report.py > profiles/<round>/parity_report.json
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2412_11554_b200 as A  # noqa: E402
+from accord_inputs import get_config, make_problem  # noqa: E402
+from oracle import accord_oracle as O  # noqa: E402
+from tests.parity_util import compare_full  # noqa: E402
+from tests.test_gpu_fullsize import sample_rows  # noqa: E402
+
+
+def full(key, lam, gemm=A.GEMM_AUTO):
+    pr = make_problem(key)
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    X = torch.from_numpy(pr.Xt).cuda()
+    t0 = time.perf_counter()
+    with A.AccordSolver(X, lam, tau0=c.tau0, beta=c.beta, inv_L=inv_L, gemm=gemm) as s:
+        st = s.step(c.T)
+        csr = s.export_csr()
+        info = s.info()
+    tg = time.perf_counter() - t0
+    kind = "f64" if c.dtype == "f64" else "f32"
+    rep = compare_full(pr.Xt, lam, c.T, inv_L, csr.to_dense(c.p), st, kind)
+    rep.update(config=c.name, lam=lam, T=c.T, mode="full oracle", gemm=A.GEMM_NAMES[info["gemm"]],
+               gpu_seconds=tg, taus_equal=not rep["replayed"])
+    return rep
+
+
+def sampled(key):
+    cfg = get_config(key)
+    pr = make_problem(cfg)
+    lam = cfg.lambdas[0]
+    X = torch.from_numpy(pr.Xt).cuda()
+    with A.AccordSolver(X, lam, tau0=cfg.tau0, beta=cfg.beta, inv_L=0.0) as s:
+        st = s.step(cfg.T)
+        rows = sample_rows(pr)
+        csr = s.export_csr()
+        info = s.info()
+    del X
+    taus = [x["tau"] for x in st]
+    ref = O.fbs_rows(pr.Xt, rows, lam, taus)
+    W = ref["Omega_rows"]
+    G = np.zeros_like(W)
+    for q, i in enumerate(rows):
+        a, b = csr.row_ptr[i], csr.row_ptr[i + 1]
+        G[q, csr.col[a:b]] = csr.val[a:b]
+    scale = np.abs(W).max()
+    diff = (G != 0) != (W != 0)
+    exempt = np.abs(ref["margins"]) <= 1e-6
+    return dict(config=cfg.name, lam=lam, T=cfg.T, mode=f"sampled rows ({len(rows)})",
+                gemm=A.GEMM_NAMES[info["gemm"]], rel_err=float(np.abs(G - W).max() / scale),
+                support_mismatch=int(diff.sum()), support_exempt=int((diff & exempt).sum()),
+                bad_support=int((diff & ~exempt).sum()), taus=taus,
+                trials=[x["trials"] for x in st], nnz=int(st[-1]["nnz"]),
+                n_cand=int(st[-1]["n_cand"]))
+
+
+if __name__ == "__main__":
+    out = []
+    for lam in get_config(1).lambdas:
+        out.append(full(1, lam))
+    for lam in get_config(2).lambdas:
+        out.append(full(2, lam))
+    for key in (3, 4, 5):
+        out.append(sampled(key))
+    print(json.dumps(out, indent=1))
