@@ -39,6 +39,8 @@ import numpy as np
 __all__ = [
     "prox_diag", "soft_threshold", "prox", "g_value", "objective", "gradient",
     "spectral_bound", "kkt_residual", "fbs", "fbs_rows", "candidate_set",
+    "penalty_matrix", "epbic", "fit_path", "omega_to_theta", "theta_to_omega",
+    "partial_correlations",
 ]
 
 
@@ -69,11 +71,31 @@ def soft_threshold(x, a):
 
 def prox(Z, tau, lam, diag_cols):
     """Apply Eq. (3.5) to the forward-step values Z (rows of Omega - tau*G).
-    diag_cols[r] is the column of row r's diagonal entry."""
-    W = soft_threshold(Z, tau * lam)
+    diag_cols[r] is the column of row r's diagonal entry. `lam` is a scalar or
+    an entrywise penalty matrix (np.inf = entry fixed at 0, Eq. 3.8)."""
+    W = soft_threshold(Z, tau * np.asarray(lam))
     r = np.arange(Z.shape[0])
-    W[r, diag_cols] = prox_diag(Z[r, diag_cols], tau, lam)
+    lam_d = lam[r, diag_cols] if np.ndim(lam) == 2 else lam
+    W[r, diag_cols] = prox_diag(Z[r, diag_cols], tau, lam_d)
     return W
+
+
+def penalty_matrix(p, lam, mask=None, phi=1.0):
+    """Entrywise penalty of the bias-correction refit, Eq. (3.8)
+    (PAPER.md:384-398): phi*lam on the support mask S_hat (and the diagonal),
+    +inf (entry fixed at zero) off it. mask=None gives the plain lam."""
+    if mask is None:
+        return lam
+    L = np.where(mask, phi * lam, np.inf)
+    np.fill_diagonal(L, phi * lam)
+    return L
+
+
+def _l1(Omega, lam):
+    if np.ndim(lam) == 0:
+        return float(lam * np.abs(Omega).sum())
+    fin = np.isfinite(lam)
+    return float((lam[fin] * np.abs(Omega[fin])).sum())
 
 
 # ---------------------------------------------------------------------------
@@ -89,11 +111,13 @@ def g_value(Omega, Xt):
 
 def objective(Omega, Xt, lam):
     """f(Omega) = -log det Omega_D + 1/2 tr(Omega^T Omega S) + lam ||Omega||_1
-    (Eq. 3.2); +inf off the domain (omega_ii <= 0)."""
+    (Eq. 3.2); +inf off the domain (omega_ii <= 0). An
+    entrywise lam (Eq. 3.8) sums lam_ij |omega_ij| over finite entries (the
+    infinite ones are zero by construction)."""
     d = np.diag(Omega)
     if np.any(d <= 0):
         return float("inf")
-    return float(-np.log(d).sum() + g_value(Omega, Xt) + lam * np.abs(Omega).sum())
+    return float(-np.log(d).sum() + g_value(Omega, Xt) + _l1(Omega, lam))
 
 
 def gradient(Omega, Xt):
@@ -122,10 +146,15 @@ def kkt_residual(Omega, Xt, lam):
       zero off-diag:      max(0, |[Omega S]_ij| - lam)."""
     G = gradient(Omega, Xt)
     p = Omega.shape[0]
-    R = np.where(Omega != 0, np.abs(G + lam * np.sign(Omega)),
-                 np.maximum(0.0, np.abs(G) - lam))
+    lam = np.asarray(lam, dtype=np.float64)
+    with np.errstate(invalid="ignore"):
+        R = np.where(Omega != 0, np.abs(G + lam * np.sign(Omega)),
+                     np.maximum(0.0, np.abs(G) - lam))
+    if lam.ndim == 2:          # masked (Eq. 3.8): entries fixed at zero are skipped
+        R = np.where(np.isfinite(lam), R, 0.0)
     i = np.arange(p)
-    R[i, i] = np.abs(-1.0 / Omega[i, i] + G[i, i] + lam)
+    lam_d = lam[i, i] if lam.ndim == 2 else lam
+    R[i, i] = np.abs(-1.0 / Omega[i, i] + G[i, i] + lam_d)
     return float(R.max())
 
 
@@ -176,7 +205,7 @@ def fbs(Xt, lam, tau0=0.5, beta=0.5, inv_L=None, T=10, Omega0=None,
         Y = Om @ Xt                       # Y = Omega X^T
         G = (Y @ Xt.T) / n                # grad g = (1/n) Y X
         gO = float((Y * Y).sum() / (2 * n))
-        ncand.append(int(candidate_set(Om, G, lam).sum()))
+        ncand.append(int(candidate_set(Om, G, lam).sum()) if np.ndim(lam) == 0 else -1)
         tau = tau0 if tau_schedule is None else float(tau_schedule[t])
         k = 0
         while True:
@@ -198,7 +227,9 @@ def fbs(Xt, lam, tau0=0.5, beta=0.5, inv_L=None, T=10, Omega0=None,
                 break
             tau *= beta
         off = ~np.eye(p, dtype=bool)
-        margins = np.where(off, np.abs(Z) - tau * lam, np.inf)
+        with np.errstate(invalid="ignore"):
+            margins = np.where(off & np.isfinite(np.broadcast_to(lam, Z.shape)),
+                               np.abs(Z) - tau * np.asarray(lam), np.inf)
         Om = On
         taus.append(tau)
         trials.append(k)
@@ -259,3 +290,66 @@ def _y_times_x(Y, Xt, chunk):
     for s in range(0, p, chunk):
         out[:, s:s + chunk] = Y @ np.asarray(Xt[s:s + chunk], dtype=np.float64).T
     return out
+
+
+# ---------------------------------------------------------------------------
+# Tuning and post-processing
+# ---------------------------------------------------------------------------
+
+def epbic(Omega, Xt, gamma=0.5):
+    """Extended pseudo-BIC, Eq. (3.7):
+    2n{-log det Omega_D + 1/2 tr(Omega^T Omega S)} + ||Omega||_0 log n
+      + 4 gamma ||Omega||_0 log p,
+    ||Omega||_0 = number of nonzero OFF-diagonal entries."""
+    Xt = np.asarray(Xt, dtype=np.float64)
+    p, n = Xt.shape
+    loss = -np.log(np.diag(Omega)).sum() + g_value(Omega, Xt)
+    k = int((Omega != 0).sum() - np.count_nonzero(np.diag(Omega)))
+    return float(2 * n * loss + k * np.log(n) + 4 * gamma * k * np.log(p))
+
+
+def fit_path(Xt, lambdas, tau0=0.5, beta=0.5, inv_L=None, tol=1e-6, max_iter=500,
+             gamma=0.5):
+    """Regularisation path with warm starts: for each lambda
+    in the given order, run Algorithm 1 from the previous estimate until
+    ||Omega^(t+1) - Omega^(t)||_F < tol (reading R13) or max_iter, and score it
+    by epBIC (Eq. 3.7). Returns estimates, epBIC values, iteration counts and
+    the index of the minimum."""
+    Om = None
+    out = dict(Omega=[], epbic=[], iters=[], nnz_off=[])
+    if inv_L is None:
+        inv_L = 1.0 / spectral_bound(Xt)
+    for lam in lambdas:
+        it = 0
+        while it < max_iter:
+            r = fbs(Xt, lam, tau0, beta, inv_L, T=1, Omega0=Om)
+            d = np.linalg.norm(r["Omega"] - (np.eye(Xt.shape[0]) if Om is None else Om))
+            Om = r["Omega"]
+            it += 1
+            if d < tol:
+                break
+        out["Omega"].append(Om)
+        out["epbic"].append(epbic(Om, Xt, gamma))
+        out["iters"].append(it)
+        out["nnz_off"].append(int((Om != 0).sum() - Om.shape[0]))
+    out["best"] = int(np.argmin(out["epbic"]))
+    return out
+
+
+def theta_to_omega(Theta):
+    """T: Theta -> Theta_D^{-1/2} Theta (PAPER.md:151-156)."""
+    return Theta / np.sqrt(np.diag(Theta))[:, None]
+
+
+def omega_to_theta(Omega):
+    """T^{-1}: Omega -> Omega_D Omega."""
+    return np.diag(Omega)[:, None] * Omega
+
+
+def partial_correlations(Omega):
+    """rho_ij = -1/2 (omega_ij / omega_jj + omega_ji / omega_ii), i != j
+    (PAPER.md:167-169); symmetric, zero diagonal."""
+    d = np.diag(Omega)
+    R = -0.5 * (Omega / d[None, :] + Omega.T / d[:, None])
+    np.fill_diagonal(R, 0.0)
+    return R
