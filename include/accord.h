@@ -206,6 +206,42 @@ accord_status accord_export_csr(accord_ctx* ctx, int32_t scope, int64_t* row_ptr
 accord_status accord_set_omega_csr(accord_ctx* ctx, const int64_t* row_ptr,
                                    const int32_t* col, const void* val, int64_t nnz);
 
+/* Change lambda (keeps Omega: warm start for a path).
+ * Collective (recomputes the global objective). */
+accord_status accord_set_lambda(accord_ctx* ctx, double lambda);
+
+/* Bias-correction refit, Eq. (3.8): freeze S_hat = the
+ * support of the current estimate (diagonal included) and continue
+ * Algorithm 1 with penalty phi*lambda on S_hat and +inf (entries fixed at 0)
+ * off it; 0 <= phi <= 1. The gradient is then needed only on S_hat and comes
+ * from the SDDMM (no GEMM). Collective. */
+accord_status accord_refit(accord_ctx* ctx, double phi);
+
+/* Run Algorithm 1 until ||Omega^(t+1) - Omega^(t)||_F < tol or max_iter
+ * iterations (reading R13). Collective. */
+accord_status accord_solve(accord_ctx* ctx, int32_t max_iter, double tol, int32_t* iters_done,
+                           accord_iter_stats* last);
+
+/* KKT certificate (Eq. 3.3; supp. :985-997) of the current
+ * iterate: max over all entries of | -1/omega_ii + [Omega S]_ii + lambda |,
+ * | [Omega S]_ij + lambda sign omega_ij | (nonzero), max(0, |[Omega S]_ij| -
+ * lambda) (zero). Entries outside the candidate set have |[Omega S]_ij| <=
+ * lambda by the filter's certificate and contribute 0; under a refit, entries
+ * off S_hat are skipped. Costs one gradient pass. Collective. */
+accord_status accord_kkt_residual(accord_ctx* ctx, double* kkt);
+
+/* Regularisation path with warm starts and epBIC selection (Eq. 3.7,
+ * PAPER.md:360-377): for j = 0..k-1 (lambdas in the given order, normally
+ * descending) set lambda_j, solve to tol / max_iter from the previous
+ * estimate, record epBIC_j = 2n(-log det Omega_D + ||Omega X^T||^2/2n)
+ * + k_j (log n + 4 gamma log p), k_j = number of nonzero off-diagonal
+ * entries, and the iterations used. On return the context holds the
+ * epBIC-minimising estimate and its lambda; *best = its index. Any output
+ * pointer may be NULL. Collective. */
+accord_status accord_path(accord_ctx* ctx, const double* lambdas, int32_t k, int32_t max_iter,
+                          double tol, double gamma, double* epbic, int64_t* nnz_off,
+                          int32_t* iters, int32_t* best);
+
 /* Per-row line-search summands of the LAST trial evaluated by accord_step
  * (||D_i||^2, ||Delta_i||^2, i = local row indices). For sampled-row parity. */
 accord_status accord_row_stats(accord_ctx* ctx, const int64_t* rows, int64_t count,

@@ -101,7 +101,9 @@ _LIB = None
 EXPORTED = ["accord_default_params", "accord_create", "accord_step", "accord_objective",
             "accord_export_csr", "accord_set_omega_csr", "accord_row_stats",
             "accord_get_info", "accord_nccl_unique_id", "accord_destroy",
-            "accord_status_string", "accord_last_error", "accord_abi_version"]
+            "accord_status_string", "accord_last_error", "accord_abi_version",
+            "accord_set_lambda", "accord_refit", "accord_solve", "accord_kkt_residual",
+            "accord_path"]
 
 
 def lib():
@@ -125,6 +127,14 @@ def lib():
                                        C.c_int64]
     L.accord_row_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
     L.accord_get_info.argtypes = [C.c_void_p, C.POINTER(Info)]
+    L.accord_set_lambda.argtypes = [C.c_void_p, C.c_double]
+    L.accord_refit.argtypes = [C.c_void_p, C.c_double]
+    L.accord_solve.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.POINTER(C.c_int32),
+                               C.POINTER(IterStats)]
+    L.accord_kkt_residual.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.accord_path.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double,
+                              C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.POINTER(C.c_int32)]
     L.accord_nccl_unique_id.argtypes = [C.c_void_p]
     L.accord_destroy.argtypes = [C.c_void_p]
     L.accord_destroy.restype = None
@@ -289,6 +299,39 @@ class AccordSolver:
         vv = np.ascontiguousarray(val, dtype=self.dtype)
         _check(lib().accord_set_omega_csr(self.ctx, rp.ctypes.data, cc.ctypes.data,
                                           vv.ctypes.data, int(rp[-1])), self.ctx)
+
+    def set_lambda(self, lam):
+        _check(lib().accord_set_lambda(self.ctx, float(lam)), self.ctx)
+
+    def refit(self, phi=0.0):
+        """Bias-correction refit (Eq. 3.8) on the current support."""
+        _check(lib().accord_refit(self.ctx, float(phi)), self.ctx)
+
+    def solve(self, max_iter=1000, tol=1e-8):
+        it = C.c_int32()
+        st = IterStats()
+        _check(lib().accord_solve(self.ctx, int(max_iter), float(tol), C.byref(it),
+                                  C.byref(st)), self.ctx)
+        return it.value, st.as_dict()
+
+    def kkt_residual(self):
+        v = C.c_double()
+        _check(lib().accord_kkt_residual(self.ctx, C.byref(v)), self.ctx)
+        return v.value
+
+    def path(self, lambdas, max_iter=1000, tol=1e-8, gamma=0.5):
+        """Warm-started lambda path with epBIC (Eq. 3.7); leaves the selected
+        estimate in the context."""
+        lam = np.ascontiguousarray(lambdas, dtype=np.float64)
+        k = len(lam)
+        e = np.zeros(k)
+        nz = np.zeros(k, dtype=np.int64)
+        it = np.zeros(k, dtype=np.int32)
+        best = C.c_int32()
+        _check(lib().accord_path(self.ctx, lam.ctypes.data, k, int(max_iter), float(tol),
+                                 float(gamma), e.ctypes.data, nz.ctypes.data, it.ctypes.data,
+                                 C.byref(best)), self.ctx)
+        return dict(epbic=e, nnz_off=nz, iters=it, best=best.value)
 
     def row_stats(self, rows):
         r = np.ascontiguousarray(rows, dtype=np.int64)

@@ -98,11 +98,22 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
                 void* Yout, __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A,
                 float* row_B, double* row_D2, double* row_Y2, cudaStream_t st);
 
-// Exact candidate values (BF16_FILTER): c_g[e] = (1/n) sum_m Y_im Xt_km in
-// float64 accumulation, for every entry of C (block per row).
-int launch_refine(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
-                  const int32_t* c_col, const float* Y, const float* Xt, float* c_g,
+// Exact candidate values: c_g[e] = (1/n) sum_m Y_im Xt_km in float64
+// accumulation, for every entry of C (block per row). BF16_FILTER refine and
+// the fixed-support gradient of the refit.
+int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
+                  const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
                   cudaStream_t st);
+
+// c_w[e] = omega_{i, c_col[e]} (0 if absent) on the structure (c_ptr, c_col).
+int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
+                  const int64_t* om_ptr, const int32_t* om_col, const void* om_val, void* c_w,
+                  cudaStream_t st);
+
+// KKT residual (Eq. 3.3) over C with penalty lam: row maxima -> *out (device).
+int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+               const void* c_g, const void* c_w, double lam, double* row_max, double* out,
+               cudaStream_t st);
 
 // Per-column constants of the filter bound from Xt (f32).
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st);

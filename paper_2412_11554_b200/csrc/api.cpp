@@ -136,12 +136,18 @@ struct accord_ctx {
   TcGemmPlan* plan = nullptr;
   cudaEvent_t ev[8] = {};
 
+  // bias-correction refit (Eq. 3.8): fixed support S_hat, penalty phi * lambda
+  bool refit = false;
+  double phi = 1.0;
+  int64_t* refit_ptr = nullptr;
+  int32_t* refit_col = nullptr;
+  int64_t refit_nnz = 0;
   // optional per-kernel tracing (ACCORD_TRACE=1): events after each launch,
   // printed to stderr at the end of every iteration
   bool trace = false;
   std::vector<cudaEvent_t> tr_pool;
   std::vector<std::pair<const char*, cudaEvent_t>> tr_marks;
-  int64_t launches = 0, gemm_launches = 0, iters = 0, nnz_local = 0;
+  int64_t launches = 0, gemm_launches = 0, iters = 0, nnz_local = 0, nnz_global = 0;
   double f = 0, parts[3] = {0, 0, 0};
   std::vector<void*> allocs;
   size_t bytes = 0;
@@ -184,6 +190,22 @@ void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
   if (c->world > 1 && c->comm == ACCORD_COMM_HOST) {
     if (c->ar(c->cu, h_buf, count) != 0) throw Fail{ACCORD_E_COMM, "host allreduce failed"};
   }
+}
+
+// Global maximum of one value per rank (KKT certificate).
+double allreduce_max(accord_ctx* c, double* d_val) {
+  double h = 0;
+  if (c->world > 1 && c->comm == ACCORD_COMM_NCCL)
+    NK(nccl_api()->AllReduce(d_val, d_val, 1, ncclDouble, ncclMax, c->nccl, c->st));
+  CK(cudaMemcpyAsync(&h, d_val, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->world > 1 && c->comm == ACCORD_COMM_HOST) {
+    std::vector<double> v(c->world, 0.0);
+    v[c->rank] = h;
+    if (c->ar(c->cu, v.data(), c->world) != 0) throw Fail{ACCORD_E_COMM, "host allreduce failed"};
+    h = *std::max_element(v.begin(), v.end());
+  }
+  return h;
 }
 
 OmegaView omega_view(accord_ctx* c) { return OmegaView{c->om_ptr, c->om_col, c->om_val}; }
@@ -252,10 +274,11 @@ void refresh_objective(accord_ctx* c) {
   CK(cudaMemcpyAsync(c->red_d, loc, sizeof(loc), cudaMemcpyHostToDevice, c->st));
   allreduce(c, c->red_d, c->h_red, 8);
   const bool bad_any = c->h_red[7] > 0;
+  c->nnz_global = (int64_t)c->h_red[5];
   const double* r = c->h_red;
   c->parts[0] = -r[2];
   c->parts[1] = r[3] / (2.0 * (double)c->n);
-  c->parts[2] = c->lam * r[4];
+  c->parts[2] = (c->refit ? c->phi * c->lam : c->lam) * r[4];
   c->f = c->parts[0] + c->parts[1] + c->parts[2];
   if (bad_any) throw Fail{ACCORD_E_DOMAIN, "Omega has a missing or nonpositive diagonal entry"};
 }
@@ -523,11 +546,31 @@ float ev_ms(accord_ctx* c, int a, int b) {
   return ms;
 }
 
-void step_one(accord_ctx* c, accord_iter_stats* s) {
-  accord_iter_stats st{};
+double lam_eff(const accord_ctx* c) { return c->refit ? c->phi * c->lam : c->lam; }
+
+// Candidate set C with exact gradient values G on it and the current omega:
+// either the GEMM + fused epilogue + finalize (+ refine) of a plain iteration,
+// or, for the bias-correction refit (Eq. 3.8), the fixed support S_hat with G
+// from the SDDMM (entries off S_hat carry an infinite penalty and stay 0).
+void build_candidates(accord_ctx* c, accord_iter_stats& st) {
   cudaStream_t S = c->st;
-  CK(cudaEventRecord(c->ev[0], S));
-  TR(c, "start");
+  if (c->refit) {
+    CK(cudaEventRecord(c->ev[1], S));
+    CK(cudaEventRecord(c->ev[2], S));
+    CK(cudaMemcpyAsync(c->c_ptr, c->refit_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, S));
+    CK(cudaMemcpyAsync(c->c_col, c->refit_col, c->refit_nnz * 4, cudaMemcpyDeviceToDevice, S));
+    c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
+                                 c->om_val, c->c_w, S);
+    CK(cudaEventRecord(c->ev[3], S));
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
+                                 c->Y[c->cur], c->Xt, c->c_g, S);
+    CK(cudaEventRecord(c->ev[4], S));
+    TR(c, "refit_sddmm");
+    CK(cudaEventSynchronize(c->ev[4]));
+    st.ms_finalize = ev_ms(c, 2, 3);
+    st.ms_refine = ev_ms(c, 3, 4);
+    return;
+  }
   // ---------------- a2 + a3: gradient GEMM with the fused epilogue --------
   for (;;) {
     CK(cudaMemsetAsync(c->row_cnt, 0, c->pk * 4, S));
@@ -597,15 +640,23 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   TR(c, "finalize");
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) {
     // exact values of the filtered candidates: G_ik = <Y_i, X_k> / n (f64 accumulation)
-    c->launches += launch_refine(c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
-                                 (const float*)c->Y[c->cur], (const float*)c->Xt,
-                                 (float*)c->c_g, S);
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
+                                 c->Y[c->cur], c->Xt, c->c_g, S);
   }
   CK(cudaEventRecord(c->ev[4], S));
   TR(c, "refine");
   CK(cudaEventSynchronize(c->ev[4]));
   st.ms_finalize = ev_ms(c, 2, 3);
   st.ms_refine = ev_ms(c, 3, 4);
+}
+
+void step_one(accord_ctx* c, accord_iter_stats* s) {
+  accord_iter_stats st{};
+  cudaStream_t S = c->st;
+  CK(cudaEventRecord(c->ev[0], S));
+  TR(c, "start");
+  build_candidates(c, st);
+  const double lam = lam_eff(c);
   // ---------------- a5-a7: line search ----------------
   const int nb = c->cur ^ 1;
   double tau = c->tau0;
@@ -614,7 +665,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
     st.trials++;
     CK(cudaEventRecord(c->ev[4], S));
     c->launches += launch_prox(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, c->c_w,
-                               c->c_wn, tau, c->lam, c->row_dd, c->row_l1, c->row_logd,
+                               c->c_wn, tau, lam, c->row_dd, c->row_l1, c->row_logd,
                                c->row_nnz, S);
     CK(cudaEventRecord(c->ev[5], S));
     TR(c, "prox");
@@ -665,9 +716,10 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   CK(cudaEventRecord(c->ev[7], S));
   CK(cudaEventSynchronize(c->ev[7]));
   c->nnz_local = nnz_loc;
+  c->nnz_global = (int64_t)r[5];
   c->parts[0] = -r[2];
   c->parts[1] = r[3] / (2.0 * (double)c->n);
-  c->parts[2] = c->lam * r[4];
+  c->parts[2] = lam * r[4];
   c->f = c->parts[0] + c->parts[1] + c->parts[2];
   c->iters++;
   st.tau = tau;
@@ -895,6 +947,134 @@ accord_status accord_set_omega_csr(accord_ctx* c, const int64_t* row_ptr, const 
     c->nnz_local = nnz;
     recompute_y(c);
     refresh_objective(c);
+  });
+}
+
+accord_status accord_set_lambda(accord_ctx* c, double lambda) {
+  if (!c) return ACCORD_E_INVALID;
+  if (!(lambda >= 0) || !std::isfinite(lambda)) {
+    c->err = "lambda must be finite and >= 0";
+    return ACCORD_E_INVALID;
+  }
+  return guard(c, [&] {
+    c->lam = lambda;
+    refresh_objective(c);
+  });
+}
+
+accord_status accord_refit(accord_ctx* c, double phi) {
+  if (!c) return ACCORD_E_INVALID;
+  if (!(phi >= 0 && phi <= 1)) {
+    c->err = "phi must be in [0, 1] (Eq. 3.8)";
+    return ACCORD_E_INVALID;
+  }
+  return guard(c, [&] {
+    // S_hat = support of the current estimate (diagonal always stored)
+    c->dfree(c->refit_ptr, (c->pk + 1) * 8);
+    c->dfree(c->refit_col, c->refit_nnz * 4);
+    c->refit_nnz = c->nnz_local;
+    c->refit_ptr = c->dalloc<int64_t>(c->pk + 1);
+    c->refit_col = c->dalloc<int32_t>(std::max<int64_t>(c->refit_nnz, 1));
+    CK(cudaMemcpyAsync(c->refit_ptr, c->om_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice,
+                       c->st));
+    CK(cudaMemcpyAsync(c->refit_col, c->om_col, c->refit_nnz * 4, cudaMemcpyDeviceToDevice,
+                       c->st));
+    c->refit = true;
+    c->phi = phi;
+    refresh_objective(c);
+  });
+}
+
+accord_status accord_solve(accord_ctx* c, int32_t max_iter, double tol, int32_t* iters_done,
+                           accord_iter_stats* last) {
+  if (!c || max_iter < 0 || !(tol >= 0)) return ACCORD_E_INVALID;
+  return guard(c, [&] {
+    accord_iter_stats st{};
+    int32_t it = 0;
+    while (it < max_iter) {
+      step_one(c, &st);
+      ++it;
+      if (st.delta_fro < tol) break;   // ||Omega^(t+1) - Omega^(t)||_F < tol (reading R13)
+    }
+    if (iters_done) *iters_done = it;
+    if (last) *last = st;
+  });
+}
+
+accord_status accord_kkt_residual(accord_ctx* c, double* kkt) {
+  if (!c || !kkt) return ACCORD_E_INVALID;
+  return guard(c, [&] {
+    accord_iter_stats st{};
+    build_candidates(c, st);
+    c->launches += launch_kkt(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, c->c_w,
+                              lam_eff(c), c->row_dd, c->red_d + 8, c->st);
+    CK(cudaGetLastError());
+    *kkt = allreduce_max(c, c->red_d + 8);
+  });
+}
+
+accord_status accord_path(accord_ctx* c, const double* lambdas, int32_t k, int32_t max_iter,
+                          double tol, double gamma, double* epbic, int64_t* nnz_off,
+                          int32_t* iters, int32_t* best) {
+  if (!c || !lambdas || k < 1 || max_iter < 1 || !(gamma >= 0)) return ACCORD_E_INVALID;
+  return guard(c, [&] {
+    const size_t T = c->tsz;
+    int64_t* bptr = c->dalloc<int64_t>(c->pk + 1);
+    int32_t* bcol = nullptr;
+    void* bval = nullptr;
+    int64_t bcap = 0, bnnz = 0;
+    double best_e = INFINITY, best_lam = c->lam;
+    int32_t bi = 0;
+    for (int32_t j = 0; j < k; ++j) {
+      if (!(lambdas[j] >= 0) || !std::isfinite(lambdas[j]))
+        throw Fail{ACCORD_E_INVALID, "bad lambda in the path"};
+      c->lam = lambdas[j];
+      refresh_objective(c);                       // warm start from the previous estimate
+      accord_iter_stats st{};
+      int32_t it = 0;
+      while (it < max_iter) {
+        step_one(c, &st);
+        ++it;
+        if (st.delta_fro < tol) break;
+      }
+      // epBIC, Eq. (3.7): 2n (loss) + ||Omega||_0 (log n + 4 gamma log p), off-diagonal count
+      const double loss = c->parts[0] + c->parts[1];
+      const int64_t koff = c->nnz_global - c->p;
+      const double e = 2.0 * (double)c->n * loss +
+                       (double)koff * (std::log((double)c->n) + 4.0 * gamma * std::log((double)c->p));
+      if (epbic) epbic[j] = e;
+      if (nnz_off) nnz_off[j] = koff;
+      if (iters) iters[j] = it;
+      if (e < best_e) {
+        best_e = e;
+        best_lam = lambdas[j];
+        bi = j;
+        if (c->nnz_local > bcap) {
+          c->dfree(bcol, bcap * 4);
+          c->dfree(bval, bcap * T);
+          bcap = c->nnz_local + c->nnz_local / 4 + 16;
+          bcol = c->dalloc<int32_t>(bcap);
+          bval = c->dalloc_bytes(bcap * T);
+        }
+        bnnz = c->nnz_local;
+        CK(cudaMemcpyAsync(bptr, c->om_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(bcol, c->om_col, bnnz * 4, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(bval, c->om_val, bnnz * T, cudaMemcpyDeviceToDevice, c->st));
+      }
+    }
+    // restore the epBIC-selected estimate (and its lambda)
+    CK(cudaMemcpyAsync(c->om_ptr, bptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->om_col, bcol, bnnz * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->om_val, bval, bnnz * T, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->dfree(bptr, (c->pk + 1) * 8);
+    c->dfree(bcol, bcap * 4);
+    c->dfree(bval, bcap * T);
+    c->nnz_local = bnnz;
+    c->lam = best_lam;
+    recompute_y(c);
+    refresh_objective(c);
+    if (best) *best = bi;
   });
 }
 

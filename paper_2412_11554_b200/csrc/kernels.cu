@@ -525,53 +525,114 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// BF16_FILTER refinement: exact candidate values, warp per entry, Y_i staged
-// in shared memory, float64 accumulation. c_g[e] = (1/n) <Y_i, Xt_k>.
+// Exact candidate values (BF16_FILTER refine, and the gradient on a fixed
+// support for the bias-correction refit): c_g[e] = (1/n) <Y_i, Xt_k> with
+// float64 accumulation; warp per candidate, Y_i staged in shared memory.
 // ---------------------------------------------------------------------------
-constexpr int kRefineMaxK = 4096;   // samples per row staged in smem (ldk <= 4096)
-
+template <typename T>
 __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
                                                      const int64_t* __restrict__ c_ptr,
                                                      const int32_t* __restrict__ c_col,
-                                                     const float* __restrict__ Y,
-                                                     const float* __restrict__ Xt,
-                                                     float* __restrict__ c_g) {
-  __shared__ __align__(16) float ys[kRefineMaxK];
+                                                     const T* __restrict__ Y,
+                                                     const T* __restrict__ Xt,
+                                                     T* __restrict__ c_g) {
+  using VT = typename Vec<T>::type;
+  constexpr int V = Vec<T>::V;
+  extern __shared__ __align__(16) uint8_t ys_raw[];
+  T* ys = reinterpret_cast<T*>(ys_raw);
   const int64_t r = blockIdx.x;
   const int64_t beg = c_ptr[r], end = c_ptr[r + 1];
   if (beg == end) return;
-  for (int64_t m = threadIdx.x * 4; m < ldk; m += blockDim.x * 4)
-    *reinterpret_cast<float4*>(ys + m) = *reinterpret_cast<const float4*>(Y + r * ldk + m);
+  for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V)
+    *reinterpret_cast<VT*>(ys + m) = *reinterpret_cast<const VT*>(Y + r * ldk + m);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double inv_n = 1.0 / (double)n;
+  constexpr int kStep = 32 * V;           // elements per lane-pass over the row
   for (int64_t e = beg + wid; e < end; e += nw) {
-    const float* xr = Xt + (int64_t)c_col[e] * ldk;
+    const T* xr = Xt + (int64_t)c_col[e] * ldk;
     double s = 0.0;
-    int64_t m = lane * 4;
-    for (; m + 3 * 128 < ldk; m += 4 * 128) {
-      float4 x[4];
+    int64_t m = lane * V;
+    for (; m + 7 * kStep < ldk; m += 8 * kStep) {   // 8 loads in flight per lane
+      VT x[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(xr + m + u * 128));
+      for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const VT*>(xr + m + u * kStep));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float4 yv = *reinterpret_cast<const float4*>(ys + m + u * 128);
-        s = fma((double)yv.x, (double)x[u].x, s);
-        s = fma((double)yv.y, (double)x[u].y, s);
-        s = fma((double)yv.z, (double)x[u].z, s);
-        s = fma((double)yv.w, (double)x[u].w, s);
+      for (int u = 0; u < 8; ++u) {
+        const VT yv = *reinterpret_cast<const VT*>(ys + m + u * kStep);
+#pragma unroll
+        for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
       }
     }
-    for (; m < ldk; m += 128) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(xr + m));
-      const float4 yv = *reinterpret_cast<const float4*>(ys + m);
-      s = fma((double)yv.x, (double)x.x, s);
-      s = fma((double)yv.y, (double)x.y, s);
-      s = fma((double)yv.z, (double)x.z, s);
-      s = fma((double)yv.w, (double)x.w, s);
+    for (; m < ldk; m += kStep) {
+      const VT x = __ldg(reinterpret_cast<const VT*>(xr + m));
+      const VT yv = *reinterpret_cast<const VT*>(ys + m);
+#pragma unroll
+      for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
     }
     s = warp_sum(s);
-    if (lane == 0) c_g[e] = (float)(s * inv_n);
+    if (lane == 0) c_g[e] = (T)(s * inv_n);
+  }
+}
+
+// Values of Omega on a fixed structure (refit support): c_w[e] = omega_{i, c_col[e]}
+// or 0. Warp per row, binary search in Omega's sorted row.
+template <typename T>
+__global__ void lookup_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
+                              const int32_t* __restrict__ c_col, const int64_t* __restrict__ om_ptr,
+                              const int32_t* __restrict__ om_col, const T* __restrict__ om_val,
+                              T* __restrict__ c_w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const int64_t ob = om_ptr[r], oe = om_ptr[r + 1];
+  for (int64_t e = c_ptr[r] + lane; e < c_ptr[r + 1]; e += 32) {
+    const int32_t k = c_col[e];
+    int64_t lo = ob, hi = oe;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (om_col[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    c_w[e] = (lo < oe && om_col[lo] == k) ? om_val[lo] : T(0);
+  }
+}
+
+// KKT residual of Eq. (3.3) over the candidate set, per row:
+//   diagonal |-1/w + G + lam|, nonzero |G + lam sign w|, zero max(0, |G| - lam).
+// Entries outside C have |G| <= lam (certified by the GEMM epilogue) and
+// contribute 0; on a refit support, entries outside it are fixed at zero.
+template <typename T>
+__global__ void kkt_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
+                           const int32_t* __restrict__ c_col, const T* __restrict__ c_g,
+                           const T* __restrict__ c_w, double lam, double* __restrict__ row_max) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  double mx = 0.0;
+  for (int64_t e = c_ptr[r] + lane; e < c_ptr[r + 1]; e += 32) {
+    const double g = (double)c_g[e], w = (double)c_w[e];
+    double v;
+    if (c_col[e] == r0 + r) v = fabs(-1.0 / w + g + lam);
+    else if (w != 0.0) v = fabs(g + copysign(lam, w));
+    else v = fmax(0.0, fabs(g) - lam);
+    mx = fmax(mx, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) row_max[r] = mx;
+}
+
+__global__ void __launch_bounds__(1024) reduce_max_kernel(int64_t pk, const double* __restrict__ v,
+                                                          double* out) {
+  __shared__ double sh[32];
+  double mx = 0.0;
+  for (int64_t r = threadIdx.x; r < pk; r += blockDim.x) mx = fmax(mx, v[r]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+    *out = mx;
   }
 }
 
@@ -909,11 +970,55 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
   return 1;
 }
 
-int launch_refine(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
-                  const float* Y, const float* Xt, float* c_g, cudaStream_t st) {
+int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
+                  const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
+                  cudaStream_t st) {
   if (pk == 0) return 0;
-  refine_kernel<<<(unsigned)pk, 256, 0, st>>>(pk, n, ldk, c_ptr, c_col, Y, Xt, c_g);
+  const size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(refine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(refine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  if (dtype == ACCORD_F64)
+    refine_kernel<double><<<(unsigned)pk, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                           (const double*)Y, (const double*)Xt,
+                                                           (double*)c_g);
+  else
+    refine_kernel<float><<<(unsigned)pk, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                          (const float*)Y, (const float*)Xt,
+                                                          (float*)c_g);
   return 1;
+}
+
+int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
+                  const int64_t* om_ptr, const int32_t* om_col, const void* om_val, void* c_w,
+                  cudaStream_t st) {
+  const unsigned g = (unsigned)((pk + 7) / 8);
+  if (dtype == ACCORD_F64)
+    lookup_kernel<double><<<g, 256, 0, st>>>(pk, c_ptr, c_col, om_ptr, om_col,
+                                             (const double*)om_val, (double*)c_w);
+  else
+    lookup_kernel<float><<<g, 256, 0, st>>>(pk, c_ptr, c_col, om_ptr, om_col,
+                                            (const float*)om_val, (float*)c_w);
+  return 1;
+}
+
+int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+               const void* c_g, const void* c_w, double lam, double* row_max, double* out,
+               cudaStream_t st) {
+  const unsigned g = (unsigned)((pk + 7) / 8);
+  if (dtype == ACCORD_F64)
+    kkt_kernel<double><<<g, 256, 0, st>>>(pk, r0, c_ptr, c_col, (const double*)c_g,
+                                          (const double*)c_w, lam, row_max);
+  else
+    kkt_kernel<float><<<g, 256, 0, st>>>(pk, r0, c_ptr, c_col, (const float*)c_g,
+                                         (const float*)c_w, lam, row_max);
+  reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
+  return 2;
 }
 
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st) {
