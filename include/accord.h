@@ -13,10 +13,15 @@
  *                                                      (reading R8)
  *   Omega is asymmetric, the l1 norm covers the diagonal (Eq. 3.2).
  *
- * Data layout and sharding: X is replicated on every rank; rank k owns the
- * contiguous row block [row_begin, row_end) of Omega (rows separate,
- * PAPER.md:948-957, and Alg. 1 couples them only through tau_t). Collectives
- * carry only the per-trial line-search sums (8 doubles) and the export gather.
+ * Data layout and sharding: rank k owns the contiguous row block
+ * [row_begin, row_end) of Omega (rows separate, and Alg. 1
+ * couples them only through tau_t). X is either replicated on every rank
+ * (default; collectives then carry only the per-trial line-search sums, 8
+ * doubles, and the export gather) or, for X beyond one GPU's memory, sharded
+ * by variables (x_sharded = 1: rank k holds the columns [row_begin, row_end)
+ * of X, and every pass that needs all of X (gradient GEMM, candidate refine,
+ * SpMM) visits the slabs in a ring, the 1DMM scheme of Alg. 2,
+ * PAPER.md:326-356).
  *
  * Conventions for every call:
  *   - No C++ exception crosses the ABI. Every call returns an accord_status;
@@ -37,7 +42,7 @@
 extern "C" {
 #endif
 
-#define ACCORD_ABI_VERSION 1
+#define ACCORD_ABI_VERSION 2
 
 typedef enum {
   ACCORD_OK = 0,
@@ -93,6 +98,11 @@ typedef int (*accord_allreduce_fn)(void* user, double* buf, int32_t count);
  * with ACCORD_COMM_HOST. */
 typedef int (*accord_allgatherv_fn)(void* user, const void* in, int64_t in_bytes,
                                     void* out, int64_t* counts);
+/* Ring exchange of host buffers (x_sharded with ACCORD_COMM_HOST): send
+ * send_bytes from `send` to rank dst and receive recv_bytes from rank src into
+ * `recv` (all ranks call together). Return 0 on success. */
+typedef int (*accord_sendrecv_fn)(void* user, const void* send, int64_t send_bytes, int32_t dst,
+                                  void* recv, int64_t recv_bytes, int32_t src);
 
 typedef struct {
   int32_t abi_version;      /* must be ACCORD_ABI_VERSION */
@@ -120,6 +130,14 @@ typedef struct {
   void* comm_user;                   /* passed to the callbacks */
   void* stream;             /* cudaStream_t to order all work on (NULL = legacy default stream) */
   int64_t cand_capacity;    /* initial candidate-pool capacity in entries (0 = auto); grows on demand */
+  int32_t x_sharded;        /* 0: X holds all p variables (replicated on every rank).
+                               1: X holds only this rank's variables [row_begin, row_end)
+                               (n x p_k samples-major or p_k x n variables-major); the
+                               rank blocks must tile [0, p) in rank order, each starting at
+                               a multiple of 256. Collective passes over X run as a ring
+                               (Alg. 2): NCCL send/recv on a split
+                               communicator, or `sendrecv` with ACCORD_COMM_HOST. */
+  accord_sendrecv_fn sendrecv;       /* ACCORD_COMM_HOST with x_sharded */
 } accord_init_params;
 
 /* Per accepted outer iteration (one element per iteration of accord_step). */
@@ -198,6 +216,28 @@ accord_status accord_objective(accord_ctx* ctx, double* f, double* parts);
 accord_status accord_export_csr(accord_ctx* ctx, int32_t scope, int64_t* row_ptr,
                                 int32_t* col, void* val, int64_t capacity,
                                 int64_t* nnz_out, int32_t on_device);
+
+typedef enum {
+  ACCORD_EXPORT_OMEGA = 0,  /* Omega-hat itself (same as accord_export_csr) */
+  ACCORD_EXPORT_THETA = 1,  /* Theta-hat = T^{-1}(Omega-hat) = Omega_D Omega: theta_ij = omega_ii omega_ij
+                               (PAPER.md:151-156, :166); same CSR structure as Omega */
+  ACCORD_EXPORT_PCORR = 2   /* partial correlations rho-hat_ij = -1/2 (omega_ij / omega_jj + omega_ji / omega_ii),
+                               i != j: symmetric, stored on supp(Omega) U supp(Omega^T)
+                               off the diagonal (no diagonal entries) */
+} accord_export_kind;
+
+/* Post-processing of the current estimate on the device (SURVEY.md §8(f)
+ * NEXT(4)). Same conventions as accord_export_csr (two-call size query,
+ * sorted columns, rows = local block for LOCAL and p for GATHER, buffers
+ * host or device per on_device); values in the context dtype, computed in
+ * double. PCORR needs the transpose, so it gathers Omega (collective for any
+ * scope when world > 1); THETA with LOCAL scope is rank-local. Each call
+ * recomputes (a size query costs the same as the export). Errors:
+ * ACCORD_E_DOMAIN (a diagonal entry <= 0), ACCORD_E_CAPACITY, ACCORD_E_INVALID
+ * (bad kind or scope), ACCORD_E_CUDA, ACCORD_E_NCCL, ACCORD_E_COMM. */
+accord_status accord_export_transformed(accord_ctx* ctx, int32_t kind, int32_t scope,
+                                        int64_t* row_ptr, int32_t* col, void* val,
+                                        int64_t capacity, int64_t* nnz_out, int32_t on_device);
 
 /* Warm start / resume: replace this rank's rows of Omega by a host CSR
  * (local rows, global sorted columns, context dtype). Validates a positive

@@ -26,12 +26,15 @@ F32, F64 = 0, 1
 GEMM_AUTO, GEMM_BF16X3, GEMM_SIMT, GEMM_BF16_FILTER = 0, 1, 2, 3
 COMM_NONE, COMM_NCCL, COMM_HOST = 0, 1, 2
 SCOPE_LOCAL, SCOPE_GATHER = 0, 1
+EXPORT_OMEGA, EXPORT_THETA, EXPORT_PCORR = 0, 1, 2
 GEMM_NAMES = {GEMM_AUTO: "auto", GEMM_BF16X3: "bf16x3_tcgen05", GEMM_SIMT: "simt",
               GEMM_BF16_FILTER: "bf16_filter_tcgen05+sddmm"}
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int32)
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                             C.POINTER(C.c_int64))
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                          C.c_int64, C.c_int32)
 
 
 class InitParams(C.Structure):
@@ -49,6 +52,7 @@ class InitParams(C.Structure):
         ("allreduce", ALLREDUCE_FN), ("allgatherv", ALLGATHERV_FN),
         ("comm_user", C.c_void_p), ("stream", C.c_void_p),
         ("cand_capacity", C.c_int64),
+        ("x_sharded", C.c_int32), ("sendrecv", SENDRECV_FN),
     ]
 
 
@@ -103,7 +107,7 @@ EXPORTED = ["accord_default_params", "accord_create", "accord_step", "accord_obj
             "accord_get_info", "accord_nccl_unique_id", "accord_destroy",
             "accord_status_string", "accord_last_error", "accord_abi_version",
             "accord_set_lambda", "accord_refit", "accord_solve", "accord_kkt_residual",
-            "accord_path"]
+            "accord_path", "accord_export_transformed"]
 
 
 def lib():
@@ -123,6 +127,9 @@ def lib():
     L.accord_objective.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.accord_export_csr.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int64, C.POINTER(C.c_int64), C.c_int32]
+    L.accord_export_transformed.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_int64,
+                                            C.POINTER(C.c_int64), C.c_int32]
     L.accord_set_omega_csr.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_int64]
     L.accord_row_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
@@ -206,12 +213,16 @@ class AccordSolver:
 
     X: torch tensor (CUDA or CPU) or numpy array. layout: "variables" (p x n,
     X^T) or "samples" (n x p, the paper's X). The library copies X.
+    x_sharded=True (with p_global and a communicator): X holds only this
+    rank's variables [row_begin, row_end) and every pass over X runs as a ring
+    of slab exchanges (Alg. 2; include/accord.h `x_sharded`).
     """
 
     def __init__(self, X, lam, *, layout="variables", tau0=0.5, beta=0.5, inv_L=0.0,
                  row_begin=0, row_end=None, rank=0, world=1, comm=COMM_NONE,
                  nccl_id: bytes | None = None, allreduce=None, allgatherv=None,
-                 gemm=GEMM_AUTO, cand_capacity=0, stream=None, device=None):
+                 gemm=GEMM_AUTO, cand_capacity=0, stream=None, device=None,
+                 x_sharded=False, p_global=None, sendrecv=None):
         import torch
         L = lib()
         self._keep = []
@@ -224,6 +235,13 @@ class AccordSolver:
         lay = LAYOUT_VARIABLES if layout.startswith("var") else LAYOUT_SAMPLES
         p = X.shape[0] if lay == LAYOUT_VARIABLES else X.shape[1]
         n = X.shape[1] if lay == LAYOUT_VARIABLES else X.shape[0]
+        if x_sharded:
+            # X holds this rank's variables [row_begin, row_end) only (NEXT(3))
+            if row_end is None or p_global is None:
+                raise ValueError("x_sharded needs row_begin, row_end and p_global")
+            if p != int(row_end) - int(row_begin):
+                raise ValueError("sharded X must hold exactly the rank's variables")
+            p = int(p_global)
         prm = InitParams()
         L.accord_default_params(C.byref(prm))
         if device is None:
@@ -253,6 +271,11 @@ class AccordSolver:
             cb2 = ALLGATHERV_FN(allgatherv)
             self._keep.append(cb2)
             prm.allgatherv = cb2
+        if sendrecv is not None:
+            cb3 = SENDRECV_FN(sendrecv)
+            self._keep.append(cb3)
+            prm.sendrecv = cb3
+        prm.x_sharded = 1 if x_sharded else 0
         if stream is None:
             stream = torch.cuda.current_stream(prm.device)
         prm.stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
@@ -292,6 +315,23 @@ class AccordSolver:
                                    val.ctypes.data, nnz.value, C.byref(nnz), 0), self.ctx)
         rb = self.row_begin if (scope == SCOPE_LOCAL or self.world == 1) else 0
         return CSR(rp, col[:nnz.value], val[:nnz.value], rb)
+
+    def export_transformed(self, kind, scope=SCOPE_LOCAL) -> CSR:
+        """Theta-hat = Omega_D Omega (EXPORT_THETA) or the partial correlations
+        (EXPORT_PCORR), computed on the device (accord_export_transformed)."""
+        nnz = C.c_int64()
+        L = lib()
+        _check(L.accord_export_transformed(self.ctx, kind, scope, None, None, None, 0,
+                                           C.byref(nnz), 0), self.ctx)
+        local = scope == SCOPE_LOCAL or self.world == 1
+        rows = (self.row_end - self.row_begin) if local else self.p
+        rp = np.zeros(rows + 1, dtype=np.int64)
+        col = np.zeros(max(1, nnz.value), dtype=np.int32)
+        val = np.zeros(max(1, nnz.value), dtype=self.dtype)
+        _check(L.accord_export_transformed(self.ctx, kind, scope, rp.ctypes.data,
+                                           col.ctypes.data, val.ctypes.data, nnz.value,
+                                           C.byref(nnz), 0), self.ctx)
+        return CSR(rp, col[:nnz.value], val[:nnz.value], self.row_begin if local else 0)
 
     def set_omega_csr(self, row_ptr, col, val):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)

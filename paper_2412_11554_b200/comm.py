@@ -9,9 +9,11 @@ and the export gather through other transports:
   one-GPU emulation of P ranks: the kernels never wait on each other, only
   the host threads meet at a barrier).
 
-Each exposes `allreduce(user, buf, count)` and `allgatherv(user, in, in_bytes,
-out, counts)` with the C callback signatures; pass them to AccordSolver
-(comm=COMM_HOST, allreduce=..., allgatherv=...).
+Each exposes `allreduce(user, buf, count)`, `allgatherv(user, in, in_bytes,
+out, counts)` and `sendrecv(user, send, send_bytes, dst, recv, recv_bytes,
+src)` (the ring of the sharded-X mode) with the C callback signatures; pass
+them to AccordSolver (comm=COMM_HOST, allreduce=..., allgatherv=...,
+sendrecv=...).
 """
 from __future__ import annotations
 
@@ -70,6 +72,27 @@ class TorchDistComm:
             return 1
 
 
+    def sendrecv(self, user, send, send_bytes, dst, recv, recv_bytes, src):
+        """Ring exchange (sharded-X mode) over torch.distributed point-to-point."""
+        import torch
+        try:
+            out = torch.from_numpy(np.ctypeslib.as_array(
+                C.cast(send, C.POINTER(C.c_uint8)), shape=(send_bytes,)).copy()) \
+                if send_bytes else torch.zeros(0, dtype=torch.uint8)
+            inb = torch.zeros(recv_bytes, dtype=torch.uint8)
+            ops = [self.dist.P2POp(self.dist.isend, out, dst, group=self.group),
+                   self.dist.P2POp(self.dist.irecv, inb, src, group=self.group)]
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+            if recv_bytes:
+                dstv = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)),
+                                             shape=(recv_bytes,))
+                dstv[:] = inb.numpy()
+            return 0
+        except Exception:
+            return 1
+
+
 class ThreadComm:
     """P ranks = P host threads of one process (one context each)."""
 
@@ -115,6 +138,24 @@ class ThreadComm:
                 dst = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_uint8)),
                                             shape=(len(blob),))
                 dst[:] = np.frombuffer(blob, dtype=np.uint8)
+            return 0
+        except Exception:
+            return 1
+
+    def sendrecv(self, user, send, send_bytes, dst, recv, recv_bytes, src):
+        """Ring exchange of the sharded-X mode: every rank deposits its block
+        for `dst` and takes the one `src` deposited for it."""
+        try:
+            mine = bytes(np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)),
+                                               shape=(send_bytes,))) if send_bytes else b""
+            vals = self._exchange((dst, mine))
+            to, blob = vals[src]
+            if to != self.tls.rank or len(blob) != recv_bytes:
+                return 1
+            if recv_bytes:
+                dstv = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)),
+                                             shape=(recv_bytes,))
+                dstv[:] = np.frombuffer(blob, dtype=np.uint8)
             return 0
         except Exception:
             return 1

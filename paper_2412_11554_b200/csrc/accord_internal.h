@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <functional>
 #include <string>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -44,6 +45,10 @@ struct PoolView {             // candidate pool written by the GEMM epilogue (un
 
 struct EpiParams {            // candidate rule of the fused epilogue
   int64_t pk, p, r0;          // local rows, columns, global index of local row 0
+  // columns [col_base, col_end) of this launch; the B operand (X^T rows) holds
+  // exactly these, row 0 = column col_base (all p columns unless X is sharded
+  // and this is one step of the ring, NEXT(3)); col_base is a multiple of 256
+  int64_t col_base, col_end;
   double inv_n;
   double lam_cand;            // emit (i,k) iff k == i, or omega_ik != 0, or |g| > lam_cand
   // BF16_FILTER only: per-entry rigorous error bound of the single-pass bf16
@@ -69,9 +74,13 @@ int launch_split_bf16(const float* src, int64_t elems, __nv_bfloat16* hi,
 
 // Power iteration for L = lambda_max(X^T X / n) on Xt (p x ldk). Deterministic.
 // Returns launches; writes the estimate to *L_host (synchronizes).
+// With X sharded by variables (NEXT(3)), p = this rank's variables, p_global
+// = all, and `ar` sums a device vector of doubles across ranks in place
+// (stream-ordered; returns false on failure).
+using DevAllreduce = std::function<bool(double* dev, int count)>;
 int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk,
                     int max_iter, double tol, double* L_host, cudaStream_t st,
-                    std::string* err);
+                    std::string* err, int64_t p_global = 0, const DevAllreduce* ar = nullptr);
 
 // Exclusive scan: out[0..N] (out[N] = total) from int32 counts.
 int launch_scan_i32(const int32_t* in, int64_t* out, int64_t N, void* tmp, size_t tmp_bytes,
@@ -83,6 +92,32 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
                     int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col,
                     void* c_g, void* c_w, int32_t* long_rows, cudaStream_t st);
 
+// Sort every CSR row segment of 64-bit keys ascending (warp bitonic for rows
+// <= 1024, block bitonic + merge path above). long_rows: int32[rows + 1],
+// zeroed by the caller; tmp: scratch of the same size as keys.
+int launch_rowsort(int64_t rows, const int64_t* ptr, uint64_t* keys, uint64_t* tmp,
+                   int32_t* long_rows, cudaStream_t st);
+
+// NEXT(4) post-processing on the GLOBAL CSR of Omega (postproc.cu):
+// d[i] = omega_{i, i + off} for the CSR's rows (bad = 1 if some omega_ii <= 0);
+// theta_ij = omega_ii omega_ij
+// on rows [a, b) (output indexed from ptr[a]); partial correlations rho on
+// supp(Omega) U supp(Omega^T) off the diagonal, rows [a, b): count -> scan ->
+// fill keys -> launch_rowsort -> values.
+int launch_diag(int dtype, int64_t rows, int64_t off, const int64_t* ptr, const int32_t* col,
+                const void* val, double* d, int32_t* bad, cudaStream_t st);
+int launch_theta(int dtype, int64_t a, int64_t b, const int64_t* ptr, const int32_t* col,
+                 const void* val, const double* d, void* out, cudaStream_t st);
+int launch_pcorr_count(int dtype, int64_t p, int64_t a, int64_t b, const int64_t* ptr,
+                       const int32_t* col, const void* val, int32_t* own, int32_t* cnt,
+                       cudaStream_t st);
+int launch_pcorr_fill(int dtype, int64_t p, int64_t a, int64_t b, const int64_t* ptr,
+                      const int32_t* col, const void* val, const int32_t* own,
+                      const int64_t* optr, int32_t* ext, uint64_t* keys, cudaStream_t st);
+int launch_pcorr_value(int dtype, int64_t a, int64_t b, const int64_t* ptr, const int32_t* col,
+                       const void* val, const double* d, const int64_t* optr,
+                       const uint64_t* keys, int32_t* ocol, void* oval, cudaStream_t st);
+
 // Prox at trial tau over C (Eq. 3.5) with per-row partial sums.
 int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
                 const void* c_g, const void* c_w, void* c_wn, double tau, double lam,
@@ -93,17 +128,25 @@ int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const i
 // NULL (Delta = 0). Accumulates in double; writes Y (T), optionally its bf16
 // hi (and lo) copies with the per-row norms ||y||, ||y - bf16(y)||, and the
 // per-row ||D_i||^2, ||Y+_i||^2.
+struct SpmmRing {             // one ring step of the sharded-X SpMM (NEXT(3))
+  int64_t v0, v1;             // columns of the resident slab; Xt row 0 = column v0
+  double* yacc;               // [pk x ldk] partial Y+ across the ring steps (NULL: plain SpMM)
+  double* dacc;               // [pk x ldk] partial D
+  int first, last;            // first step initialises, last step finalises (Y, norms)
+};
 int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* ptr,
                 const int32_t* col, const void* wn, const void* wo, const void* Xt,
                 void* Yout, __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A,
-                float* row_B, double* row_D2, double* row_Y2, cudaStream_t st);
+                float* row_B, double* row_D2, double* row_Y2, cudaStream_t st,
+                const SpmmRing* ring = nullptr);
 
 // Exact candidate values: c_g[e] = (1/n) sum_m Y_im Xt_km in float64
 // accumulation, for every entry of C (block per row). BF16_FILTER refine and
 // the fixed-support gradient of the refit.
+// Columns [v0, v1) only, Xt row 0 = column v0 (one ring step of the sharded mode).
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
-                  cudaStream_t st);
+                  cudaStream_t st, int64_t v0 = 0, int64_t v1 = INT64_MAX);
 
 // c_w[e] = omega_{i, c_col[e]} (0 if absent) on the structure (c_ptr, c_col).
 int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
@@ -150,14 +193,18 @@ struct TcGemmPlan;   // opaque: tensor maps for both Y buffers
 TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            const __nv_bfloat16* Yhi1, const __nv_bfloat16* Ylo1,
                            int64_t pk_pad, const __nv_bfloat16* Xhi,
-                           const __nv_bfloat16* Xlo, int64_t p_pad, int64_t ldk,
-                           std::string* err);
+                           const __nv_bfloat16* Xlo, int64_t xrows_pad, int64_t p_pad,
+                           int64_t kdim, int64_t ldk, std::string* err);
 void tc_plan_destroy(TcGemmPlan*);
 // per-256-column maxima of the filter's column constants (after launch_col_norms)
 int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st);
 int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs
+// B operand idx 1/2 = ring buffers of the sharded mode (rows_pad x ldk bf16)
+bool tc_plan_set_b(TcGemmPlan* plan, int idx, const __nv_bfloat16* hi, const __nv_bfloat16* lo,
+                   int64_t rows_pad, std::string* err);
+// columns [ep.col_base, ep.col_end) against B operand `bsel`
 int launch_gemm_tc(TcGemmPlan* plan, int mode /* accord_gemm: BF16X3 or BF16_FILTER */,
-                   int ybuf, int64_t kdim, int sm_count, const EpiParams& ep,
+                   int ybuf, int bsel, int sm_count, const EpiParams& ep,
                    const OmegaView& om, const PoolView& pool, cudaStream_t st);
 bool tc_supported(int cc_major, int cc_minor);
 

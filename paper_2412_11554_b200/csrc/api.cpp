@@ -50,6 +50,9 @@ struct NcclApi {
                             cudaStream_t);
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
   ncclResult_t (*GroupStart)();
   ncclResult_t (*GroupEnd)();
   ncclResult_t (*CommDestroy)(ncclComm_t);
@@ -67,6 +70,7 @@ NcclApi* nccl_api() {
 #define SYM(name) api.name = (decltype(api.name))dlsym(h, "nccl" #name)
     SYM(GetUniqueId); SYM(CommInitRank); SYM(AllReduce); SYM(AllGather); SYM(Broadcast);
     SYM(GroupStart); SYM(GroupEnd); SYM(CommDestroy); SYM(GetErrorString);
+    SYM(Send); SYM(Recv); SYM(CommSplit);   // ring of the sharded mode (checked at use)
 #undef SYM
     ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather &&
          api.Broadcast && api.GroupStart && api.GroupEnd && api.CommDestroy &&
@@ -98,6 +102,23 @@ struct accord_ctx {
   accord_allgatherv_fn agv = nullptr;
   void* cu = nullptr;
   ncclComm_t nccl = nullptr;
+
+  // X sharded by variables (NEXT(3), 1DMM ring of Alg. 2): Xt holds this
+  // rank's slab (columns [r0, r1)); vb[q] .. vb[q+1] is rank q's slab
+  bool sharded = false;
+  int64_t xrows_pad = 0;                   // rows of Xt / Xhi / Xlo
+  std::vector<int64_t> vb;
+  void* rbuf[2] = {nullptr, nullptr};      // ring buffers (f32/f64), max slab rows
+  __nv_bfloat16* rhi[2] = {nullptr, nullptr};
+  __nv_bfloat16* rlo[2] = {nullptr, nullptr};
+  int64_t rrows_pad = 0;
+  double *yacc = nullptr, *dacc = nullptr; // SpMM partial sums across the ring steps
+  cudaStream_t cs = nullptr;               // ring transfers (NCCL)
+  cudaEvent_t ev_comp[2] = {}, ev_recv[2] = {};
+  ncclComm_t nccl_ring = nullptr;          // split communicator for the ring
+  accord_sendrecv_fn sr = nullptr;
+  void *h_send = nullptr, *h_recv = nullptr;   // pinned staging (ACCORD_COMM_HOST)
+  int64_t ring_steps = 0;                  // slab exchanges so far (diagnostic)
 
   void* Xt = nullptr;
   __nv_bfloat16 *Xhi = nullptr, *Xlo = nullptr;
@@ -208,11 +229,120 @@ double allreduce_max(accord_ctx* c, double* d_val) {
   return h;
 }
 
+// Sum a device vector of doubles across ranks in place (stream-ordered for
+// NCCL; the host transport synchronizes). Power iteration of the sharded mode.
+void dev_allreduce(accord_ctx* c, double* d, int count) {
+  if (c->world == 1) return;
+  if (c->comm == ACCORD_COMM_NCCL) {
+    NK(nccl_api()->AllReduce(d, d, count, ncclDouble, ncclSum, c->nccl, c->st));
+    return;
+  }
+  std::vector<double> h(count);
+  CK(cudaMemcpyAsync(h.data(), d, count * 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->ar(c->cu, h.data(), count) != 0) throw Fail{ACCORD_E_COMM, "host allreduce failed"};
+  CK(cudaMemcpyAsync(d, h.data(), count * 8, cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+}
+
 OmegaView omega_view(accord_ctx* c) { return OmegaView{c->om_ptr, c->om_col, c->om_val}; }
 
 PoolView pool_view(accord_ctx* c) {
   return PoolView{c->pool_row, c->pool_col, c->pool_g, c->pool_w, c->chunk, c->nchunks,
                   c->chunk_next, c->chunk_fill, c->row_cnt};
+}
+
+// ---- X sharded by variables: the ring over the slabs (NEXT(3), Alg. 2) ----
+// At ring step s this rank holds slab j = (rank + s) mod P (the variables
+// [vb[j], vb[j+1]) of X, variable-major); while step s computes on it, slab
+// j+1 arrives from rank+1 and slab j leaves for rank-1 (the
+// 1DMM rotation, here of the X slabs, since Omega's rows stay put). NCCL
+// transfers run on their own stream and communicator and overlap the
+// compute; the host-callback transport (tests) is synchronous.
+int64_t slab_rows(const accord_ctx* c, int q) { return c->vb[q + 1] - c->vb[q]; }
+
+void ring_exchange(accord_ctx* c, int s, const void* slab, int j) {
+  const int P = c->world;
+  const int jn = (j + 1) % P;
+  const size_t sb = (size_t)slab_rows(c, j) * c->ldk * c->tsz;
+  const size_t rb = (size_t)slab_rows(c, jn) * c->ldk * c->tsz;
+  const int left = (c->rank + P - 1) % P, right = (c->rank + 1) % P;
+  void* target = c->rbuf[s & 1];
+  c->ring_steps++;
+  if (c->comm == ACCORD_COMM_NCCL) {
+    NcclApi* api = nccl_api();
+    // rbuf[s & 1] was the resident slab of step s-1: wait until that step's
+    // kernels (and its bf16 split) are done with it
+    if (s >= 2) CK(cudaStreamWaitEvent(c->cs, c->ev_comp[s & 1], 0));
+    NK(api->GroupStart());
+    NK(api->Send(slab, sb, ncclChar, left, c->nccl_ring, c->cs));
+    NK(api->Recv(target, rb, ncclChar, right, c->nccl_ring, c->cs));
+    NK(api->GroupEnd());
+    CK(cudaEventRecord(c->ev_recv[s & 1], c->cs));
+  } else {
+    CK(cudaMemcpyAsync(c->h_send, slab, sb, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (c->sr(c->cu, c->h_send, (int64_t)sb, left, c->h_recv, (int64_t)rb, right) != 0)
+      throw Fail{ACCORD_E_COMM, "host sendrecv failed"};
+    CK(cudaMemcpyAsync(target, c->h_recv, rb, cudaMemcpyHostToDevice, c->st));
+  }
+}
+
+// fn(slab, bsel, v0, v1, first, last): Xt rows of the columns [v0, v1) at
+// `slab`; bsel = the GEMM B operand holding its bf16 copy (when want_bf16).
+// Collective: every rank runs the P steps.
+template <typename F>
+void ring_pass(accord_ctx* c, bool want_bf16, F&& fn) {
+  const int P = c->world;
+  for (int s = 0; s < P; ++s) {
+    const int j = (c->rank + s) % P;
+    const void* slab = s == 0 ? c->Xt : c->rbuf[(s - 1) & 1];
+    if (s + 1 < P) ring_exchange(c, s, slab, j);
+    int bsel = 0;
+    if (s > 0) {
+      const int b = (s - 1) & 1;
+      if (c->comm == ACCORD_COMM_NCCL) CK(cudaStreamWaitEvent(c->st, c->ev_recv[b], 0));
+      if (want_bf16) {
+        c->launches += launch_split_bf16((const float*)c->rbuf[b],
+                                         round_up(slab_rows(c, j), kRowPad) * c->ldk, c->rhi[b],
+                                         c->rlo[b], c->st);
+        bsel = 1 + b;
+      }
+    }
+    fn(slab, bsel, c->vb[j], c->vb[j + 1], s == 0, s == P - 1);
+    if (s > 0) CK(cudaEventRecord(c->ev_comp[(s - 1) & 1], c->st));
+  }
+}
+
+// SpMM Y+ = W X^T (and D = (W - Wold) X^T) over all of X: one launch, or a
+// ring pass accumulating in float64 when X is sharded.
+void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void* wn,
+              const void* wo, int yb, double* row_D2, double* row_Y2) {
+  if (!c->sharded) {
+    c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, ptr, col, wn, wo, c->Xt, c->Y[yb],
+                               c->Yhi[yb], c->Ylo[yb], c->row_A[yb], c->row_B[yb], row_D2,
+                               row_Y2, c->st);
+    return;
+  }
+  ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool first, bool last) {
+    SpmmRing rg{v0, v1, c->yacc, c->dacc, first ? 1 : 0, last ? 1 : 0};
+    c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, ptr, col, wn, wo, slab, c->Y[yb],
+                               c->Yhi[yb], c->Ylo[yb], c->row_A[yb], c->row_B[yb], row_D2,
+                               row_Y2, c->st, &rg);
+  });
+}
+
+// Exact candidate values c_g = (1/n) <Y_i, X_k> over all of X.
+void refine_all(accord_ctx* c) {
+  if (!c->sharded) {
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
+                                 c->Y[c->cur], c->Xt, c->c_g, c->st);
+    return;
+  }
+  ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
+                                 c->Y[c->cur], slab, c->c_g, c->st, v0, v1);
+  });
 }
 
 // (Re)allocate the entry-indexed arrays for capacity `cap`, preserving Omega.
@@ -285,9 +415,7 @@ void refresh_objective(accord_ctx* c) {
 
 // Y = Omega X^T for the current Omega into Y[cur] (+ row norms).
 void recompute_y(accord_ctx* c) {
-  c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, c->om_ptr, c->om_col, c->om_val,
-                             nullptr, c->Xt, c->Y[c->cur], c->Yhi[c->cur], c->Ylo[c->cur],
-                             c->row_A[c->cur], c->row_B[c->cur], nullptr, c->row_Y2, c->st);
+  spmm_all(c, c->om_ptr, c->om_col, c->om_val, nullptr, c->cur, nullptr, c->row_Y2);
 }
 
 void validate(const accord_init_params* prm) {
@@ -301,7 +429,9 @@ void validate(const accord_init_params* prm) {
   if (prm->layout != ACCORD_LAYOUT_SAMPLES_ROW_MAJOR &&
       prm->layout != ACCORD_LAYOUT_VARIABLES_ROW_MAJOR)
     bad("bad layout");
-  const int64_t minld = prm->layout == ACCORD_LAYOUT_SAMPLES_ROW_MAJOR ? prm->p : prm->n;
+  const bool shard = prm->x_sharded && prm->world > 1;
+  const int64_t pv = shard ? prm->row_end - prm->row_begin : prm->p;   // variables held
+  const int64_t minld = prm->layout == ACCORD_LAYOUT_SAMPLES_ROW_MAJOR ? pv : prm->n;
   if (prm->ldx != 0 && prm->ldx < minld) bad("ldx smaller than the row length");
   if (!(prm->lambda >= 0) || !std::isfinite(prm->lambda)) bad("lambda must be finite and >= 0");
   if (!(prm->tau0 > 0) || !std::isfinite(prm->tau0)) bad("tau0 must be > 0");
@@ -313,10 +443,43 @@ void validate(const accord_init_params* prm) {
   if (prm->world > 1 && prm->comm == ACCORD_COMM_NONE) bad("world > 1 needs a communicator");
   if (prm->comm == ACCORD_COMM_NCCL && prm->world > 1 && !prm->nccl_id) bad("nccl_id is NULL");
   if (prm->comm == ACCORD_COMM_HOST && !prm->allreduce) bad("allreduce callback is NULL");
+  if (shard && prm->comm == ACCORD_COMM_HOST && !prm->sendrecv)
+    bad("x_sharded with the host communicator needs a sendrecv callback");
+  if (shard && prm->row_begin % kRowPad != 0)
+    bad("x_sharded: row_begin must be a multiple of 256");
   if (prm->gemm < ACCORD_GEMM_AUTO || prm->gemm > ACCORD_GEMM_BF16_FILTER) bad("bad gemm kind");
   if (prm->dtype == ACCORD_F64 &&
       (prm->gemm == ACCORD_GEMM_BF16X3 || prm->gemm == ACCORD_GEMM_BF16_FILTER))
     bad("tensor-core GEMM kinds need dtype F32");
+}
+
+// All ranks' per-column filter constants into every rank's col_sd[p]
+// (sharded mode; each rank computed its slab's at col_sd + r0).
+void gather_col_sd(accord_ctx* c) {
+  const int P = c->world;
+  if (c->comm == ACCORD_COMM_NCCL) {
+    NcclApi* api = nccl_api();
+    NK(api->GroupStart());
+    for (int q = 0; q < P; ++q)
+      NK(api->Broadcast(c->col_sd + c->vb[q], c->col_sd + c->vb[q],
+                        (size_t)slab_rows(c, q) * sizeof(float2), ncclChar, q, c->nccl, c->st));
+    NK(api->GroupEnd());
+    CK(cudaStreamSynchronize(c->st));
+    return;
+  }
+  if (!c->agv) throw Fail{ACCORD_E_INVALID, "x_sharded with host comm needs allgatherv"};
+  std::vector<float2> mine(c->pk), all(c->p);
+  CK(cudaMemcpyAsync(mine.data(), c->col_sd + c->r0, c->pk * sizeof(float2),
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  std::vector<int64_t> counts(P, 0);
+  const int64_t bytes = c->pk * (int64_t)sizeof(float2);
+  if (c->agv(c->cu, mine.data(), bytes, nullptr, counts.data()) != 0 ||
+      c->agv(c->cu, mine.data(), bytes, all.data(), counts.data()) != 0)
+    throw Fail{ACCORD_E_COMM, "allgatherv failed"};
+  CK(cudaMemcpyAsync(c->col_sd, all.data(), c->p * sizeof(float2), cudaMemcpyHostToDevice,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
 }
 
 void create_impl(accord_ctx* c, const accord_init_params* prm) {
@@ -374,12 +537,51 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     std::memcpy(&id, prm->nccl_id, sizeof(id));
     NK(api->CommInitRank(&c->nccl, c->world, id, c->rank));
   }
+  c->red_d = c->dalloc<double>(16);
+
+  // ---- X sharded by variables (NEXT(3)): every rank's slab boundaries ----
+  c->sharded = prm->x_sharded && c->world > 1;
+  if (c->sharded) {
+    const int P = c->world;
+    std::vector<double> mine(2 * P, 0.0), tot(2 * P, 0.0);
+    mine[2 * c->rank] = (double)c->r0;
+    mine[2 * c->rank + 1] = (double)c->r1;
+    for (int q = 0; q < 2 * P; q += 8) {
+      const int cnt = std::min(8, 2 * P - q);
+      CK(cudaMemcpyAsync(c->red_d, mine.data() + q, cnt * 8, cudaMemcpyHostToDevice, c->st));
+      allreduce(c, c->red_d, c->h_red, cnt);
+      std::memcpy(tot.data() + q, c->h_red, cnt * 8);
+    }
+    c->vb.assign(P + 1, 0);
+    for (int q = 0; q < P; ++q) {
+      c->vb[q] = (int64_t)tot[2 * q];
+      if (q > 0 && (int64_t)tot[2 * q] != (int64_t)tot[2 * q - 1])
+        throw Fail{ACCORD_E_INVALID, "x_sharded: rank blocks must tile [0, p) in rank order"};
+    }
+    c->vb[P] = (int64_t)tot[2 * P - 1];
+    if (c->vb[0] != 0 || c->vb[P] != c->p)
+      throw Fail{ACCORD_E_INVALID, "x_sharded: rank blocks must tile [0, p) in rank order"};
+    if (c->comm == ACCORD_COMM_NCCL) {
+      NcclApi* api = nccl_api();
+      if (!api->Send || !api->Recv || !api->CommSplit)
+        throw Fail{ACCORD_E_NCCL, "NCCL without send/recv/split"};
+      NK(api->CommSplit(c->nccl, 0, c->rank, &c->nccl_ring, nullptr));
+      CK(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_recv[b], cudaEventDisableTiming));
+      }
+    }
+    c->sr = prm->sendrecv;
+  }
+  const int64_t pv = c->sharded ? c->pk : c->p;   // variables held in Xt
+  c->xrows_pad = c->sharded ? c->pk_pad : c->p_pad;
 
   // ---- X -> Xt (variable-major, padded), finiteness check ----
   const size_t T = c->tsz;
-  c->Xt = c->dalloc_bytes((size_t)c->p_pad * c->ldk * T);
-  const int64_t rows_src = prm->layout == ACCORD_LAYOUT_SAMPLES_ROW_MAJOR ? c->n : c->p;
-  const int64_t cols_src = prm->layout == ACCORD_LAYOUT_SAMPLES_ROW_MAJOR ? c->p : c->n;
+  c->Xt = c->dalloc_bytes((size_t)c->xrows_pad * c->ldk * T);
+  const int64_t rows_src = prm->layout == ACCORD_LAYOUT_SAMPLES_ROW_MAJOR ? c->n : pv;
+  const int64_t cols_src = prm->layout == ACCORD_LAYOUT_SAMPLES_ROW_MAJOR ? pv : c->n;
   const int64_t ldx = prm->ldx ? prm->ldx : cols_src;
   const void* Xsrc = prm->X;
   void* staging = nullptr;
@@ -392,7 +594,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   unsigned long long* badidx = c->dalloc<unsigned long long>(1);
   CK(cudaMemsetAsync(badidx, 0xff, 8, c->st));
   c->launches += launch_load_xt(c->dtype, Xsrc, prm->x_on_device ? ldx : cols_src, prm->layout,
-                                c->n, c->p, c->Xt, c->ldk, c->p_pad, badidx, c->st);
+                                c->n, pv, c->Xt, c->ldk, c->xrows_pad, badidx, c->st);
   unsigned long long hb = 0;
   CK(cudaMemcpyAsync(&hb, badidx, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -413,7 +615,12 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     std::string e;
     // power iteration from the all-ones start, relative tolerance,
     // then a safety inflation (overestimating L is safe, underestimating is not)
-    int l = power_iteration(c->dtype, c->Xt, c->p, c->n, c->ldk, 600, 1e-8, &L, c->st, &e);
+    DevAllreduce ar = [c](double* d, int count) {
+      dev_allreduce(c, d, count);
+      return true;
+    };
+    int l = power_iteration(c->dtype, c->Xt, pv, c->n, c->ldk, 600, 1e-8, &L, c->st, &e, c->p,
+                            c->sharded ? &ar : nullptr);
     if (l < 0) throw Fail{ACCORD_E_CUDA, e};
     c->launches += l;
     c->L = L * (1.0 + 2e-3);
@@ -427,15 +634,10 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     CK(cudaMemsetAsync(c->Y[b], 0, (size_t)c->pk_pad * c->ldk * T, c->st));
   }
   if (tc) {
-    c->Xhi = c->dalloc<__nv_bfloat16>((size_t)c->p_pad * c->ldk);
-    c->Xlo = c->dalloc<__nv_bfloat16>((size_t)c->p_pad * c->ldk);   // scratch when !x3
-    c->launches += launch_split_bf16((const float*)c->Xt, c->p_pad * c->ldk, c->Xhi, c->Xlo,
+    c->Xhi = c->dalloc<__nv_bfloat16>((size_t)c->xrows_pad * c->ldk);
+    if (x3) c->Xlo = c->dalloc<__nv_bfloat16>((size_t)c->xrows_pad * c->ldk);
+    c->launches += launch_split_bf16((const float*)c->Xt, c->xrows_pad * c->ldk, c->Xhi, c->Xlo,
                                      c->st);
-    if (!x3) {
-      CK(cudaStreamSynchronize(c->st));
-      c->dfree(c->Xlo, (size_t)c->p_pad * c->ldk * 2);
-      c->Xlo = nullptr;
-    }
     for (int b = 0; b < 2; ++b) {
       c->Yhi[b] = c->dalloc<__nv_bfloat16>((size_t)c->pk_pad * c->ldk);
       CK(cudaMemsetAsync(c->Yhi[b], 0, (size_t)c->pk_pad * c->ldk * 2, c->st));
@@ -447,15 +649,47 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
       c->row_B[b] = c->dalloc<float>(c->pk);
     }
     if (filt) {
+      // per-column constants of the filter bound for all p columns (the
+      // sharded mode computes its slab's and gathers the rest)
       c->col_sd = c->dalloc<float2>(c->p);
-      c->launches += launch_col_norms(c->p, c->ldk, (const float*)c->Xt, c->col_sd, c->st);
+      const int64_t off = c->sharded ? c->r0 : 0;
+      c->launches += launch_col_norms(pv, c->ldk, (const float*)c->Xt, c->col_sd + off, c->st);
+      if (c->sharded) gather_col_sd(c);
     }
     std::string e;
     c->plan = tc_plan_create(c->Yhi[0], x3 ? c->Ylo[0] : c->Yhi[0], c->Yhi[1],
                              x3 ? c->Ylo[1] : c->Yhi[1], c->pk_pad, c->Xhi,
-                             x3 ? c->Xlo : c->Xhi, c->p_pad, c->ldk, &e);
+                             x3 ? c->Xlo : c->Xhi, c->xrows_pad, c->p_pad, c->n, c->ldk, &e);
     if (!c->plan) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
     if (filt) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
+  }
+
+  // ---- ring buffers of the sharded mode ----
+  if (c->sharded) {
+    for (int q = 0; q < c->world; ++q)
+      c->rrows_pad = std::max(c->rrows_pad, round_up(slab_rows(c, q), kRowPad));
+    const size_t rb = (size_t)c->rrows_pad * c->ldk;
+    for (int b = 0; b < 2; ++b) {
+      c->rbuf[b] = c->dalloc_bytes(rb * T);
+      CK(cudaMemsetAsync(c->rbuf[b], 0, rb * T, c->st));
+      if (tc) {
+        c->rhi[b] = c->dalloc<__nv_bfloat16>(rb);
+        CK(cudaMemsetAsync(c->rhi[b], 0, rb * 2, c->st));
+        if (x3) {
+          c->rlo[b] = c->dalloc<__nv_bfloat16>(rb);
+          CK(cudaMemsetAsync(c->rlo[b], 0, rb * 2, c->st));
+        }
+        std::string e;
+        if (!tc_plan_set_b(c->plan, 1 + b, c->rhi[b], x3 ? c->rlo[b] : c->rhi[b], c->rrows_pad, &e))
+          throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
+      }
+    }
+    c->yacc = c->dalloc<double>((size_t)c->pk_pad * c->ldk);
+    c->dacc = c->dalloc<double>((size_t)c->pk_pad * c->ldk);
+    if (c->comm == ACCORD_COMM_HOST) {
+      CK(cudaMallocHost(&c->h_send, rb * T));
+      CK(cudaMallocHost(&c->h_recv, rb * T));
+    }
   }
 
   // ---- per-row and entry-indexed state ----
@@ -472,7 +706,6 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->row_l1 = c->dalloc<double>(c->pk);
   c->row_logd = c->dalloc<double>(c->pk);
   c->row_nnz = c->dalloc<int32_t>(c->pk);
-  c->red_d = c->dalloc<double>(16);
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
   c->scan_tmp = c->dalloc_bytes(c->scan_tmp_sz);
@@ -562,8 +795,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
                                  c->om_val, c->c_w, S);
     CK(cudaEventRecord(c->ev[3], S));
-    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
-                                 c->Y[c->cur], c->Xt, c->c_g, S);
+    refine_all(c);
     CK(cudaEventRecord(c->ev[4], S));
     TR(c, "refit_sddmm");
     CK(cudaEventSynchronize(c->ev[4]));
@@ -585,6 +817,8 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     ep.pk = c->pk;
     ep.p = c->p;
     ep.r0 = c->r0;
+    ep.col_base = 0;
+    ep.col_end = c->p;
     ep.inv_n = 1.0 / (double)c->n;
     ep.lam_cand = c->dtype == ACCORD_F64 ? c->lam : c->lam * (1.0 - 4e-6);
     ep.row_A = c->row_A[c->cur];
@@ -593,17 +827,27 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     // fp32-accumulation term of the filter bound: (n/16 + 17) * 2^-22 * sum|y^ x^|
     ep.gamma = (float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
     CK(cudaEventRecord(c->ev[1], S));
-    if (c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER)
-    {
-      const int l = launch_gemm_tc(c->plan, c->gemm, c->cur, c->ldk, c->sm_count, ep,
-                                   omega_view(c), pool_view(c), S);
-      if (l < 0) throw Fail{ACCORD_E_CUDA, "GEMM grid / pool segment mismatch"};
-      c->launches += l;
-    }
+    const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
+    auto gemm = [&](const void* xt, int bsel, int64_t v0, int64_t v1) {
+      ep.col_base = v0;
+      ep.col_end = v1;
+      if (tc) {
+        const int l = launch_gemm_tc(c->plan, c->gemm, c->cur, bsel, c->sm_count, ep,
+                                     omega_view(c), pool_view(c), S);
+        if (l < 0) throw Fail{ACCORD_E_CUDA, "GEMM grid / pool segment mismatch"};
+        c->launches += l;
+      } else {
+        c->launches += launch_gemm_simt(c->dtype, c->Y[c->cur], xt, c->ldk, c->ldk, ep,
+                                        omega_view(c), pool_view(c), S);
+      }
+      c->gemm_launches++;
+    };
+    if (c->sharded)   // G_k[:, slab j] for every slab j, the pool filling across the ring
+      ring_pass(c, tc, [&](const void* xt, int bsel, int64_t v0, int64_t v1, bool, bool) {
+        gemm(xt, bsel, v0, v1);
+      });
     else
-      c->launches += launch_gemm_simt(c->dtype, c->Y[c->cur], c->Xt, c->ldk, c->ldk, ep,
-                                      omega_view(c), pool_view(c), S);
-    c->gemm_launches++;
+      gemm(c->Xt, 0, 0, c->p);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], S));
     TR(c, "gemm");
@@ -619,7 +863,15 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     const int64_t need = c->gemm_warps == 0 ? (int64_t)c->h_seg[0]
                                             : (int64_t)c->h_seg[1] * c->chunk;
     const bool ovf = c->gemm_warps == 0 ? need > c->chunk : (int64_t)c->h_seg[1] > c->nchunks;
-    if (!ovf) break;
+    bool ovf_any = ovf;
+    if (c->sharded) {   // the ring is collective: redo it together if any rank overflowed
+      c->h_red[0] = ovf ? 1.0 : 0.0;
+      CK(cudaMemcpyAsync(c->red_d, c->h_red, 8, cudaMemcpyHostToDevice, S));
+      allreduce(c, c->red_d, c->h_red, 1);
+      ovf_any = c->h_red[0] > 0;
+    }
+    if (!ovf_any) break;
+    if (!ovf) continue;
     const int64_t want = need + need / 4 + (1 << 20);
     if (want >= (int64_t)UINT32_MAX)
       throw Fail{ACCORD_E_NOMEM, "candidate pool exceeds 2^32 entries"};
@@ -640,8 +892,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
   TR(c, "finalize");
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) {
     // exact values of the filtered candidates: G_ik = <Y_i, X_k> / n (f64 accumulation)
-    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
-                                 c->Y[c->cur], c->Xt, c->c_g, S);
+    refine_all(c);
   }
   CK(cudaEventRecord(c->ev[4], S));
   TR(c, "refine");
@@ -669,9 +920,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
                                c->row_nnz, S);
     CK(cudaEventRecord(c->ev[5], S));
     TR(c, "prox");
-    c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, c->c_wn,
-                               c->c_w, c->Xt, c->Y[nb], c->Yhi[nb], c->Ylo[nb], c->row_A[nb],
-                               c->row_B[nb], c->row_D2, c->row_Y2, S);
+    spmm_all(c, c->c_ptr, c->c_col, c->c_wn, c->c_w, nb, c->row_D2, c->row_Y2);
     CK(cudaEventRecord(c->ev[6], S));
     TR(c, "spmm");
     c->launches += launch_reduce_rows(c->pk, c->row_D2, c->row_dd, c->row_logd, c->row_Y2,
@@ -735,6 +984,122 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   TR_flush(c);
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
   if (s) *s = st;
+}
+
+// Gather every rank's row block of Omega into one global host CSR (collective).
+// fetch = false: only the global nnz.
+void gather_host(accord_ctx* c, bool fetch, int64_t* total_out, std::vector<int64_t>* gp_out,
+                 std::vector<int32_t>* gc_out, std::vector<char>* gv_out) {
+    const size_t T = c->tsz;
+    // ---- gather all ranks' row blocks (collective) ----
+    // 1) per-rank (rows, nnz)
+    std::vector<double> h(2 * c->world, 0.0);
+    double* d = c->red_d;
+    std::vector<double> mine(2 * c->world, 0.0);
+    mine[2 * c->rank] = (double)c->pk;
+    mine[2 * c->rank + 1] = (double)c->nnz_local;
+    std::vector<double> tot(2 * c->world);
+    for (int q = 0; q < 2 * c->world; q += 8) {
+      const int cnt = std::min(8, 2 * c->world - q);
+      CK(cudaMemcpyAsync(d, mine.data() + q, cnt * 8, cudaMemcpyHostToDevice, c->st));
+      allreduce(c, d, c->h_red, cnt);
+      std::memcpy(tot.data() + q, c->h_red, cnt * 8);
+    }
+    int64_t total = 0, rows_total = 0;
+    for (int q = 0; q < c->world; ++q) {
+      rows_total += (int64_t)tot[2 * q];
+      total += (int64_t)tot[2 * q + 1];
+    }
+    *total_out = total;
+    if (!fetch) return;
+    if (rows_total != c->p) throw Fail{ACCORD_E_INVALID, "row blocks do not cover p rows"};
+    // local block to host
+    std::vector<int64_t> lp(c->pk + 1);
+    std::vector<int32_t> lc(c->nnz_local);
+    std::vector<char> lv(c->nnz_local * T);
+    CK(cudaMemcpyAsync(lp.data(), c->om_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(lc.data(), c->om_col, c->nnz_local * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(lv.data(), c->om_val, c->nnz_local * T, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<int64_t>& gp = *gp_out;
+    std::vector<int32_t>& gc = *gc_out;
+    std::vector<char>& gv = *gv_out;
+    gp.assign(c->p + 1, 0);
+    gc.resize(total);
+    gv.resize(total * T);
+    if (c->comm == ACCORD_COMM_NCCL) {
+      NcclApi* api = nccl_api();
+      int64_t* dptr = nullptr;
+      int32_t* dcol = nullptr;
+      char* dval = nullptr;
+      CK(cudaMalloc(&dptr, (rows_total + c->world) * 8));
+      CK(cudaMalloc(&dcol, std::max<int64_t>(total, 1) * 4));
+      CK(cudaMalloc(&dval, std::max<int64_t>(total, 1) * T));
+      int64_t ro = 0, eo = 0;
+      NK(api->GroupStart());
+      for (int q = 0; q < c->world; ++q) {
+        const int64_t rq = (int64_t)tot[2 * q], nq = (int64_t)tot[2 * q + 1];
+        const bool me = q == c->rank;
+        NK(api->Broadcast(me ? (const void*)c->om_ptr : nullptr, dptr + ro + q, (rq + 1) * 8,
+                          ncclChar, q, c->nccl, c->st));
+        if (nq > 0) {
+          NK(api->Broadcast(me ? (const void*)c->om_col : nullptr, dcol + eo, nq * 4, ncclChar, q,
+                            c->nccl, c->st));
+          NK(api->Broadcast(me ? (const void*)c->om_val : nullptr, dval + eo * T, nq * T,
+                            ncclChar, q, c->nccl, c->st));
+        }
+        ro += rq;
+        eo += nq;
+      }
+      NK(api->GroupEnd());
+      std::vector<int64_t> hp(rows_total + c->world);
+      CK(cudaMemcpyAsync(hp.data(), dptr, hp.size() * 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(gc.data(), dcol, total * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(gv.data(), dval, total * T, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      cudaFree(dptr);
+      cudaFree(dcol);
+      cudaFree(dval);
+      ro = 0;
+      eo = 0;
+      for (int q = 0; q < c->world; ++q) {
+        const int64_t rq = (int64_t)tot[2 * q];
+        for (int64_t i = 0; i <= rq; ++i) gp[ro + i] = eo + hp[ro + q + i];
+        ro += rq;
+        eo += (int64_t)tot[2 * q + 1];
+      }
+    } else {
+      if (!c->agv) throw Fail{ACCORD_E_INVALID, "GATHER with host comm needs allgatherv"};
+      // pack [rows][nnz][row_ptr][col][val]
+      std::vector<char> blob(16 + lp.size() * 8 + lc.size() * 4 + lv.size());
+      int64_t hdr[2] = {c->pk, c->nnz_local};
+      char* w = blob.data();
+      std::memcpy(w, hdr, 16); w += 16;
+      std::memcpy(w, lp.data(), lp.size() * 8); w += lp.size() * 8;
+      std::memcpy(w, lc.data(), lc.size() * 4); w += lc.size() * 4;
+      std::memcpy(w, lv.data(), lv.size());
+      std::vector<int64_t> counts(c->world, 0);
+      if (c->agv(c->cu, blob.data(), (int64_t)blob.size(), nullptr, counts.data()) != 0)
+        throw Fail{ACCORD_E_COMM, "allgatherv (sizes) failed"};
+      int64_t all = 0;
+      for (auto x : counts) all += x;
+      std::vector<char> buf(all);
+      if (c->agv(c->cu, blob.data(), (int64_t)blob.size(), buf.data(), counts.data()) != 0)
+        throw Fail{ACCORD_E_COMM, "allgatherv failed"};
+      const char* rd = buf.data();
+      int64_t ro = 0, eo = 0;
+      for (int q = 0; q < c->world; ++q) {
+        int64_t hq[2];
+        std::memcpy(hq, rd, 16);
+        const int64_t* qp = (const int64_t*)(rd + 16);
+        for (int64_t i = 0; i <= hq[0]; ++i) gp[ro + i] = eo + qp[i];
+        std::memcpy(gc.data() + eo, rd + 16 + (hq[0] + 1) * 8, hq[1] * 4);
+        std::memcpy(gv.data() + eo * T, rd + 16 + (hq[0] + 1) * 8 + hq[1] * 4, hq[1] * T);
+        rd += counts[q];
+        ro += hq[0];
+        eo += hq[1];
+      }
+    }
 }
 
 }  // namespace
@@ -813,117 +1178,143 @@ accord_status accord_export_csr(accord_ctx* c, int32_t scope, int64_t* row_ptr, 
       return;
     }
     if (scope != ACCORD_SCOPE_GATHER) throw Fail{ACCORD_E_INVALID, "bad scope"};
-    // ---- gather all ranks' row blocks (collective) ----
-    // 1) per-rank (rows, nnz)
-    std::vector<double> h(2 * c->world, 0.0);
-    double* d = c->red_d;
-    std::vector<double> mine(2 * c->world, 0.0);
-    mine[2 * c->rank] = (double)c->pk;
-    mine[2 * c->rank + 1] = (double)c->nnz_local;
-    std::vector<double> tot(2 * c->world);
-    for (int q = 0; q < 2 * c->world; q += 8) {
-      const int cnt = std::min(8, 2 * c->world - q);
-      CK(cudaMemcpyAsync(d, mine.data() + q, cnt * 8, cudaMemcpyHostToDevice, c->st));
-      allreduce(c, d, c->h_red, cnt);
-      std::memcpy(tot.data() + q, c->h_red, cnt * 8);
-    }
-    int64_t total = 0, rows_total = 0;
-    for (int q = 0; q < c->world; ++q) {
-      rows_total += (int64_t)tot[2 * q];
-      total += (int64_t)tot[2 * q + 1];
-    }
+    std::vector<int64_t> gp;
+    std::vector<int32_t> gc;
+    std::vector<char> gv;
+    int64_t total = 0;
+    gather_host(c, !!row_ptr, &total, &gp, &gc, &gv);
     *nnz_out = total;
     if (!row_ptr) return;
     if (capacity < total) throw Fail{ACCORD_E_CAPACITY, "capacity too small"};
-    if (rows_total != c->p) throw Fail{ACCORD_E_INVALID, "row blocks do not cover p rows"};
-    // local block to host
-    std::vector<int64_t> lp(c->pk + 1);
-    std::vector<int32_t> lc(c->nnz_local);
-    std::vector<char> lv(c->nnz_local * T);
-    CK(cudaMemcpyAsync(lp.data(), c->om_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(lc.data(), c->om_col, c->nnz_local * 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(lv.data(), c->om_val, c->nnz_local * T, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    std::vector<int64_t> gp(c->p + 1, 0);
-    std::vector<int32_t> gc(total);
-    std::vector<char> gv(total * T);
-    if (c->comm == ACCORD_COMM_NCCL) {
-      NcclApi* api = nccl_api();
-      int64_t* dptr = nullptr;
-      int32_t* dcol = nullptr;
-      char* dval = nullptr;
-      CK(cudaMalloc(&dptr, (rows_total + c->world) * 8));
-      CK(cudaMalloc(&dcol, std::max<int64_t>(total, 1) * 4));
-      CK(cudaMalloc(&dval, std::max<int64_t>(total, 1) * T));
-      int64_t ro = 0, eo = 0;
-      NK(api->GroupStart());
-      for (int q = 0; q < c->world; ++q) {
-        const int64_t rq = (int64_t)tot[2 * q], nq = (int64_t)tot[2 * q + 1];
-        const bool me = q == c->rank;
-        NK(api->Broadcast(me ? (const void*)c->om_ptr : nullptr, dptr + ro + q, (rq + 1) * 8,
-                          ncclChar, q, c->nccl, c->st));
-        if (nq > 0) {
-          NK(api->Broadcast(me ? (const void*)c->om_col : nullptr, dcol + eo, nq * 4, ncclChar, q,
-                            c->nccl, c->st));
-          NK(api->Broadcast(me ? (const void*)c->om_val : nullptr, dval + eo * T, nq * T,
-                            ncclChar, q, c->nccl, c->st));
-        }
-        ro += rq;
-        eo += nq;
-      }
-      NK(api->GroupEnd());
-      std::vector<int64_t> hp(rows_total + c->world);
-      CK(cudaMemcpyAsync(hp.data(), dptr, hp.size() * 8, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaMemcpyAsync(gc.data(), dcol, total * 4, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaMemcpyAsync(gv.data(), dval, total * T, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      cudaFree(dptr);
-      cudaFree(dcol);
-      cudaFree(dval);
-      ro = 0;
-      eo = 0;
-      for (int q = 0; q < c->world; ++q) {
-        const int64_t rq = (int64_t)tot[2 * q];
-        for (int64_t i = 0; i <= rq; ++i) gp[ro + i] = eo + hp[ro + q + i];
-        ro += rq;
-        eo += (int64_t)tot[2 * q + 1];
-      }
-    } else {
-      if (!c->agv) throw Fail{ACCORD_E_INVALID, "GATHER with host comm needs allgatherv"};
-      // pack [rows][nnz][row_ptr][col][val]
-      std::vector<char> blob(16 + lp.size() * 8 + lc.size() * 4 + lv.size());
-      int64_t hdr[2] = {c->pk, c->nnz_local};
-      char* w = blob.data();
-      std::memcpy(w, hdr, 16); w += 16;
-      std::memcpy(w, lp.data(), lp.size() * 8); w += lp.size() * 8;
-      std::memcpy(w, lc.data(), lc.size() * 4); w += lc.size() * 4;
-      std::memcpy(w, lv.data(), lv.size());
-      std::vector<int64_t> counts(c->world, 0);
-      if (c->agv(c->cu, blob.data(), (int64_t)blob.size(), nullptr, counts.data()) != 0)
-        throw Fail{ACCORD_E_COMM, "allgatherv (sizes) failed"};
-      int64_t all = 0;
-      for (auto x : counts) all += x;
-      std::vector<char> buf(all);
-      if (c->agv(c->cu, blob.data(), (int64_t)blob.size(), buf.data(), counts.data()) != 0)
-        throw Fail{ACCORD_E_COMM, "allgatherv failed"};
-      const char* rd = buf.data();
-      int64_t ro = 0, eo = 0;
-      for (int q = 0; q < c->world; ++q) {
-        int64_t hq[2];
-        std::memcpy(hq, rd, 16);
-        const int64_t* qp = (const int64_t*)(rd + 16);
-        for (int64_t i = 0; i <= hq[0]; ++i) gp[ro + i] = eo + qp[i];
-        std::memcpy(gc.data() + eo, rd + 16 + (hq[0] + 1) * 8, hq[1] * 4);
-        std::memcpy(gv.data() + eo * T, rd + 16 + (hq[0] + 1) * 8 + hq[1] * 4, hq[1] * T);
-        rd += counts[q];
-        ro += hq[0];
-        eo += hq[1];
-      }
-    }
     const cudaMemcpyKind hk = on_device ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost;
     CK(cudaMemcpy(row_ptr, gp.data(), gp.size() * 8, hk));
     CK(cudaMemcpy(col, gc.data(), gc.size() * 4, hk));
     CK(cudaMemcpy(val, gv.data(), gv.size(), hk));
+  });
+}
+
+// NEXT(4): Theta-hat = Omega_D Omega and the partial correlations rho-hat
+// computed on the device (postproc.cu).
+accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t scope,
+                                        int64_t* row_ptr, int32_t* col, void* val,
+                                        int64_t capacity, int64_t* nnz_out, int32_t on_device) {
+  if (!c || !nnz_out) return ACCORD_E_INVALID;
+  if (kind == ACCORD_EXPORT_OMEGA)
+    return accord_export_csr(c, scope, row_ptr, col, val, capacity, nnz_out, on_device);
+  return guard(c, [&] {
+    if (kind != ACCORD_EXPORT_THETA && kind != ACCORD_EXPORT_PCORR)
+      throw Fail{ACCORD_E_INVALID, "bad export kind"};
+    if (scope != ACCORD_SCOPE_LOCAL && scope != ACCORD_SCOPE_GATHER)
+      throw Fail{ACCORD_E_INVALID, "bad scope"};
+    const size_t T = c->tsz;
+    cudaStream_t S = c->st;
+    // temporaries of this call only
+    std::vector<void*> tmp;
+    struct Free {
+      std::vector<void*>& v;
+      ~Free() { for (void* q : v) cudaFree(q); }
+    } fr{tmp};
+    auto talloc = [&](size_t b) {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, std::max<size_t>(b, 1)));
+      tmp.push_back(q);
+      return q;
+    };
+    // The input CSR: this rank's block (THETA of the local rows, or P = 1) or the
+    // gathered global Omega (collective) uploaded to the device.
+    const bool local_in = c->world == 1 || (kind == ACCORD_EXPORT_THETA && scope == ACCORD_SCOPE_LOCAL);
+    const int64_t* iptr = c->om_ptr;
+    const int32_t* icol = c->om_col;
+    const void* ival = c->om_val;
+    int64_t irows = c->pk, ioff = c->r0;
+    if (!local_in) {
+      std::vector<int64_t> gp;
+      std::vector<int32_t> gc;
+      std::vector<char> gv;
+      int64_t total = 0;
+      gather_host(c, true, &total, &gp, &gc, &gv);
+      int64_t* dp = (int64_t*)talloc(gp.size() * 8);
+      int32_t* dc = (int32_t*)talloc(gc.size() * 4);
+      void* dv = talloc(gv.size());
+      CK(cudaMemcpyAsync(dp, gp.data(), gp.size() * 8, cudaMemcpyHostToDevice, S));
+      CK(cudaMemcpyAsync(dc, gc.data(), gc.size() * 4, cudaMemcpyHostToDevice, S));
+      CK(cudaMemcpyAsync(dv, gv.data(), gv.size(), cudaMemcpyHostToDevice, S));
+      CK(cudaStreamSynchronize(S));   // the host vectors go out of scope
+      iptr = dp;
+      icol = dc;
+      ival = dv;
+      irows = c->p;
+      ioff = 0;
+    }
+    // output rows [a, b) of the input CSR
+    const bool all = scope == ACCORD_SCOPE_GATHER || c->world == 1;
+    const int64_t a = all || local_in ? 0 : c->r0, b = all ? irows : (local_in ? irows : c->r1);
+    const int64_t rows = b - a;
+    double* d = (double*)talloc(irows * 8);
+    int32_t* bad = (int32_t*)talloc(4);
+    CK(cudaMemsetAsync(bad, 0, 4, S));
+    c->launches += launch_diag(c->dtype, irows, ioff, iptr, icol, ival, d, bad, S);
+    int64_t* optr = nullptr;
+    int32_t* ocol = nullptr;
+    void* oval = nullptr;
+    int64_t h_ab[2] = {0, 0};
+    CK(cudaMemcpyAsync(h_ab, iptr + a, 8, cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(h_ab + 1, iptr + b, 8, cudaMemcpyDeviceToHost, S));
+    int32_t hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    if (hbad) throw Fail{ACCORD_E_DOMAIN, "Omega has a missing or nonpositive diagonal entry"};
+    int64_t nnz = 0;
+    if (kind == ACCORD_EXPORT_THETA) {
+      nnz = h_ab[1] - h_ab[0];
+      oval = talloc(nnz * T);
+      c->launches += launch_theta(c->dtype, a, b, iptr, icol, ival, d, oval, S);
+      // structure = Omega's rows [a, b), rebased to 0
+      optr = (int64_t*)talloc((rows + 1) * 8);
+      std::vector<int64_t> hp(rows + 1);
+      CK(cudaMemcpyAsync(hp.data(), iptr + a, (rows + 1) * 8, cudaMemcpyDeviceToHost, S));
+      CK(cudaStreamSynchronize(S));
+      for (auto& x : hp) x -= h_ab[0];
+      CK(cudaMemcpyAsync(optr, hp.data(), (rows + 1) * 8, cudaMemcpyHostToDevice, S));
+      ocol = const_cast<int32_t*>(icol) + h_ab[0];
+      CK(cudaStreamSynchronize(S));
+    } else {
+      int32_t* own = (int32_t*)talloc(rows * 4);
+      int32_t* cnt = (int32_t*)talloc(rows * 4);
+      int32_t* ext = (int32_t*)talloc(rows * 4);
+      int32_t* long_rows = (int32_t*)talloc((rows + 1) * 4);
+      optr = (int64_t*)talloc((rows + 1) * 8);
+      CK(cudaMemsetAsync(own, 0, rows * 4, S));
+      CK(cudaMemsetAsync(cnt, 0, rows * 4, S));
+      CK(cudaMemsetAsync(ext, 0, rows * 4, S));
+      CK(cudaMemsetAsync(long_rows, 0, 4, S));
+      c->launches += launch_pcorr_count(c->dtype, irows, a, b, iptr, icol, ival, own, cnt, S);
+      void* stmp = talloc(scan_tmp_bytes(rows + 1));
+      c->launches += launch_scan_i32(cnt, optr, rows, stmp, scan_tmp_bytes(rows + 1), S);
+      CK(cudaMemcpyAsync(&nnz, optr + rows, 8, cudaMemcpyDeviceToHost, S));
+      CK(cudaStreamSynchronize(S));
+      uint64_t* keys = (uint64_t*)talloc(nnz * 8);
+      uint64_t* ktmp = (uint64_t*)talloc(nnz * 8);
+      c->launches += launch_pcorr_fill(c->dtype, irows, a, b, iptr, icol, ival, own, optr, ext,
+                                       keys, S);
+      c->launches += launch_rowsort(rows, optr, keys, ktmp, long_rows, S);
+      ocol = (int32_t*)talloc(nnz * 4);
+      oval = talloc(nnz * T);
+      c->launches += launch_pcorr_value(c->dtype, a, b, iptr, icol, ival, d, optr, keys, ocol,
+                                        oval, S);
+    }
+    CK(cudaGetLastError());
+    *nnz_out = nnz;
+    if (!row_ptr) {
+      CK(cudaStreamSynchronize(S));
+      return;
+    }
+    if (capacity < nnz) throw Fail{ACCORD_E_CAPACITY, "capacity too small"};
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(cudaMemcpyAsync(row_ptr, optr, (rows + 1) * 8, k, S));
+    CK(cudaMemcpyAsync(col, ocol, nnz * 4, k, S));
+    CK(cudaMemcpyAsync(val, oval, nnz * T, k, S));
+    CK(cudaStreamSynchronize(S));
   });
 }
 
@@ -1142,6 +1533,17 @@ void accord_destroy(accord_ctx* c) {
   for (auto& e : c->tr_pool) cudaEventDestroy(e);
   if (c->h_red) cudaFreeHost(c->h_red);
   if (c->h_seg) cudaFreeHost(c->h_seg);
+  if (c->h_send) cudaFreeHost(c->h_send);
+  if (c->h_recv) cudaFreeHost(c->h_recv);
+  if (c->cs) {
+    cudaStreamSynchronize(c->cs);
+    cudaStreamDestroy(c->cs);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (c->ev_comp[b]) cudaEventDestroy(c->ev_comp[b]);
+    if (c->ev_recv[b]) cudaEventDestroy(c->ev_recv[b]);
+  }
+  if (c->nccl_ring && nccl_api()) nccl_api()->CommDestroy(c->nccl_ring);
   if (c->nccl && nccl_api()) nccl_api()->CommDestroy(c->nccl);
   delete c;
 }

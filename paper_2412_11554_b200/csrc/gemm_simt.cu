@@ -35,7 +35,8 @@ gemm_simt_kernel(const T* __restrict__ Y, const T* __restrict__ Xt, int64_t ldk,
   __shared__ T As[BK][BM + 4];
   __shared__ T Bs[BK][BN + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;   // n0: slab row
+  const int64_t ncols = ep.col_end - ep.col_base;
   T acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -51,7 +52,7 @@ gemm_simt_kernel(const T* __restrict__ Y, const T* __restrict__ Xt, int64_t ldk,
     for (int q = 0; q < 4; ++q) {
       const int64_t kk = k0 + lk + q;
       As[lk + q][lr] = (ra < ep.pk && kk < ldk) ? Y[ra * ldk + kk] : T(0);
-      Bs[lk + q][lr] = (rb < ep.p && kk < ldk) ? Xt[rb * ldk + kk] : T(0);
+      Bs[lk + q][lr] = (rb < ncols && kk < ldk) ? Xt[rb * ldk + kk] : T(0);
     }
     __syncthreads();
 #pragma unroll
@@ -80,8 +81,8 @@ gemm_simt_kernel(const T* __restrict__ Y, const T* __restrict__ Xt, int64_t ldk,
     int cnt = 0;
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
-      const int64_t k = n0 + tx * 4 + y;
-      if (k >= ep.p) continue;
+      const int64_t k = ep.col_base + n0 + tx * 4 + y;
+      if (k >= ep.col_end) continue;
       const T g = acc[x][y] / nT;
       const T w = lookup_omega<T>(om, r, (int32_t)k);
       const bool emit = (k == gi) || (w != T(0)) || (fabs((double)g) > ep.lam_cand);
@@ -104,7 +105,8 @@ gemm_simt_kernel(const T* __restrict__ Y, const T* __restrict__ Xt, int64_t ldk,
 int launch_gemm_simt(int dtype, const void* Y, const void* Xt, int64_t ldk, int64_t kdim,
                      const EpiParams& ep, const OmegaView& om, const PoolView& pool,
                      cudaStream_t st) {
-  dim3 grd((unsigned)((ep.p + BN - 1) / BN), (unsigned)((ep.pk + BM - 1) / BM));
+  dim3 grd((unsigned)((ep.col_end - ep.col_base + BN - 1) / BN),
+           (unsigned)((ep.pk + BM - 1) / BM));
   if (dtype == ACCORD_F64)
     gemm_simt_kernel<double><<<grd, 256, 0, st>>>((const double*)Y, (const double*)Xt, ldk,
                                                    kdim, ep, om, pool);

@@ -41,6 +41,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -63,7 +64,7 @@ constexpr int kEpiWarp0 = 4;
 template <int kMode> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
   static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 64 / 32 KB
-  static constexpr int kStages = kMode == 0 ? 3 : 6;
+  static constexpr int kStages = kMode == 0 ? 3 : 7;   // 7 x 32 KB + barriers <= 227 KB
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
 };
 
@@ -134,7 +135,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
                const __grid_constant__ CUtensorMap mB_hi,
-               const __grid_constant__ CUtensorMap mB_lo, int num_kb, int num_m, int num_n,
+               const __grid_constant__ CUtensorMap mB_lo, int num_kb, int kk_last, int num_m,
+               int num_n,
                int group_n, int unit_n, int dbg, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
   constexpr int kStages = Cfg<kMode>::kStages;
@@ -224,8 +226,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           const uint64_t b_hi = tc::sdesc_k_sw128(s + kTileA);
           const uint64_t a_lo = tc::sdesc_k_sw128(s + kTileA + kTileB);
           const uint64_t b_lo = tc::sdesc_k_sw128(s + 2 * kTileA + kTileB);
+          // the last k-block issues only the K16 steps that reach a sample
+          // (the rest of its box is TMA zero fill past n)
+          const int nkk = kb == num_kb - 1 ? kk_last : BK / 16;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
+            if (kk >= nkk) break;
             const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 = 32 B along K
             const uint32_t accum = (kb | kk) != 0;
             if (dbg != 2) tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
@@ -260,7 +266,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     int32_t nxt = INT_MAX;
     float r1 = 0.f, Bn = 0.f;
     for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
-      const int n0 = it.n() * BN;
+      const int n0 = (int)ep.col_base + it.n() * BN;   // global column of the tile
       if (it.unit_start()) {
         // new row block: row constants and the start of the CSR walk (the
         // walk then continues across the unit's consecutive column tiles)
@@ -288,7 +294,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
       }
       float tfast = thr;
       if (kMode == 1 && row_ok) {
-        const float2 mx = blk_sdmax[it.n()];     // tile max of the column constants
+        const float2 mx = blk_sdmax[n0 / BN];    // tile max of the column constants
         tfast = thr - fmaf(r1, mx.x, Bn * mx.y);
       }
       tc::mbar_wait(tc::smem_u32(&tfull[acc]), acc_phase);
@@ -315,9 +321,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           const int64_t sp0 = sp;
           uint32_t mask = 0, sup = 0;
           if (row_ok) {
+            // common case first: no |acc| in these 32 columns passes the fast
+            // test (one FMNMX per value instead of a compare + select + add)
+            float m0 = 0.f, m1 = 0.f;
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
+            for (int c = 0; c < 32; c += 2) {
+              m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
+              m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
+            }
+            if (fmaxf(m0, m1) > tfast) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
+            }
             if (kMode == 1 && mask) {
               // exact per-column bound for the (rare) survivors of the fast test
 #pragma unroll
@@ -336,7 +352,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               nxt = sp < se ? om.col[sp] : INT_MAX;
             }
             mask |= sup;
-            const int64_t left = ep.p - c0;                           // ragged p
+            const int64_t left = ep.col_end - c0;                     // ragged p / slab
             if (left < 32) mask &= left <= 0 ? 0u : ((1u << left) - 1u);
           }
           const int cnt = __popc(mask);
@@ -448,14 +464,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ldk, int box_rows,
-              std::string* err) {
+// rows x kdim bf16 (row stride ldk elements); the box runs past kdim into TMA
+// zero fill, so the padding columns [kdim, ldk) are never read
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t kdim, int64_t ldk,
+              int box_rows, std::string* err) {
   auto fn = encode_fn();
   if (!fn) {
     *err = "cuTensorMapEncodeTiled unavailable";
     return false;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)ldk, (cuuint64_t)rows};
+  cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ldk * 2)};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
@@ -472,8 +490,10 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ldk, int b
 }  // namespace
 
 struct TcGemmPlan {
-  CUtensorMap a_hi[2], a_lo[2], b_hi, b_lo;
-  int64_t pk_pad = 0, p_pad = 0, ldk = 0;
+  // B operand maps: [0] = X^T (all columns, or this rank's slab when X is
+  // sharded), [1], [2] = the two ring buffers of the sharded mode (NEXT(3))
+  CUtensorMap a_hi[2], a_lo[2], b_hi[3], b_lo[3];
+  int64_t pk_pad = 0, p_pad = 0, ldk = 0, kdim = 0;   // p_pad: padded column count (all p)
   float2* blk_sdmax = nullptr;   // [p_pad / 256] (BF16_FILTER)
 };
 
@@ -481,18 +501,21 @@ bool tc_supported(int cc_major, int cc_minor) { return cc_major == 10 && cc_mino
 
 TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            const __nv_bfloat16* Yhi1, const __nv_bfloat16* Ylo1, int64_t pk_pad,
-                           const __nv_bfloat16* Xhi, const __nv_bfloat16* Xlo, int64_t p_pad,
-                           int64_t ldk, std::string* err) {
+                           const __nv_bfloat16* Xhi, const __nv_bfloat16* Xlo, int64_t xrows_pad,
+                           int64_t p_pad, int64_t kdim, int64_t ldk, std::string* err) {
   auto* p = new TcGemmPlan();
   p->pk_pad = pk_pad;
   p->p_pad = p_pad;
   p->ldk = ldk;
-  bool ok = make_map(&p->a_hi[0], Yhi0, pk_pad, ldk, BM, err) &&
-            make_map(&p->a_lo[0], Ylo0, pk_pad, ldk, BM, err) &&
-            make_map(&p->a_hi[1], Yhi1, pk_pad, ldk, BM, err) &&
-            make_map(&p->a_lo[1], Ylo1, pk_pad, ldk, BM, err) &&
-            make_map(&p->b_hi, Xhi, p_pad, ldk, BNH, err) &&
-            make_map(&p->b_lo, Xlo, p_pad, ldk, BNH, err);
+  p->kdim = kdim;
+  bool ok = make_map(&p->a_hi[0], Yhi0, pk_pad, kdim, ldk, BM, err) &&
+            make_map(&p->a_lo[0], Ylo0, pk_pad, kdim, ldk, BM, err) &&
+            make_map(&p->a_hi[1], Yhi1, pk_pad, kdim, ldk, BM, err) &&
+            make_map(&p->a_lo[1], Ylo1, pk_pad, kdim, ldk, BM, err) &&
+            make_map(&p->b_hi[0], Xhi, xrows_pad, kdim, ldk, BNH, err) &&
+            make_map(&p->b_lo[0], Xlo, xrows_pad, kdim, ldk, BNH, err);
+  p->b_hi[1] = p->b_hi[2] = p->b_hi[0];
+  p->b_lo[1] = p->b_lo[2] = p->b_lo[0];
   if (ok && cudaMalloc(&p->blk_sdmax, (p_pad / BN) * sizeof(float2)) != cudaSuccess) {
     *err = "alloc";
     ok = false;
@@ -513,6 +536,12 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
   return p;
 }
 
+bool tc_plan_set_b(TcGemmPlan* p, int idx, const __nv_bfloat16* hi, const __nv_bfloat16* lo,
+                   int64_t rows_pad, std::string* err) {
+  return make_map(&p->b_hi[idx], hi, rows_pad, p->kdim, p->ldk, BNH, err) &&
+         make_map(&p->b_lo[idx], lo, rows_pad, p->kdim, p->ldk, BNH, err);
+}
+
 int tc_plan_set_col_norms(TcGemmPlan* p, const float2* col_sd, int64_t pcols, cudaStream_t st) {
   const int nblk = (int)(p->p_pad / BN);
   blk_max_kernel<<<nblk, 256, 0, st>>>(col_sd, pcols, nblk, p->blk_sdmax);
@@ -531,18 +560,23 @@ int tc_grid_size(const TcGemmPlan* plan, int sm_count) {
   return (int)(2 * clusters);
 }
 
-int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int64_t kdim, int sm_count,
+int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
                    const EpiParams& ep, const OmegaView& om, const PoolView& pool,
                    cudaStream_t st) {
   const int num_m = (int)(plan->pk_pad / (2 * BM));
-  const int num_n = (int)(plan->p_pad / BN);
+  const int num_n = (int)((ep.col_end - ep.col_base + BN - 1) / BN);
+  const int64_t kdim = plan->kdim;
   const int num_kb = (int)((kdim + BK - 1) / BK);
+  const int kk_last = (int)((kdim - (int64_t)(num_kb - 1) * BK + 15) / 16);   // 1..4
   const int grid = tc_grid_size(plan, sm_count);
   // A group of <= 64 N-blocks (<= 32 MB of X^T_hi at n = 1000) stays in L2;
   // units small enough that the per-cluster imbalance is <= ~6% of its work
-  const int group_n = num_n < 64 ? num_n : 64;
+  int gn = 64;
+  if (const char* e = std::getenv("ACCORD_GEMM_GN")) gn = std::max(1, std::atoi(e));   // tuning
+  const int group_n = num_n < gn ? num_n : gn;
   const long long tiles = (long long)num_m * num_n;
   long long u = tiles / ((long long)(grid / 2) * 16);
+  if (const char* e = std::getenv("ACCORD_GEMM_UNIT")) u = std::max(1, std::atoi(e));  // tuning
   const int unit_n = (int)(u < 1 ? 1 : (u > group_n ? group_n : u));
   // ACCORD_DEBUG_GEMM (diagnostics only; results are wrong when set):
   // 1 = skip the epilogue, 2 = skip the MMAs
@@ -550,11 +584,15 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int64_t kdim, int sm_co
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0><<<grid, kThreads, Cfg<0>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi, plan->b_lo, num_kb, num_m, num_n, group_n, unit_n, dbg,
+        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi[bsel], plan->b_lo[bsel], num_kb, kk_last,
+        num_m, num_n,
+        group_n, unit_n, dbg,
         ep, plan->blk_sdmax, om, pool);
   else
     gemm_tc_kernel<1><<<grid, kThreads, Cfg<1>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi, plan->b_hi, num_kb, num_m, num_n, group_n, unit_n, dbg,
+        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi[bsel], plan->b_hi[bsel], num_kb, kk_last,
+        num_m, num_n,
+        group_n, unit_n, dbg,
         ep, plan->blk_sdmax, om, pool);
   return 1;
 }

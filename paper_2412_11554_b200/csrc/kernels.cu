@@ -100,8 +100,10 @@ __global__ void split_bf16_kernel(const float4* __restrict__ src, int64_t n4,
     float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
     hi[2 * i] = h0;
     hi[2 * i + 1] = h1;
-    lo[2 * i] = __floats2bfloat162_rn(v.x - f0.x, v.y - f0.y);
-    lo[2 * i + 1] = __floats2bfloat162_rn(v.z - f1.x, v.w - f1.y);
+    if (lo) {   // NULL: the single-pass filter needs no low part
+      lo[2 * i] = __floats2bfloat162_rn(v.x - f0.x, v.y - f0.y);
+      lo[2 * i + 1] = __floats2bfloat162_rn(v.z - f1.x, v.w - f1.y);
+    }
   }
 }
 
@@ -391,6 +393,16 @@ __global__ void prox_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ 
 // a6: SpMM Y+_i = sum_j w+_ij Xt_j and D_i = sum_j Delta_ij Xt_j, block per row,
 // 16-byte coalesced gathers of Xt rows; fused ||D_i||^2 and ||Y+_i||^2.
 // ---------------------------------------------------------------------------
+// first index e in [lo, hi) of a sorted column run with col[e] >= v
+__device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ col, int64_t lo,
+                                                   int64_t hi, int64_t v) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)col[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 constexpr int kSpmmMaxThreads = 1024;
 
 template <typename T, bool kSplit>
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
     const int32_t* __restrict__ col, const T* __restrict__ wn, const T* __restrict__ wo,
     const T* __restrict__ Xt, T* __restrict__ Yout, __nv_bfloat16* __restrict__ Yhi,
     __nv_bfloat16* __restrict__ Ylo, float* __restrict__ row_A, float* __restrict__ row_B,
-    double* __restrict__ row_D2, double* __restrict__ row_Y2) {
+    double* __restrict__ row_D2, double* __restrict__ row_Y2, SpmmRing rg) {
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   __shared__ int32_t s_col[kSpmmMaxThreads];
@@ -408,7 +420,17 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
   __shared__ int s_wc[32];
   __shared__ double s_red[32];
   const int64_t r = blockIdx.x;
-  const int64_t beg = ptr[r], end = ptr[r + 1];
+  int64_t beg = ptr[r], end = ptr[r + 1];
+  // sharded X (NEXT(3)): only this row's entries in the resident slab's
+  // columns [v0, v1) (a contiguous run of the sorted row); partial sums carry
+  // across the ring steps in float64 accumulators
+  const bool ring = rg.yacc != nullptr;
+  const int32_t xoff = ring ? (int32_t)rg.v0 : 0;
+  if (ring) {
+    beg = lower_bound_col(col, beg, end, rg.v0);
+    end = lower_bound_col(col, beg, end, rg.v1);
+    if (beg == end && !rg.first && !rg.last) return;   // nothing to add
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0;
   for (int64_t c0 = 0; c0 < ldk; c0 += (int64_t)blockDim.x * V) {
@@ -417,6 +439,13 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
     double ay[V], ad[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+    if (ring && !rg.first && active) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        ay[v] = rg.yacc[r * ldk + c + v];
+        ad[v] = rg.dacc[r * ldk + c + v];
+      }
+    }
     for (int64_t e0 = beg; e0 < end; e0 += blockDim.x) {
       // stage the next blockDim entries in order, dropping w+ = Delta = 0
       // (deterministic ballot/prefix compaction)
@@ -427,7 +456,7 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
       if (e < end) {
         w = (double)wn[e];
         d = wo ? w - (double)wo[e] : 0.0;
-        cc = col[e];
+        cc = col[e] - xoff;
         keep = (w != 0.0) || (d != 0.0);
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -475,6 +504,16 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
       }
       __syncthreads();
     }
+    if (ring && !rg.last) {
+      if (active) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          rg.yacc[r * ldk + c + v] = ay[v];
+          rg.dacc[r * ldk + c + v] = ad[v];
+        }
+      }
+      continue;
+    }
     if (active) {
       T yt[V];
 #pragma unroll
@@ -506,6 +545,7 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
       }
     }
   }
+  if (ring && !rg.last) return;   // block-uniform
   d2 = block_sum(d2, s_red);
   y2 = block_sum(y2, s_red);
   if constexpr (kSplit) {
@@ -535,13 +575,18 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
                                                      const int32_t* __restrict__ c_col,
                                                      const T* __restrict__ Y,
                                                      const T* __restrict__ Xt,
-                                                     T* __restrict__ c_g) {
+                                                     T* __restrict__ c_g, int64_t v0,
+                                                     int64_t v1) {
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   extern __shared__ __align__(16) uint8_t ys_raw[];
   T* ys = reinterpret_cast<T*>(ys_raw);
   const int64_t r = blockIdx.x;
-  const int64_t beg = c_ptr[r], end = c_ptr[r + 1];
+  int64_t beg = c_ptr[r], end = c_ptr[r + 1];
+  // columns [v0, v1) only (Xt row 0 = column v0): one ring step of the
+  // sharded mode (NEXT(3)); v0 = 0, v1 = p otherwise
+  beg = lower_bound_col(c_col, beg, end, v0);
+  end = lower_bound_col(c_col, beg, end, v1);
   if (beg == end) return;
   for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V)
     *reinterpret_cast<VT*>(ys + m) = *reinterpret_cast<const VT*>(Y + r * ldk + m);
@@ -550,7 +595,7 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   const double inv_n = 1.0 / (double)n;
   constexpr int kStep = 32 * V;           // elements per lane-pass over the row
   for (int64_t e = beg + wid; e < end; e += nw) {
-    const T* xr = Xt + (int64_t)c_col[e] * ldk;
+    const T* xr = Xt + (int64_t)(c_col[e] - v0) * ldk;
     double s = 0.0;
     int64_t m = lane * V;
     for (; m + 7 * kStep < ldk; m += 8 * kStep) {   // 8 loads in flight per lane
@@ -890,6 +935,26 @@ int launch_scan_i32(const int32_t* in, int64_t* out, int64_t N, void* tmp, size_
   return 3;
 }
 
+int launch_rowsort(int64_t rows, const int64_t* ptr, uint64_t* keys, uint64_t* tmp,
+                   int32_t* long_rows, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  const int warps = 8;
+  const size_t smem = (size_t)warps * kWarpSortMax * sizeof(uint64_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rowsort_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(rowsort_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kBlockSortMax * sizeof(uint64_t)));
+    attr = true;
+  }
+  rowsort_warp_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, smem, st>>>(
+      rows, ptr, keys, long_rows);
+  rowsort_block_kernel<<<148, 1024, kBlockSortMax * sizeof(uint64_t), st>>>(ptr, keys, tmp,
+                                                                           long_rows);
+  return 2;
+}
+
 int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* c_ptr,
                     int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col, void* c_g,
                     void* c_w, int32_t* long_rows, cudaStream_t st) {
@@ -902,23 +967,7 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
                                                  keys);
   }
   ++launches;
-  {
-    const int warps = 8;
-    const size_t smem = (size_t)warps * kWarpSortMax * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(rowsort_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      cudaFuncSetAttribute(rowsort_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(kBlockSortMax * sizeof(uint64_t)));
-      attr = true;
-    }
-    rowsort_warp_kernel<<<(unsigned)((pk + warps - 1) / warps), warps * 32, smem, st>>>(
-        pk, c_ptr, keys, long_rows);
-    rowsort_block_kernel<<<148, 1024, kBlockSortMax * sizeof(uint64_t), st>>>(
-        c_ptr, keys, keys_tmp, long_rows);
-    launches += 2;
-  }
+  launches += launch_rowsort(pk, c_ptr, keys, keys_tmp, long_rows, st);
   if (dtype == ACCORD_F64)
     gather_kernel<double><<<148 * 8, 256, 0, st>>>(pk, c_ptr, keys, (const double*)pool.g,
                                                    (const double*)pool.w, c_col, (double*)c_g,
@@ -950,29 +999,30 @@ int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const i
 int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* ptr,
                 const int32_t* col, const void* wn, const void* wo, const void* Xt, void* Yout,
                 __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
-                double* row_D2, double* row_Y2, cudaStream_t st) {
+                double* row_D2, double* row_Y2, cudaStream_t st, const SpmmRing* ring) {
+  const SpmmRing rg = ring ? *ring : SpmmRing{0, 0, nullptr, nullptr, 1, 1};
   const int V = dtype == ACCORD_F64 ? 2 : 4;
   int threads = (int)std::min<int64_t>(kSpmmMaxThreads, round_up(ldk / V, 32));
   if (pk == 0) return 0;
   if (dtype == ACCORD_F64) {
     spmm_kernel<double, false><<<(unsigned)pk, threads, 0, st>>>(
         pk, n, ldk, ptr, col, (const double*)wn, (const double*)wo, (const double*)Xt,
-        (double*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2);
+        (double*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2, rg);
   } else if (Yhi) {
     spmm_kernel<float, true><<<(unsigned)pk, threads, 0, st>>>(
         pk, n, ldk, ptr, col, (const float*)wn, (const float*)wo, (const float*)Xt,
-        (float*)Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2);
+        (float*)Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2, rg);
   } else {
     spmm_kernel<float, false><<<(unsigned)pk, threads, 0, st>>>(
         pk, n, ldk, ptr, col, (const float*)wn, (const float*)wo, (const float*)Xt,
-        (float*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2);
+        (float*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2, rg);
   }
   return 1;
 }
 
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
-                  cudaStream_t st) {
+                  cudaStream_t st, int64_t v0, int64_t v1) {
   if (pk == 0) return 0;
   const size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
   static bool attr = false;
@@ -986,11 +1036,11 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
   if (dtype == ACCORD_F64)
     refine_kernel<double><<<(unsigned)pk, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                            (const double*)Y, (const double*)Xt,
-                                                           (double*)c_g);
+                                                           (double*)c_g, v0, v1);
   else
     refine_kernel<float><<<(unsigned)pk, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                           (const float*)Y, (const float*)Xt,
-                                                          (float*)c_g);
+                                                          (float*)c_g, v0, v1);
   return 1;
 }
 
@@ -1075,7 +1125,11 @@ int launch_identity(int dtype, int64_t pk, int64_t r0, int64_t* om_ptr, int32_t*
 }
 
 int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk, int max_iter,
-                    double tol, double* L_host, cudaStream_t st, std::string* err) {
+                    double tol, double* L_host, cudaStream_t st, std::string* err,
+                    int64_t p_global, const DevAllreduce* ar) {
+  // Sharded X (NEXT(3)): this rank holds p of the p_global variables; X v is
+  // summed over ranks (allreduce of the n-vector u) and so are the two dots.
+  if (p_global <= 0) p_global = p;
   int launches = 0;
   const int64_t nsplit = std::min<int64_t>(256, std::max<int64_t>(1, p / 256));
   const int64_t rows_per = (p + nsplit - 1) / nsplit;
@@ -1090,7 +1144,7 @@ int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk
     *err = std::string("power iteration alloc: ") + cudaGetErrorString(e);
     return -1;
   }
-  fill_d<<<grid_for(p, 256), 256, 0, st>>>(v, p, 1.0 / std::sqrt((double)p));
+  fill_d<<<grid_for(p, 256), 256, 0, st>>>(v, p, 1.0 / std::sqrt((double)p_global));
   ++launches;
   double rq_prev = -1.0, rq = 0.0, h[2];
   const int check_every = 10;
@@ -1101,12 +1155,22 @@ int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk
     else
       pi_xv_kernel<float><<<g1, 256, 0, st>>>((const float*)Xt, p, ldk, rows_per, v, part);
     pi_sum_parts<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(part, nsplit, ldk, u);
+    if (ar && !(*ar)(u, (int)ldk)) {
+      e = cudaErrorUnknown;
+      *err = "power iteration: allreduce failed";
+      break;
+    }
     const unsigned g3 = (unsigned)((p + 7) / 8);
     if (dtype == ACCORD_F64)
       pi_xtu_kernel<double><<<g3, 256, 0, st>>>((const double*)Xt, p, ldk, n, u, w);
     else
       pi_xtu_kernel<float><<<g3, 256, 0, st>>>((const float*)Xt, p, ldk, n, u, w);
     pi_dots<<<1, 1024, 0, st>>>(v, w, p, dots);
+    if (ar && !(*ar)(dots, 2)) {
+      e = cudaErrorUnknown;
+      *err = "power iteration: allreduce failed";
+      break;
+    }
     pi_normalize<<<grid_for(p, 256), 256, 0, st>>>(w, p, dots, v);
     launches += 5;
     if ((it + 1) % check_every == 0 || it + 1 == max_iter) {
@@ -1129,7 +1193,7 @@ int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk
   cudaFreeAsync(part, st);
   cudaFreeAsync(dots, st);
   if (e != cudaSuccess) {
-    *err = std::string("power iteration: ") + cudaGetErrorString(e);
+    if (err->empty()) *err = std::string("power iteration: ") + cudaGetErrorString(e);
     return -1;
   }
   *L_host = rq;

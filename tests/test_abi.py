@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in decl if not hasattr(L, n)]
     assert not missing, missing
     assert set(decl) == set(A.EXPORTED)
-    assert A.lib().accord_abi_version() == 1
+    assert A.lib().accord_abi_version() == 2
 
 
 def test_status_strings_and_create_error_without_gpu():
@@ -60,6 +60,7 @@ int main(void) {
   printf("accord_info %zu\n", sizeof(accord_info));
   P(accord_init_params, lambda) P(accord_init_params, row_begin) P(accord_init_params, nccl_id)
   P(accord_init_params, stream) P(accord_init_params, cand_capacity)
+  P(accord_init_params, x_sharded) P(accord_init_params, sendrecv)
   P(accord_iter_stats, nnz) P(accord_iter_stats, trials) P(accord_iter_stats, ms_total)
   P(accord_info, f) P(accord_info, device_bytes) P(accord_info, kernel_launches)
   return 0;

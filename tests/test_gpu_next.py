@@ -1,6 +1,7 @@
 """GPU parity of the NEXT rows against the float64 oracle:
 KKT certificate (Eq. 3.3), solve-to-tolerance, bias-correction refit
-(Eq. 3.8), warm-started lambda path with epBIC (Eq. 3.7)."""
+(Eq. 3.8), warm-started lambda path with epBIC (Eq. 3.7), Theta-hat and
+partial correlations."""
 import numpy as np
 import pytest
 
@@ -17,8 +18,6 @@ def _cuda():
         pytest.fail("CUDA not available on a -m gpu run")
 
 
-@pytest.mark.parametrize("key,gemm", [("t_ba_f64", A.GEMM_SIMT), ("t_ba_f32", A.GEMM_AUTO),
-                                      ("t_hubs_f32", A.GEMM_AUTO)])
 def to_csr(W):
     rp = np.zeros(W.shape[0] + 1, dtype=np.int64)
     cols, vals = [], []
@@ -119,3 +118,67 @@ def test_path_epbic_matches_oracle_f64():
     np.testing.assert_allclose(res["epbic"], ref["epbic"], rtol=1e-10)
     assert res["best"] == ref["best"] and lam_sel == grid[ref["best"]]
     assert np.abs(W - ref["Omega"][ref["best"]]).max() < 1e-10
+
+
+def _pc_support(W):
+    """supp(Omega) U supp(Omega^T) off the diagonal."""
+    M = (W != 0) | (W.T != 0)
+    np.fill_diagonal(M, False)
+    return M
+
+
+@pytest.mark.parametrize("key,gemm,T", [("t_ba_f64", A.GEMM_SIMT, 30), ("t_ba_f32", A.GEMM_AUTO, 30),
+                                        ("t_hubs_f32", A.GEMM_AUTO, 12)])
+def test_theta_and_partial_correlations_match_oracle(key, gemm, T):
+    """NEXT(4): Theta-hat = Omega_D Omega and rho-hat on the device vs the
+    oracle's T^{-1} and partial_correlations, applied (a) to
+    the GPU's own Omega (pins the transform, to rounding) and (b) to the
+    oracle's Omega after the same iterations (the parity bar)."""
+    _cuda()
+    pr = make_problem(key)
+    c = pr.cfg
+    lam = c.lambdas[0]
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    with A.AccordSolver(torch.from_numpy(pr.Xt).cuda(), lam, inv_L=inv_L, gemm=gemm) as s:
+        s.step(T)
+        om = s.export_csr()
+        th = s.export_transformed(A.EXPORT_THETA)
+        pc = s.export_transformed(A.EXPORT_PCORR)
+    W = om.to_dense(c.p)
+    f64 = c.dtype == "f64"
+    eps = 1e-14 if f64 else 2e-7
+    # structure: Theta keeps Omega's CSR; rho lives on the symmetrised support, no diagonal
+    assert np.array_equal(th.row_ptr, om.row_ptr) and np.array_equal(th.col, om.col)
+    R = pc.to_dense(c.p)
+    Mpc = np.zeros_like(W, dtype=bool)
+    for i in range(c.p):
+        Mpc[i, pc.col[pc.row_ptr[i]:pc.row_ptr[i + 1]]] = True
+        assert np.all(np.diff(pc.col[pc.row_ptr[i]:pc.row_ptr[i + 1]]) > 0)
+    assert np.array_equal(Mpc, _pc_support(W))
+    # (a) transform of the GPU's own Omega
+    Th_a = O.omega_to_theta(W)
+    R_a = O.partial_correlations(W)
+    assert np.abs(th.to_dense(c.p) - Th_a).max() <= eps * np.abs(Th_a).max()
+    assert np.abs(R - R_a).max() <= eps * max(1.0, np.abs(R_a).max())
+    assert np.abs(R - R.T).max() <= eps                        # symmetric by construction
+    # (b) against the oracle's own iterate
+    ref = O.fbs(pr.Xt, lam, c.tau0, c.beta, inv_L, T=T)["Omega"]
+    tol = 1e-10 if f64 else 1e-5
+    Th_b = O.omega_to_theta(ref)
+    R_b = O.partial_correlations(ref)
+    assert np.abs(th.to_dense(c.p) - Th_b).max() <= tol * np.abs(Th_b).max()
+    assert np.abs(R - R_b).max() <= tol * max(1.0, np.abs(R_b).max())
+
+
+def test_transformed_bad_kind_and_identity():
+    _cuda()
+    pr = make_problem("t_ba_f64")
+    with A.AccordSolver(torch.from_numpy(pr.Xt).cuda(), 0.1, gemm=A.GEMM_SIMT) as s:
+        with pytest.raises(A.AccordError) as e:
+            s.export_transformed(7)
+        assert e.value.status == 1
+        # identity: Theta = I, rho = empty
+        th = s.export_transformed(A.EXPORT_THETA)
+        assert np.array_equal(th.val, np.ones(pr.cfg.p))
+        pc = s.export_transformed(A.EXPORT_PCORR)
+        assert len(pc.col) == 0 and np.all(pc.row_ptr == 0)

@@ -163,3 +163,237 @@ def test_p_invariance_one_gpu(gemm):
             assert np.abs(Wg - W1).max() <= 1e-6 * np.abs(W1).max()
             b, e = bounds[r]
             assert np.array_equal(loc.to_dense(c.p), Wg[b:e])
+
+
+@pytest.mark.gpu
+def test_transformed_exports_p_invariant_one_gpu():
+    """NEXT(4) with P = 2 row blocks (ThreadComm): PCORR needs the transpose
+    across ranks (gathered), THETA is rank-local; both must equal P = 1."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import make_problem
+    from oracle import accord_oracle as O
+    pr = make_problem("t_hubs_f32")
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    X = torch.from_numpy(pr.Xt).cuda()
+    T = 8
+    res = {}
+    for P in (1, 2):
+        comm = ThreadComm(P)
+        bounds = A.partition_rows(c.p, P, align=1)
+        out = [None] * P
+        errs = []
+
+        def run(r):
+            try:
+                comm.bind(r)
+                s = A.AccordSolver(X, c.lambdas[0], inv_L=inv_L, row_begin=bounds[r][0],
+                                   row_end=bounds[r][1], rank=r, world=P, comm=A.COMM_HOST,
+                                   allreduce=comm.allreduce, allgatherv=comm.allgatherv,
+                                   stream=torch.cuda.Stream())
+                s.step(T)
+                got = {}
+                for kind in (A.EXPORT_THETA, A.EXPORT_PCORR):
+                    for sc in (A.SCOPE_LOCAL, A.SCOPE_GATHER):
+                        got[(kind, sc)] = s.export_transformed(kind, sc)
+                out[r] = got
+                s.close()
+            except Exception as e:
+                errs.append(e)
+                comm.barrier.abort()
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        res[P] = (out, bounds)
+    one = res[1][0][0]
+    for kind in (A.EXPORT_THETA, A.EXPORT_PCORR):
+        full = one[(kind, A.SCOPE_GATHER)].to_dense(c.p)
+        out, bounds = res[2]
+        for r in range(2):
+            g = out[r][(kind, A.SCOPE_GATHER)].to_dense(c.p)
+            assert np.abs(g - full).max() <= 1e-6 * max(1.0, np.abs(full).max())
+            b, e = bounds[r]
+            loc = out[r][(kind, A.SCOPE_LOCAL)]
+            assert loc.row_begin == b
+            assert np.array_equal(loc.to_dense(c.p), g[b:e])
+
+
+def test_thread_comm_sendrecv_ring():
+    """The ring exchange of the sharded-X mode (NEXT(3)): rank r sends its
+    block to r-1 and receives r+1's; blocks of different sizes."""
+    import ctypes as C
+    P = 3
+    comm = ThreadComm(P)
+    results = [None] * P
+
+    def run(r):
+        comm.bind(r)
+        mine = (C.c_uint8 * (r + 2))(*([r] * (r + 2)))
+        src = (r + 1) % P
+        got = (C.c_uint8 * (src + 2))()
+        rc = comm.sendrecv(None, C.addressof(mine), r + 2, (r - 1) % P, C.addressof(got),
+                           src + 2, src)
+        results[r] = (rc, list(got))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r, (rc, got) in enumerate(results):
+        src = (r + 1) % P
+        assert rc == 0 and got == [src] * (src + 2)
+
+
+def _gloo_ring_worker(rank, world, port, q):
+    import ctypes as C
+    import torch.distributed as dist
+    from paper_2412_11554_b200.comm import TorchDistComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchDistComm()
+        src = (rank + 1) % world
+        mine = (C.c_uint8 * (rank + 3))(*([rank + 7] * (rank + 3)))
+        got = (C.c_uint8 * (src + 3))()
+        rc = comm.sendrecv(None, C.addressof(mine), rank + 3, (rank - 1) % world,
+                           C.addressof(got), src + 3, src)
+        q.put((rank, rc, list(got)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sendrecv_ring():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_ring_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, rc, got in res:
+        src = (rank + 1) % 2
+        assert rc == 0 and got == [src + 7] * (src + 3)
+
+
+def run_ranks_sharded(Xt, lam, T, inv_L, P, gemm, layout="variables", extra=None):
+    """P ranks on one GPU, each holding only its slab of X (x_sharded)."""
+    import torch
+    comm = ThreadComm(P)
+    p = Xt.shape[0]
+    bounds = A.partition_rows(p, P)
+    out = [None] * P
+    errs = []
+
+    def run(r):
+        try:
+            comm.bind(r)
+            b, e = bounds[r]
+            slab = np.ascontiguousarray(Xt[b:e] if layout == "variables" else Xt[b:e].T)
+            s = A.AccordSolver(torch.from_numpy(slab).cuda(), lam, layout=layout, inv_L=inv_L,
+                               gemm=gemm, row_begin=b, row_end=e, rank=r, world=P,
+                               comm=A.COMM_HOST, allreduce=comm.allreduce,
+                               allgatherv=comm.allgatherv, sendrecv=comm.sendrecv,
+                               x_sharded=True, p_global=p, stream=torch.cuda.Stream())
+            st = s.step(T)
+            res = {"st": st, "g": s.export_csr(A.SCOPE_GATHER), "f": s.objective()[0],
+                   "L": s.info()["L"]}
+            if extra:
+                res.update(extra(s))
+            s.close()
+            out[r] = res
+        except Exception as ex:
+            errs.append(ex)
+            comm.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out, bounds
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key,gemm", [("t_ba_f64", A.GEMM_SIMT), ("t_hubs_f32", A.GEMM_SIMT),
+                                      ("t_hubs_f32", A.GEMM_BF16_FILTER),
+                                      ("t_hubs_f32", A.GEMM_BF16X3)])
+def test_sharded_x_ring_matches_replicated(key, gemm):
+    """NEXT(3): X split by variables over P ranks, every pass over X done as a
+    ring of slab exchanges (Alg. 2), must reproduce the replicated P = 1 run:
+    identical tau schedule, Omega within rounding (the SpMM sums the slabs in
+    ring order, in float64), and the oracle within the parity bar."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import make_problem
+    from oracle import accord_oracle as O
+    pr = make_problem(key)
+    c = pr.cfg
+    lam = c.lambdas[0]
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    ref, _ = run_ranks(pr.Xt, lam, c.T, inv_L, 1, gemm)
+    taus1 = [s["tau"] for s in ref[0][0]]
+    W1 = ref[0][1].to_dense(c.p)
+    orc = O.fbs(pr.Xt, lam, c.tau0, c.beta, inv_L, T=c.T)
+    f64 = c.dtype == "f64"
+    for P in (2, 3) if c.p >= 768 else (2,):
+        out, bounds = run_ranks_sharded(pr.Xt, lam, c.T, inv_L, P, gemm)
+        for r in range(P):
+            o = out[r]
+            assert [s["tau"] for s in o["st"]] == taus1
+            assert abs(o["f"] - ref[0][3]) <= (1e-12 if f64 else 1e-9) * abs(o["f"])
+            W = o["g"].to_dense(c.p)
+            assert np.abs(W - W1).max() <= (1e-12 if f64 else 1e-6) * np.abs(W1).max()
+            assert np.array_equal(W != 0, W1 != 0) or not f64
+            assert np.abs(W - orc["Omega"]).max() <= (1e-10 if f64 else 1e-5) * \
+                np.abs(orc["Omega"]).max()
+
+
+@pytest.mark.gpu
+def test_sharded_x_power_iteration_refit_kkt_and_layout():
+    """Sharded mode end to end: L by the sharded power iteration (allreduce of
+    X v), samples-major slabs, refit (refine ring) and the KKT certificate."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import make_problem
+    from oracle import accord_oracle as O
+    pr = make_problem("t_hubs_f32")
+    c = pr.cfg
+    lam = c.lambdas[0]
+
+    def extra(s):
+        kkt = s.kkt_residual()
+        s.refit(0.0)
+        st2 = s.step(5)
+        return {"kkt": kkt, "st2": st2, "g2": s.export_csr(A.SCOPE_GATHER)}
+
+    # reference: replicated single context, same calls
+    X = torch.from_numpy(pr.Xt).cuda()
+    with A.AccordSolver(X, lam, inv_L=0.0) as s:
+        st = s.step(6)
+        L1 = s.info()["L"]
+        ref = {"st": st, **extra(s)}
+    out, _ = run_ranks_sharded(pr.Xt, lam, 6, 0.0, 2, A.GEMM_AUTO, layout="samples", extra=extra)
+    for o in out:
+        assert abs(o["L"] - L1) <= 1e-9 * L1
+        assert [x["tau"] for x in o["st"]] == [x["tau"] for x in ref["st"]]
+        assert [x["tau"] for x in o["st2"]] == [x["tau"] for x in ref["st2"]]
+        assert abs(o["kkt"] - ref["kkt"]) <= 1e-6 * max(1.0, ref["kkt"])
+        W, Wr = o["g2"].to_dense(c.p), ref["g2"].to_dense(c.p)
+        assert np.abs(W - Wr).max() <= 1e-6 * np.abs(Wr).max()
