@@ -133,8 +133,9 @@ typedef struct {
   int32_t x_sharded;        /* 0: X holds all p variables (replicated on every rank).
                                1: X holds only this rank's variables [row_begin, row_end)
                                (n x p_k samples-major or p_k x n variables-major); the
-                               rank blocks must tile [0, p) in rank order, each starting at
-                               a multiple of 256. Collective passes over X run as a ring
+                               rank blocks must tile [0, p) in rank order (with a tensor-core
+                               GEMM each starting at a multiple of 256, the GEMM tile).
+                               Collective passes over X run as a ring
                                (Alg. 2): NCCL send/recv on a split
                                communicator, or `sendrecv` with ACCORD_COMM_HOST. */
   accord_sendrecv_fn sendrecv;       /* ACCORD_COMM_HOST with x_sharded */

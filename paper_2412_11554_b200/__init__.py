@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaccord.so")
+LIB_PATH = os.environ.get("ACCORD_LIB") or os.path.join(HERE, "libaccord.so")   # override: A-B tools
 
 # enums (accord.h)
 OK = 0

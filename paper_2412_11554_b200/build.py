@@ -42,17 +42,26 @@ def up_to_date() -> bool:
     return os.path.exists(OUT) and os.path.getmtime(OUT) >= _newest_input_mtime()
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """defines/out: diagnostic variants (e.g. an A-B build next to the product
+    library); the product is the default build to OUT."""
+    global OUT
+    if out is not None:
+        prev, OUT = OUT, out
+        try:
+            return build(verbose, True, defines)
+        finally:
+            OUT = prev
     if not force and up_to_date():
         return OUT
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if not defines else "build_variant")
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     objs = []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(objdir, s + ".o")
-        cmd = [nvcc_path(), *NVCC_FLAGS, *inc, "-c", src, "-o", obj]
+        cmd = [nvcc_path(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], *inc, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

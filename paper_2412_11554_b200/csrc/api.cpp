@@ -310,7 +310,7 @@ void ring_pass(accord_ctx* c, bool want_bf16, F&& fn) {
       }
     }
     fn(slab, bsel, c->vb[j], c->vb[j + 1], s == 0, s == P - 1);
-    if (s > 0) CK(cudaEventRecord(c->ev_comp[(s - 1) & 1], c->st));
+    if (s > 0 && c->comm == ACCORD_COMM_NCCL) CK(cudaEventRecord(c->ev_comp[(s - 1) & 1], c->st));
   }
 }
 
@@ -445,8 +445,7 @@ void validate(const accord_init_params* prm) {
   if (prm->comm == ACCORD_COMM_HOST && !prm->allreduce) bad("allreduce callback is NULL");
   if (shard && prm->comm == ACCORD_COMM_HOST && !prm->sendrecv)
     bad("x_sharded with the host communicator needs a sendrecv callback");
-  if (shard && prm->row_begin % kRowPad != 0)
-    bad("x_sharded: row_begin must be a multiple of 256");
+
   if (prm->gemm < ACCORD_GEMM_AUTO || prm->gemm > ACCORD_GEMM_BF16_FILTER) bad("bad gemm kind");
   if (prm->dtype == ACCORD_F64 &&
       (prm->gemm == ACCORD_GEMM_BF16X3 || prm->gemm == ACCORD_GEMM_BF16_FILTER))
@@ -519,6 +518,9 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     c->gemm = prm->gemm;
   const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
   if (tc && !tc_ok) throw Fail{ACCORD_E_UNSUPPORTED, "tcgen05 GEMM needs an sm_100 device"};
+  if (tc && prm->x_sharded && prm->world > 1 && prm->row_begin % kRowPad != 0)
+    throw Fail{ACCORD_E_INVALID,
+               "x_sharded with a tensor-core GEMM: row_begin must be a multiple of 256"};
   if (c->gemm == ACCORD_GEMM_BF16_FILTER && c->ldk > kMaxFilterK)
     throw Fail{ACCORD_E_UNSUPPORTED, "BF16_FILTER supports n <= 4096"};
 

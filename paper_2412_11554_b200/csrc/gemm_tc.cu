@@ -61,11 +61,12 @@ constexpr uint32_t kTileB = BNH * BK * 2;       // 16 KB
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
-template <int kMode> struct Cfg {
+template <int kMode, int kStagesT> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
   static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 64 / 32 KB
-  static constexpr int kStages = kMode == 0 ? 3 : 7;   // 7 x 32 KB + barriers <= 227 KB
+  static constexpr int kStages = kStagesT;
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
+  static_assert(kSmemBytes <= 232448, "shared memory");
 };
 
 // Tile order. Work unit = up to `U` consecutive N-blocks at a fixed M-block,
@@ -130,7 +131,7 @@ struct TileIt {
   __device__ bool unit_start() const { return ni == 0; }
 };
 
-template <int kMode>
+template <int kMode, int kStagesT, bool kFast>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
@@ -139,8 +140,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                int num_n,
                int group_n, int unit_n, int dbg, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
-  constexpr int kStages = Cfg<kMode>::kStages;
-  constexpr uint32_t kStageBytes = Cfg<kMode>::kStageBytes;
+  constexpr int kStages = Cfg<kMode, kStagesT>::kStages;
+  constexpr uint32_t kStageBytes = Cfg<kMode, kStagesT>::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + kStages * kStageBytes);
@@ -208,7 +209,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     __syncwarp();
   } else if (warp == 1) {
     // ============================ MMA issuer (leader) =====================
+    // The whole warp runs the loop (so the descriptors stay warp-uniform and
+    // live in uniform registers); one elected lane issues the MMAs/commits.
+#ifdef ACCORD_MMA_LANE0   // A-B diagnostic build: the loop in lane 0 only
     if (leader && lane == 0) {
+#else
+    if (leader) {
+#endif
       constexpr uint32_t idesc = tc::idesc_bf16_f32(2 * BM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -229,21 +236,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           // the last k-block issues only the K16 steps that reach a sample
           // (the rest of its box is TMA zero fill past n)
           const int nkk = kb == num_kb - 1 ? kk_last : BK / 16;
+          if (tc::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            if (kk >= nkk) break;
-            const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 = 32 B along K
-            const uint32_t accum = (kb | kk) != 0;
-            if (dbg != 2) tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
-            if constexpr (kMode == 0) {
-              tc::mma_bf16<2>(d, a_hi + off, b_lo + off, idesc, 1);
-              tc::mma_bf16<2>(d, a_lo + off, b_hi + off, idesc, 1);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              if (kk >= nkk) break;
+              const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 = 32 B along K
+              const uint32_t accum = (kb | kk) != 0;
+              if (dbg != 2) tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
+              if constexpr (kMode == 0) {
+                tc::mma_bf16<2>(d, a_hi + off, b_lo + off, idesc, 1);
+                tc::mma_bf16<2>(d, a_lo + off, b_hi + off, idesc, 1);
+              }
             }
+            tc::mma_commit_mc(tc::smem_u32(&empty[stage]), 0x3);   // free the slot in both CTAs
           }
-          tc::mma_commit_mc(tc::smem_u32(&empty[stage]), 0x3);   // free the slot in both CTAs
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc::mma_commit_mc(tc::smem_u32(&tfull[acc]), 0x3);       // accumulator ready
+        if (tc::elect_one()) tc::mma_commit_mc(tc::smem_u32(&tfull[acc]), 0x3);   // acc ready
+        __syncwarp();
         if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -324,10 +335,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             // common case first: no |acc| in these 32 columns passes the fast
             // test (one FMNMX per value instead of a compare + select + add)
             float m0 = 0.f, m1 = 0.f;
+            if constexpr (kFast) {
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
-              m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
+              for (int c = 0; c < 32; c += 2) {
+                m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
+                m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
+              }
+            } else {
+              m0 = INFINITY;
             }
             if (fmaxf(m0, m1) > tfast) {
 #pragma unroll
@@ -504,6 +519,7 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            const __nv_bfloat16* Xhi, const __nv_bfloat16* Xlo, int64_t xrows_pad,
                            int64_t p_pad, int64_t kdim, int64_t ldk, std::string* err) {
   auto* p = new TcGemmPlan();
+  if (std::getenv("ACCORD_GEMM_KFULL")) kdim = ldk;   // A-B diagnostic: no K-tail trim
   p->pk_pad = pk_pad;
   p->p_pad = p_pad;
   p->ldk = ldk;
@@ -527,10 +543,14 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
   cudaMemset(p->blk_sdmax, 0, (p_pad / BN) * sizeof(float2));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg<0>::kSmemBytes);
-    cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg<1>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<0, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg<0, 3>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg<1, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg<1, 7>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg<1, 6>::kSmemBytes);
     attr = true;
   }
   return p;
@@ -571,7 +591,7 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   const int grid = tc_grid_size(plan, sm_count);
   // A group of <= 64 N-blocks (<= 32 MB of X^T_hi at n = 1000) stays in L2;
   // units small enough that the per-cluster imbalance is <= ~6% of its work
-  int gn = 64;
+  int gn = 32;   // measured best of 16..64 at c5 (tools/gemm_sweep.py)
   if (const char* e = std::getenv("ACCORD_GEMM_GN")) gn = std::max(1, std::atoi(e));   // tuning
   const int group_n = num_n < gn ? num_n : gn;
   const long long tiles = (long long)num_m * num_n;
@@ -582,18 +602,26 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   // 1 = skip the epilogue, 2 = skip the MMAs
   const char* dbg_env = std::getenv("ACCORD_DEBUG_GEMM");
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+  // ACCORD_GEMM_VARIANT (tuning / A-B diagnostics, results identical):
+  // 0 = 6-stage ring + FMNMX3 fast path (default), 1 = 7 stages, 2 = no fast path
+  int var = 0;
+  if (const char* e = std::getenv("ACCORD_GEMM_VARIANT")) var = std::atoi(e);
+#define ACCORD_TC_ARGS(bsel_lo)                                                               \
+  plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi[bsel], bsel_lo, num_kb, kk_last, num_m,   \
+      num_n, group_n, unit_n, dbg, ep, plan->blk_sdmax, om, pool
   if (mode == ACCORD_GEMM_BF16X3)
-    gemm_tc_kernel<0><<<grid, kThreads, Cfg<0>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi[bsel], plan->b_lo[bsel], num_kb, kk_last,
-        num_m, num_n,
-        group_n, unit_n, dbg,
-        ep, plan->blk_sdmax, om, pool);
+    gemm_tc_kernel<0, 3, true><<<grid, kThreads, Cfg<0, 3>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_lo[bsel]));
+  else if (var == 1)
+    gemm_tc_kernel<1, 7, true><<<grid, kThreads, Cfg<1, 7>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
+  else if (var == 2)
+    gemm_tc_kernel<1, 6, false><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
   else
-    gemm_tc_kernel<1><<<grid, kThreads, Cfg<1>::kSmemBytes, st>>>(
-        plan->a_hi[ybuf], plan->a_hi[ybuf], plan->b_hi[bsel], plan->b_hi[bsel], num_kb, kk_last,
-        num_m, num_n,
-        group_n, unit_n, dbg,
-        ep, plan->blk_sdmax, om, pool);
+    gemm_tc_kernel<1, 6, true><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
+#undef ACCORD_TC_ARGS
   return 1;
 }
 

@@ -1,8 +1,10 @@
-"""Diagnostic (not the product): time the c5 gradient GEMM under different
-tile schedules (ACCORD_GEMM_GN = N-blocks per L2-resident X^T group,
-ACCORD_GEMM_UNIT = consecutive N-blocks per work unit), alternating settings
-so that slow drift in clocks hits all of them alike.
-Usage: python tools/gemm_sweep.py [config] [GN,UNIT ...]"""
+"""Diagnostic (not the product): time the c5 gradient GEMM under kernel
+variants and tile schedules, alternating the settings so that slow clock
+drift hits all of them alike. Each setting is "VAR,GN[,UNIT]":
+ACCORD_GEMM_VARIANT (0 default, 1 = 7-stage ring, 2 = no FMNMX3 fast path),
+ACCORD_GEMM_GN (N-blocks per L2-resident X^T group), ACCORD_GEMM_UNIT.
+--kfull runs a second solver built with ACCORD_GEMM_KFULL (no K-tail trim).
+Usage: python tools/gemm_sweep.py [config] [--kfull] VAR,GN[,UNIT] ..."""
 import os
 import sys
 
@@ -12,23 +14,37 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2412_11554_b200 as A  # noqa: E402
 from accord_inputs import get_config, make_problem  # noqa: E402
 
-cfg = get_config(sys.argv[1] if len(sys.argv) > 1 else "5")
-settings = [tuple(int(x) for x in a.split(",")) for a in sys.argv[2:]] or \
-    [(64, 0), (32, 0), (16, 0), (48, 0)]
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+kfull = "--kfull" in sys.argv
+cfg = get_config(args[0] if args else "5")
+settings = [tuple(int(x) for x in a.split(",")) for a in args[1:]] or [(0, 64)]
 pr = make_problem(cfg, with_blocks=False)
 X = torch.from_numpy(pr.Xt).cuda()
+
+
+def run(solver, tag):
+    res = {st: [] for st in settings}
+    for rep in range(3):
+        for st in settings:
+            os.environ["ACCORD_GEMM_VARIANT"] = str(st[0])
+            os.environ["ACCORD_GEMM_GN"] = str(st[1])
+            if len(st) > 2:
+                os.environ["ACCORD_GEMM_UNIT"] = str(st[2])
+            else:
+                os.environ.pop("ACCORD_GEMM_UNIT", None)
+            res[st].append(solver.step(1)[0]["ms_gemm"])
+    for k, v in res.items():
+        print(tag, "VAR,GN,UNIT", k, "ms_gemm", [round(x, 1) for x in v], "min",
+              round(min(v), 1), flush=True)
+
+
 s = A.AccordSolver(X, cfg.lambdas[0], inv_L=0.0)
 s.step(3)
-res = {st: [] for st in settings}
-for rep in range(3):
-    for gn, un in settings:
-        os.environ["ACCORD_GEMM_GN"] = str(gn)
-        if un:
-            os.environ["ACCORD_GEMM_UNIT"] = str(un)
-        else:
-            os.environ.pop("ACCORD_GEMM_UNIT", None)
-        st = s.step(1)
-        res[(gn, un)].append(st[0]["ms_gemm"])
-for k, v in res.items():
-    print("GN", k[0], "UNIT", k[1], "ms_gemm", [round(x, 1) for x in v],
-          "min", round(min(v), 1), flush=True)
+run(s, "ktrim")
+s.close()
+if kfull:
+    os.environ["ACCORD_GEMM_KFULL"] = "1"
+    s = A.AccordSolver(X, cfg.lambdas[0], inv_L=0.0)
+    s.step(3)
+    run(s, "kfull")
+    s.close()
