@@ -26,6 +26,10 @@
 //   warp 0  TMA producer (both CTAs; the bytes are credited to the leader's
 //           full barrier), SWIZZLE_128B, kStages-deep ring
 //   warp 1  MMA issuer (leader only), commits multicast to both CTAs
+//           (warps 0 and 1 run their loops warp-wide so that descriptors and
+//           coordinates stay in uniform registers; an elect.sync lane issues:
+//           single-lane loops made ptxas wrap every UTCHMMA in an ELECT/R2UR
+//           waterfall, which left the tensor pipe ~70% busy)
 //   warp 2  TMEM allocator (512 columns = 2 accumulator stages)
 //   warps 4-7 epilogue (both CTAs): TMEM -> registers (32x32b), candidate
 //           rule, warp prefix-sum compaction into the candidate pool, one
@@ -138,7 +142,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mB_hi,
                const __grid_constant__ CUtensorMap mB_lo, int num_kb, int kk_last, int num_m,
                int num_n,
-               int group_n, int unit_n, int dbg, EpiParams ep, const float2* __restrict__ blk_sdmax, OmegaView om,
+               int group_n, int unit_n, int dbg, int l2hint, EpiParams ep,
+               const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
   constexpr int kStages = Cfg<kMode, kStagesT>::kStages;
   constexpr uint32_t kStageBytes = Cfg<kMode, kStagesT>::kStageBytes;
@@ -182,7 +187,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
 
   if (warp == 0) {
     // ============================ TMA producer (both CTAs) ================
-    if (lane == 0) {
+    // warp-wide loop (uniform operands), one elected lane issues
+    {
+      const uint64_t bpol = l2hint == 2 ? tc::policy_evict_first() : tc::policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
@@ -192,16 +199,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           tc::mbar_wait(tc::smem_u32(&empty[stage]), phase ^ 1);
           uint8_t* s = smem + stage * kStageBytes;
           const uint32_t fb_local = tc::smem_u32(&full[stage]);
-          if (leader) tc::mbar_arrive_expect_tx(fb_local, 2 * kStageBytes);   // both CTAs' bytes
           const uint32_t fb = tc::mapa_shared(fb_local, 0);                  // leader's barrier
           const int kx = kb * BK;
-          // stage layout: A_hi | B_hi | (A_lo | B_lo)
-          tc::tma_load_2d_cg2(tc::smem_u32(s), &mA_hi, fb, kx, ya);
-          tc::tma_load_2d_cg2(tc::smem_u32(s + kTileA), &mB_hi, fb, kx, yb);
-          if constexpr (kMode == 0) {
-            tc::tma_load_2d_cg2(tc::smem_u32(s + kTileA + kTileB), &mA_lo, fb, kx, ya);
-            tc::tma_load_2d_cg2(tc::smem_u32(s + 2 * kTileA + kTileB), &mB_lo, fb, kx, yb);
+          if (tc::elect_one()) {
+            if (leader) tc::mbar_arrive_expect_tx(fb_local, 2 * kStageBytes);   // both CTAs' bytes
+            // stage layout: A_hi | B_hi | (A_lo | B_lo)
+            if (l2hint) {   // X^T group: keep in L2 (every pair re-reads it); Y: normal
+              tc::tma_load_2d_cg2(tc::smem_u32(s), &mA_hi, fb, kx, ya);
+              tc::tma_load_2d_cg2_hint(tc::smem_u32(s + kTileA), &mB_hi, fb, kx, yb, bpol);
+            } else {
+              tc::tma_load_2d_cg2(tc::smem_u32(s), &mA_hi, fb, kx, ya);
+              tc::tma_load_2d_cg2(tc::smem_u32(s + kTileA), &mB_hi, fb, kx, yb);
+            }
+            if constexpr (kMode == 0) {
+              tc::tma_load_2d_cg2(tc::smem_u32(s + kTileA + kTileB), &mA_lo, fb, kx, ya);
+              tc::tma_load_2d_cg2(tc::smem_u32(s + 2 * kTileA + kTileB), &mB_lo, fb, kx, yb);
+            }
           }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -211,11 +226,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     // ============================ MMA issuer (leader) =====================
     // The whole warp runs the loop (so the descriptors stay warp-uniform and
     // live in uniform registers); one elected lane issues the MMAs/commits.
-#ifdef ACCORD_MMA_LANE0   // A-B diagnostic build: the loop in lane 0 only
-    if (leader && lane == 0) {
-#else
     if (leader) {
-#endif
       constexpr uint32_t idesc = tc::idesc_bf16_f32(2 * BM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -606,9 +617,12 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   // 0 = 6-stage ring + FMNMX3 fast path (default), 1 = 7 stages, 2 = no fast path
   int var = 0;
   if (const char* e = std::getenv("ACCORD_GEMM_VARIANT")) var = std::atoi(e);
+  // ACCORD_GEMM_L2HINT (tuning): 1 = TMA loads of X^T with evict_last, 2 = evict_first
+  int l2hint = 0;
+  if (const char* e = std::getenv("ACCORD_GEMM_L2HINT")) l2hint = std::atoi(e);
 #define ACCORD_TC_ARGS(bsel_lo)                                                               \
   plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi[bsel], bsel_lo, num_kb, kk_last, num_m,   \
-      num_n, group_n, unit_n, dbg, ep, plan->blk_sdmax, om, pool
+      num_n, group_n, unit_n, dbg, l2hint, ep, plan->blk_sdmax, om, pool
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0, 3, true><<<grid, kThreads, Cfg<0, 3>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_lo[bsel]));

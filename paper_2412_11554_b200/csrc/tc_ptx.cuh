@@ -97,6 +97,27 @@ __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap*
       : "memory");
 }
 
+// Same, with an L2 cache-policy hint (createpolicy_*).
+__device__ __forceinline__ void tma_load_2d_cg2_hint(uint32_t dst, const CUtensorMap* m,
+                                                     uint32_t bar_cluster, int32_t x, int32_t y,
+                                                     uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // ----------------------------------------------------------------- tcgen05 --
 template <int kCols, int kGroup>
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {
@@ -201,9 +222,6 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
 
 // One lane of the (converged) warp is elected; the others get false.
 __device__ __forceinline__ bool elect_one() {
-#ifdef ACCORD_MMA_LANE0
-  return true;
-#endif
   uint32_t pred = 0;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"

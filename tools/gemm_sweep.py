@@ -1,6 +1,6 @@
 """Diagnostic (not the product): time the c5 gradient GEMM under kernel
 variants and tile schedules, alternating the settings so that slow clock
-drift hits all of them alike. Each setting is "VAR,GN[,UNIT]":
+drift hits all of them alike. Each setting is "VAR,GN[,UNIT[,L2HINT]]" (UNIT 0 = default):
 ACCORD_GEMM_VARIANT (0 default, 1 = 7-stage ring, 2 = no FMNMX3 fast path),
 ACCORD_GEMM_GN (N-blocks per L2-resident X^T group), ACCORD_GEMM_UNIT.
 --kfull runs a second solver built with ACCORD_GEMM_KFULL (no K-tail trim).
@@ -28,10 +28,11 @@ def run(solver, tag):
         for st in settings:
             os.environ["ACCORD_GEMM_VARIANT"] = str(st[0])
             os.environ["ACCORD_GEMM_GN"] = str(st[1])
-            if len(st) > 2:
+            if len(st) > 2 and st[2]:
                 os.environ["ACCORD_GEMM_UNIT"] = str(st[2])
             else:
                 os.environ.pop("ACCORD_GEMM_UNIT", None)
+            os.environ["ACCORD_GEMM_L2HINT"] = str(st[3]) if len(st) > 3 else "0"
             res[st].append(solver.step(1)[0]["ms_gemm"])
     for k, v in res.items():
         print(tag, "VAR,GN,UNIT", k, "ms_gemm", [round(x, 1) for x in v], "min",
