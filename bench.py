@@ -172,10 +172,10 @@ def metric_name(cfg):
     return f"prox-grad iterations/s (ACCORD-FBS, p={cfg.p}, n={cfg.n})"
 
 
-def workload_config(cfg, world, gemm):
+def workload_config(cfg, world, gemm, sharded=False):
     return {"workload": cfg.name, "p": cfg.p, "n": cfg.n, "lambda": cfg.lambdas[0],
             "tau0": cfg.tau0, "beta": cfg.beta, "x_dtype": cfg.dtype, "gemm": gemm,
-            "parallelism": f"row-block x{world} (X replicated)",
+            "parallelism": f"row-block x{world} (X {'sharded, ring' if sharded else 'replicated'})",
             "l2": "inputs larger than L2 (X^T 4 GB f32 + bf16 copy vs 126 MB L2)"
             if cfg.p * cfg.n * 4 > 126e6 else "L2 flushed between steps"}
 
@@ -201,11 +201,16 @@ def run_ours(args, rank, world, local_rank):
         nid = obj[0]
         comm = A.COMM_NCCL
     stream = torch.cuda.current_stream(dev)
-    Xd = torch.from_numpy(pr.Xt).to(f"cuda:{dev}")
+    # --x-sharded (N > 1): each rank holds only its variables' slab of X and
+    # every pass over X runs as a ring (Alg. 2); default: X replicated
+    shard = bool(args.x_sharded and world > 1)
+    Xh_all = pr.Xt[r0:r1] if shard else pr.Xt
+    skw = dict(x_sharded=True, p_global=p) if shard else {}
+    Xd = torch.from_numpy(np.ascontiguousarray(Xh_all)).to(f"cuda:{dev}")
     t_setup = time.perf_counter()
     solver = A.AccordSolver(Xd, lam, tau0=cfg.tau0, beta=cfg.beta, inv_L=0.0, row_begin=r0,
                             row_end=r1, rank=rank, world=world, comm=comm, nccl_id=nid,
-                            stream=stream, device=dev)
+                            stream=stream, device=dev, **skw)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     del Xd
@@ -247,14 +252,14 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: public API with host buffers (pinned X -> create -> K steps -> CSR to host)
     e2e = None
     if not args.no_e2e:
-        Xh = torch.from_numpy(pr.Xt).pin_memory()
+        Xh = torch.from_numpy(np.ascontiguousarray(Xh_all)).pin_memory()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s2 = A.AccordSolver(Xh, lam, tau0=cfg.tau0, beta=cfg.beta, inv_L=0.0, row_begin=r0,
                             row_end=r1, rank=rank, world=world, comm=comm, nccl_id=nid,
-                            stream=stream, device=dev)
+                            stream=stream, device=dev, **skw)
         s2.step(args.steps)
         csr = s2.export_csr()
         torch.cuda.synchronize()
@@ -266,7 +271,7 @@ def run_ours(args, rank, world, local_rank):
             te = float(tt[0])
         d2h = csr.row_ptr.nbytes + csr.col.nbytes + csr.val.nbytes
         e2e = {"value": args.steps / te, "unit": "iterations/s",
-               "h2d_bytes_per_step": int(pr.Xt.nbytes // args.steps),
+               "h2d_bytes_per_step": int(Xh_all.nbytes // args.steps),
                "d2h_bytes_per_step": int(d2h // args.steps),
                "note": "one solve through the C ABI from pinned host X: create (H2D copy, "
                        "power iteration for L, operand split) + K iterations + CSR export "
@@ -305,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "f32",
         "gemm_arith": "bf16 x bf16 -> fp32 TMEM (certified filter) + f64-accumulated refine",
         "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
-        "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]]),
+        "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]], shard),
         "effective_tflops": flops_iter * value / 1e12,
         "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel<1> (bf16 filter + epilogue)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -338,6 +343,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=16)
     ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--x-sharded", action="store_true",
+                    help="N > 1: shard X by variables (ring passes, NEXT(3)) instead of replicating")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
