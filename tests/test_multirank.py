@@ -397,3 +397,32 @@ def test_sharded_x_power_iteration_refit_kkt_and_layout():
         assert abs(o["kkt"] - ref["kkt"]) <= 1e-6 * max(1.0, ref["kkt"])
         W, Wr = o["g2"].to_dense(c.p), ref["g2"].to_dense(c.p)
         assert np.abs(W - Wr).max() <= 1e-6 * np.abs(Wr).max()
+
+
+@pytest.mark.gpu
+def test_sharded_x_ring_config3_scale():
+    """Sharded ring at BASELINE config 3 scale (p = 20000, n = 1000, many GEMM
+    tiles per slab, ragged last slab): P = 2 and 3 must reproduce the
+    replicated run (tau schedule, objective, Omega)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import get_config, make_problem
+    cfg = get_config("3")
+    pr = make_problem(cfg, with_blocks=False)
+    lam, T = cfg.lambdas[0], 6
+    X = torch.from_numpy(pr.Xt).cuda()
+    with A.AccordSolver(X, lam, inv_L=0.0) as s:
+        st1 = s.step(T)
+        W1 = s.export_csr()
+        f1 = s.objective()[0]
+        L1 = s.info()["L"]
+    del X
+    for P in (2, 3):
+        out, bounds = run_ranks_sharded(pr.Xt, lam, T, 1.0 / L1, P, A.GEMM_AUTO)
+        for o in out:
+            assert [x["tau"] for x in o["st"]] == [x["tau"] for x in st1]
+            assert abs(o["f"] - f1) <= 1e-9 * abs(f1)
+            g = o["g"]
+            assert np.array_equal(g.row_ptr, W1.row_ptr) and np.array_equal(g.col, W1.col)
+            assert np.abs(g.val - W1.val).max() <= 1e-6 * np.abs(W1.val).max()
