@@ -118,11 +118,20 @@ int launch_pcorr_value(int dtype, int64_t a, int64_t b, const int64_t* ptr, cons
                        const void* val, const double* d, const int64_t* optr,
                        const uint64_t* keys, int32_t* ocol, void* oval, cudaStream_t st);
 
-// Prox at trial tau over C (Eq. 3.5) with per-row partial sums.
+// Prox at trial tau over C (Eq. 3.5) with per-row partial sums. With items:
+// a warp per work item (hub rows split), per-item sums combined per row in
+// item order.
+struct ProxItems {
+  const int64_t* itm_ptr;     // [pk + 1] (NULL: warp per row)
+  const int32_t* item_row;    // [n_items]
+  int64_t n_items, L;
+  double *dd, *l1, *logd;     // [n_items] per-item partial sums
+  int32_t* nnz;
+};
 int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
                 const void* c_g, const void* c_w, void* c_wn, double tau, double lam,
                 double* row_dd, double* row_l1, double* row_logd, int32_t* row_nnz,
-                cudaStream_t st);
+                cudaStream_t st, const ProxItems* items = nullptr);
 
 // SpMM Y+ = Omega+ X^T and D = Delta X^T over a CSR (ptr/col/wn/wo); wo may be
 // NULL (Delta = 0). Accumulates in double; writes Y (T), optionally its bf16
@@ -143,10 +152,39 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 // Exact candidate values: c_g[e] = (1/n) sum_m Y_im Xt_km in float64
 // accumulation, for every entry of C (block per row). BF16_FILTER refine and
 // the fixed-support gradient of the refit.
+// Work items over a CSR (row chunks of <= L entries; rows longer than L
+// become several items) for the TMA-staged SpMM and the refine.
+constexpr int kSpmmTmaMaxConsumers = 512;
+constexpr int64_t kItemEntries = 2048;
+struct SpmmItems {
+  const int64_t* itm_ptr;     // [rows + 1] exclusive scan of items per row
+  const int32_t* item_row;    // [items] row of each item
+  const int64_t* slot_ptr;    // [rows + 1] scratch slots of multi-item rows
+  double* part_y;             // [slots x ldk] partial Y+ of multi-item rows
+  double* part_d;             // [slots x ldk] partial D
+  int32_t* row_done;          // [rows] items finished (reset to 0 by the finisher)
+  int64_t L;
+};
+int launch_item_map(int64_t rows, const int64_t* ptr, int64_t L, int32_t* nitem, int32_t* nslot,
+                    int64_t* itm_ptr, int64_t* slot_ptr, void* scan_tmp, size_t scan_tmp_bytes,
+                    cudaStream_t st);
+int launch_item_rows(int64_t rows, const int64_t* itm_ptr, int32_t* item_row, cudaStream_t st);
+bool spmm_tma_supported(int dtype, int64_t ldk);
+// Producer warp + cp.async.bulk gathers of X^T rows into a shared-memory ring,
+// float64 accumulation in the consumer warps (spmm_tma.cu). F32 only.
+int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* col,
+                    const float* wn, const float* wo, const float* Xt, float* Yout,
+                    __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
+                    double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
+                    cudaStream_t st);
+
 // Columns [v0, v1) only, Xt row 0 = column v0 (one ring step of the sharded mode).
+// itm_ptr != NULL: one block per work item (row chunk of <= L candidates).
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
-                  cudaStream_t st, int64_t v0 = 0, int64_t v1 = INT64_MAX);
+                  cudaStream_t st, int64_t v0 = 0, int64_t v1 = INT64_MAX,
+                  const int64_t* itm_ptr = nullptr, int64_t n_items = 0, int64_t L = 0,
+                  const int32_t* item_row = nullptr);
 
 // c_w[e] = omega_{i, c_col[e]} (0 if absent) on the structure (c_ptr, c_col).
 int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,

@@ -120,6 +120,18 @@ struct accord_ctx {
   void *h_send = nullptr, *h_recv = nullptr;   // pinned staging (ACCORD_COMM_HOST)
   int64_t ring_steps = 0;                  // slab exchanges so far (diagnostic)
 
+  // work items (row chunks) of the current CSR for the TMA SpMM and the refine
+  bool tma_spmm = false;
+  int32_t *itm_n = nullptr, *itm_s = nullptr, *row_done = nullptr;
+  int64_t *itm_ptr = nullptr, *slot_ptr = nullptr;
+  double *part_y = nullptr, *part_d = nullptr;
+  int64_t part_slots = 0, n_items = 0, n_slots = 0;
+  double *itm_dd = nullptr, *itm_l1 = nullptr, *itm_logd = nullptr;   // per-item prox sums
+  int32_t* itm_nnz = nullptr;
+  int64_t itm_cap = 0;
+  int32_t* item_row = nullptr;             // [itm_cap] item -> row
+  const int64_t* items_of = nullptr;       // the CSR row_ptr the map was built for
+
   void* Xt = nullptr;
   __nv_bfloat16 *Xhi = nullptr, *Xlo = nullptr;
   void* Y[2] = {nullptr, nullptr};
@@ -314,10 +326,60 @@ void ring_pass(accord_ctx* c, bool want_bf16, F&& fn) {
   }
 }
 
+// Work items of the CSR `ptr` (this rank's rows): one per row, hub rows split
+// into chunks of kItemEntries; scratch for the split rows grown on demand.
+// One small D2H (item and slot totals).
+void build_items(accord_ctx* c, const int64_t* ptr) {
+  c->launches += launch_item_map(c->pk, ptr, kItemEntries, c->itm_n, c->itm_s, c->itm_ptr,
+                                 c->slot_ptr, c->scan_tmp, c->scan_tmp_sz, c->st);
+  int64_t h[2] = {0, 0};
+  CK(cudaMemcpyAsync(&h[0], c->itm_ptr + c->pk, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&h[1], c->slot_ptr + c->pk, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->n_items = h[0];
+  c->n_slots = h[1];
+  if (c->tma_spmm && c->n_slots > c->part_slots) {
+    const size_t b = (size_t)c->part_slots * c->ldk * 8;
+    c->dfree(c->part_y, b);
+    c->dfree(c->part_d, b);
+    c->part_slots = c->n_slots + c->n_slots / 4 + 16;
+    c->part_y = c->dalloc<double>((size_t)c->part_slots * c->ldk);
+    c->part_d = c->dalloc<double>((size_t)c->part_slots * c->ldk);
+  }
+  if (c->n_items > c->itm_cap) {
+    c->dfree(c->itm_dd, c->itm_cap * 8);
+    c->dfree(c->itm_l1, c->itm_cap * 8);
+    c->dfree(c->itm_logd, c->itm_cap * 8);
+    c->dfree(c->itm_nnz, c->itm_cap * 4);
+    c->dfree(c->item_row, c->itm_cap * 4);
+    c->itm_cap = c->n_items + c->n_items / 8 + 1024;
+    c->itm_dd = c->dalloc<double>(c->itm_cap);
+    c->itm_l1 = c->dalloc<double>(c->itm_cap);
+    c->itm_logd = c->dalloc<double>(c->itm_cap);
+    c->itm_nnz = c->dalloc<int32_t>(c->itm_cap);
+    c->item_row = c->dalloc<int32_t>(c->itm_cap);
+  }
+  c->launches += launch_item_rows(c->pk, c->itm_ptr, c->item_row, c->st);
+  c->items_of = ptr;
+}
+
+SpmmItems items_view(accord_ctx* c) {
+  return SpmmItems{c->itm_ptr, c->item_row, c->slot_ptr, c->part_y, c->part_d, c->row_done,
+                   kItemEntries};
+}
+
 // SpMM Y+ = W X^T (and D = (W - Wold) X^T) over all of X: one launch, or a
 // ring pass accumulating in float64 when X is sharded.
 void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void* wn,
               const void* wo, int yb, double* row_D2, double* row_Y2) {
+  if (!c->sharded && c->tma_spmm) {
+    if (c->items_of != ptr) build_items(c, ptr);
+    c->launches += launch_spmm_tma(c->pk, c->ldk, ptr, col, (const float*)wn, (const float*)wo,
+                                   (const float*)c->Xt, (float*)c->Y[yb], c->Yhi[yb], c->Ylo[yb],
+                                   c->row_A[yb], c->row_B[yb], row_D2, row_Y2, items_view(c),
+                                   c->sm_count, c->st);
+    return;
+  }
   if (!c->sharded) {
     c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, ptr, col, wn, wo, c->Xt, c->Y[yb],
                                c->Yhi[yb], c->Ylo[yb], c->row_A[yb], c->row_B[yb], row_D2,
@@ -335,8 +397,11 @@ void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void*
 // Exact candidate values c_g = (1/n) <Y_i, X_k> over all of X.
 void refine_all(accord_ctx* c) {
   if (!c->sharded) {
+    // hub rows (up to ~1.6e5 candidates) split over several blocks
+    if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
     c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
-                                 c->Y[c->cur], c->Xt, c->c_g, c->st);
+                                 c->Y[c->cur], c->Xt, c->c_g, c->st, 0, INT64_MAX, c->itm_ptr,
+                                 c->n_items, kItemEntries, c->item_row);
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
@@ -415,6 +480,7 @@ void refresh_objective(accord_ctx* c) {
 
 // Y = Omega X^T for the current Omega into Y[cur] (+ row norms).
 void recompute_y(accord_ctx* c) {
+  c->items_of = nullptr;   // Omega's structure may have been replaced (warm start, path)
   spmm_all(c, c->om_ptr, c->om_col, c->om_val, nullptr, c->cur, nullptr, c->row_Y2);
 }
 
@@ -711,6 +777,14 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
   c->scan_tmp = c->dalloc_bytes(c->scan_tmp_sz);
+  c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk) &&
+                std::getenv("ACCORD_SPMM_PLAIN") == nullptr;   // env: A-B diagnostic
+  c->itm_n = c->dalloc<int32_t>(c->pk);
+  c->itm_s = c->dalloc<int32_t>(c->pk);
+  c->itm_ptr = c->dalloc<int64_t>(c->pk + 1);
+  c->slot_ptr = c->dalloc<int64_t>(c->pk + 1);
+  c->row_done = c->dalloc<int32_t>(c->pk);
+  CK(cudaMemsetAsync(c->row_done, 0, c->pk * 4, c->st));
   int64_t cap = prm->cand_capacity;
   if (cap <= 0) {
     // The first iteration (G = S) has the most candidates (config 5: ~365 per
@@ -793,6 +867,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     CK(cudaEventRecord(c->ev[1], S));
     CK(cudaEventRecord(c->ev[2], S));
     CK(cudaMemcpyAsync(c->c_ptr, c->refit_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, S));
+    c->items_of = nullptr;
     CK(cudaMemcpyAsync(c->c_col, c->refit_col, c->refit_nnz * 4, cudaMemcpyDeviceToDevice, S));
     c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
                                  c->om_val, c->c_w, S);
@@ -890,6 +965,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) pv.g = nullptr;   // values come from the refine
   c->launches += launch_finalize(c->dtype, c->pk, pv, c->c_ptr, c->rcur, c->keys,
                                  c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S);
+  c->items_of = nullptr;   // C changed
   CK(cudaEventRecord(c->ev[3], S));
   TR(c, "finalize");
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) {
@@ -917,9 +993,11 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   for (;;) {
     st.trials++;
     CK(cudaEventRecord(c->ev[4], S));
+    const ProxItems pitems{c->itm_ptr, c->item_row, c->n_items, kItemEntries, c->itm_dd,
+                           c->itm_l1, c->itm_logd, c->itm_nnz};
     c->launches += launch_prox(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, c->c_w,
                                c->c_wn, tau, lam, c->row_dd, c->row_l1, c->row_logd,
-                               c->row_nnz, S);
+                               c->row_nnz, S, c->items_of == c->c_ptr ? &pitems : nullptr);
     CK(cudaEventRecord(c->ev[5], S));
     TR(c, "prox");
     spmm_all(c, c->c_ptr, c->c_col, c->c_wn, c->c_w, nb, c->row_D2, c->row_Y2);
@@ -959,6 +1037,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   c->launches += launch_scan_i32(c->row_nnz, c->om_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
   c->launches += launch_compact(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_wn, c->om_ptr,
                                 c->om_col, c->om_val, S);
+  if (c->items_of == c->om_ptr) c->items_of = nullptr;   // Omega changed
   TR(c, "compact");
   c->cur = nb;
   int64_t nnz_loc = 0;

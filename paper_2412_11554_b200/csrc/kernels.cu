@@ -350,11 +350,20 @@ __global__ void prox_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ 
                             const T* __restrict__ c_w, T* __restrict__ c_wn, double tau,
                             double lam, double* __restrict__ row_dd,
                             double* __restrict__ row_l1, double* __restrict__ row_logd,
-                            int32_t* __restrict__ row_nnz) {
+                            int32_t* __restrict__ row_nnz, ProxItems pi) {
   const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= pk) return;
-  const int64_t beg = c_ptr[r], end = c_ptr[r + 1];
+  const int64_t w_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t r = w_id, beg, end;
+  if (pi.itm_ptr) {   // warp per work item (hub rows split); sums per item
+    if (w_id >= pi.n_items) return;
+    r = pi.item_row[w_id];
+    beg = c_ptr[r] + (w_id - pi.itm_ptr[r]) * pi.L;
+    end = min(c_ptr[r + 1], beg + pi.L);
+  } else {
+    if (r >= pk) return;
+    beg = c_ptr[r];
+    end = c_ptr[r + 1];
+  }
   const int64_t gi = r0 + r;
   const double tl = tau * lam;
   double dd = 0.0, l1 = 0.0, logd = 0.0;
@@ -382,6 +391,34 @@ __global__ void prox_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ 
   logd = warp_sum(logd);
   nnz = warp_sum(nnz);
   if (lane == 0) {
+    if (pi.itm_ptr) {   // per item; prox_combine_kernel sums them per row
+      pi.dd[w_id] = dd;
+      pi.l1[w_id] = l1;
+      pi.logd[w_id] = logd;
+      pi.nnz[w_id] = nnz;
+    } else {
+      row_dd[r] = dd;
+      row_l1[r] = l1;
+      row_logd[r] = logd;
+      row_nnz[r] = nnz;
+    }
+  }
+}
+
+// per-row sums from the per-item partials (fixed item order)
+__global__ void prox_combine_kernel(int64_t pk, ProxItems pi, double* __restrict__ row_dd,
+                                    double* __restrict__ row_l1, double* __restrict__ row_logd,
+                                    int32_t* __restrict__ row_nnz) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < pk;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double dd = 0.0, l1 = 0.0, logd = 0.0;
+    int nnz = 0;
+    for (int64_t it = pi.itm_ptr[r]; it < pi.itm_ptr[r + 1]; ++it) {
+      dd += pi.dd[it];
+      l1 += pi.l1[it];
+      logd += pi.logd[it];
+      nnz += pi.nnz[it];
+    }
     row_dd[r] = dd;
     row_l1[r] = l1;
     row_logd[r] = logd;
@@ -576,13 +613,23 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
                                                      const T* __restrict__ Y,
                                                      const T* __restrict__ Xt,
                                                      T* __restrict__ c_g, int64_t v0,
-                                                     int64_t v1) {
+                                                     int64_t v1, const int64_t* __restrict__ itm_ptr,
+                                                     int64_t L, const int32_t* __restrict__ item_row) {
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   extern __shared__ __align__(16) uint8_t ys_raw[];
   T* ys = reinterpret_cast<T*>(ys_raw);
-  const int64_t r = blockIdx.x;
-  int64_t beg = c_ptr[r], end = c_ptr[r + 1];
+  int64_t r = blockIdx.x;
+  int64_t beg, end;
+  if (itm_ptr) {   // work item = chunk of <= L candidates of one row (hub rows split)
+    const int64_t it = blockIdx.x;
+    r = item_row[it];
+    beg = c_ptr[r] + (it - itm_ptr[r]) * L;
+    end = min(c_ptr[r + 1], beg + L);
+  } else {
+    beg = c_ptr[r];
+    end = c_ptr[r + 1];
+  }
   // columns [v0, v1) only (Xt row 0 = column v0): one ring step of the
   // sharded mode (NEXT(3)); v0 = 0, v1 = p otherwise
   beg = lower_bound_col(c_col, beg, end, v0);
@@ -982,18 +1029,24 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
 int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
                 const void* c_g, const void* c_w, void* c_wn, double tau, double lam,
                 double* row_dd, double* row_l1, double* row_logd, int32_t* row_nnz,
-                cudaStream_t st) {
+                cudaStream_t st, const ProxItems* items) {
+  const ProxItems pi = items ? *items
+                            : ProxItems{nullptr, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr};
   const int warps = 8;
-  const unsigned g = (unsigned)((pk + warps - 1) / warps);
+  const int64_t nw = pi.itm_ptr ? pi.n_items : pk;
+  const unsigned g = (unsigned)std::max<int64_t>(1, (nw + warps - 1) / warps);
   if (dtype == ACCORD_F64)
     prox_kernel<double><<<g, warps * 32, 0, st>>>(pk, r0, c_ptr, c_col, (const double*)c_g,
                                                   (const double*)c_w, (double*)c_wn, tau, lam,
-                                                  row_dd, row_l1, row_logd, row_nnz);
+                                                  row_dd, row_l1, row_logd, row_nnz, pi);
   else
     prox_kernel<float><<<g, warps * 32, 0, st>>>(pk, r0, c_ptr, c_col, (const float*)c_g,
                                                  (const float*)c_w, (float*)c_wn, tau, lam,
-                                                 row_dd, row_l1, row_logd, row_nnz);
-  return 1;
+                                                 row_dd, row_l1, row_logd, row_nnz, pi);
+  if (!pi.itm_ptr) return 1;
+  prox_combine_kernel<<<grid_for(pk, 256), 256, 0, st>>>(pk, pi, row_dd, row_l1, row_logd,
+                                                         row_nnz);
+  return 2;
 }
 
 int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* ptr,
@@ -1022,7 +1075,9 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
-                  cudaStream_t st, int64_t v0, int64_t v1) {
+                  cudaStream_t st, int64_t v0, int64_t v1, const int64_t* itm_ptr,
+                  int64_t n_items, int64_t L, const int32_t* item_row) {
+  const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
   const size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
   static bool attr = false;
@@ -1034,13 +1089,13 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
     attr = true;
   }
   if (dtype == ACCORD_F64)
-    refine_kernel<double><<<(unsigned)pk, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
-                                                           (const double*)Y, (const double*)Xt,
-                                                           (double*)c_g, v0, v1);
+    refine_kernel<double><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                   (const double*)Y, (const double*)Xt,
+                                                   (double*)c_g, v0, v1, itm_ptr, L, item_row);
   else
-    refine_kernel<float><<<(unsigned)pk, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
-                                                          (const float*)Y, (const float*)Xt,
-                                                          (float*)c_g, v0, v1);
+    refine_kernel<float><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                  (const float*)Y, (const float*)Xt,
+                                                  (float*)c_g, v0, v1, itm_ptr, L, item_row);
   return 1;
 }
 

@@ -1,0 +1,382 @@
+// a6 SpMM, TMA-staged: Y+_i = sum_j w+_ij X^T_j and
+// D_i = sum_j Delta_ij X^T_j (PAPER.md:357 two-step gradient, :258 Delta),
+// with the fused row norms ||D_i||^2, ||Y+_i||^2 and the bf16 GEMM operand
+// copy of Y+ (DESIGN.md §5).
+//
+// The op is a gather of whole X^T rows (n floats each, at c5 mostly from
+// DRAM: the off-block candidates hit random columns), so it is bound by
+// memory-level parallelism, not arithmetic. One producer warp per block walks
+// the block's work items (row chunks of <= kItemEntries entries of C, the
+// CSR of the trial), drops entries with w+ = Delta = 0, and streams each
+// needed X^T row into a ring of shared-memory stages with cp.async.bulk
+// (one 4 KB bulk copy per entry at n = 1000, completion on an mbarrier).
+// Consumer warps (8 columns per thread) accumulate in float64 from shared
+// memory. The register file no longer limits the bytes in flight: ~16 stages
+// x 3 blocks per SM = 192 KB per SM.
+//
+// Rows longer than one item (hub rows, up to 1.6e5 candidates at c5) are
+// split over several items processed by different blocks: each writes its
+// partial sums to a scratch slot, and the block that completes the row (an
+// atomic counter per row) adds the slots in chunk order, so the result does
+// not depend on which block finishes last (deterministic).
+#include "accord_internal.h"
+#include "tc_ptx.cuh"
+
+namespace accord {
+namespace {
+
+constexpr int kFlagData = 1, kFlagLast = 2, kFlagEnd = 4;
+
+struct StageMeta {
+  double w, d;
+  int64_t row;
+  int32_t chunk, nch;
+  int32_t flags, pad;
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ double wsum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(32 + kSpmmTmaMaxConsumers)
+spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__ ptr,
+                const int32_t* __restrict__ col, const float* __restrict__ wn,
+                const float* __restrict__ wo, const float* __restrict__ Xt, float* __restrict__ Yout,
+                __nv_bfloat16* __restrict__ Yhi, __nv_bfloat16* __restrict__ Ylo,
+                float* __restrict__ row_A, float* __restrict__ row_B, double* __restrict__ row_D2,
+                double* __restrict__ row_Y2, SpmmItems items) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t stage_bytes = (uint32_t)(ldk * 4);
+  float* data = reinterpret_cast<float*>(sm);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(sm + (size_t)stages * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + stages);
+  uint64_t* empty = full + stages;
+  double* red = reinterpret_cast<double*>(empty + stages);   // [4][16] + flag
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncw = (blockDim.x >> 5) - 1;                     // consumer warps
+  const int nct = ncw * 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      tc::mbar_init(tc::smem_u32(&full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&empty[s]), ncw);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t n_items = items.itm_ptr[pk];
+
+  if (warp == 0) {
+    // ============================== producer ==============================
+    int stage = 0;
+    uint32_t phase = 0;
+    auto emit = [&](double w, double d, int32_t c, int flags, int64_t row, int chunk, int nch) {
+      tc::mbar_wait(tc::smem_u32(&empty[stage]), phase ^ 1);
+      if (lane == 0) {
+        StageMeta& m = meta[stage];
+        m.w = w;
+        m.d = d;
+        m.row = row;
+        m.chunk = chunk;
+        m.nch = nch;
+        m.flags = flags;
+        const uint32_t fb = tc::smem_u32(&full[stage]);
+        if (flags & kFlagData) {
+          tc::mbar_arrive_expect_tx(fb, stage_bytes);
+          bulk_g2s(tc::smem_u32(data + (size_t)stage * ldk), Xt + (int64_t)c * ldk, stage_bytes,
+                   fb);
+        } else {
+          tc::mbar_arrive(fb);
+        }
+      }
+      __syncwarp();
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+    };
+    // Items it = blockIdx.x + k * gridDim.x. Their metadata is fetched 32 at a
+    // time (lane j holds item j of the batch: row from the item->row map, entry
+    // range, chunk), and the first 32 entries of the next item are loaded while
+    // the current one is being emitted, so the producer's global-memory
+    // latencies overlap the copies in flight.
+    const int64_t G = gridDim.x;
+    for (int64_t base = blockIdx.x; base < n_items; base += 32 * G) {
+      const int64_t itj = base + (int64_t)lane * G;
+      const bool vj = itj < n_items;
+      const int64_t rj = vj ? (int64_t)items.item_row[itj] : 0;
+      const int64_t i0 = items.itm_ptr[rj], i1 = items.itm_ptr[rj + 1];
+      const int64_t p0 = ptr[rj], p1 = ptr[rj + 1];
+      const int chj = (int)(itj - i0), nchj = (int)(i1 - i0);
+      const int64_t begj = p0 + (int64_t)chj * items.L;
+      const int64_t endj = min(p1, begj + items.L);
+      const int nv = __popc(__ballot_sync(0xffffffffu, vj));
+      // entries of the first item
+      auto load = [&](int64_t e, int64_t end, double& w, double& d, int32_t& cc) {
+        if (e < end) {
+          w = (double)__ldg(wn + e);
+          d = wo ? w - (double)__ldg(wo + e) : 0.0;
+          cc = __ldg(col + e);
+        } else {
+          w = 0.0; d = 0.0; cc = 0;
+        }
+      };
+      double nw_ = 0.0, nd_ = 0.0;
+      int32_t nc_ = 0;
+      {
+        const int64_t b0 = __shfl_sync(0xffffffffu, begj, 0), e0_ = __shfl_sync(0xffffffffu, endj, 0);
+        load(b0 + lane, e0_, nw_, nd_, nc_);
+      }
+      for (int k = 0; k < nv; ++k) {
+        const int64_t r = __shfl_sync(0xffffffffu, rj, k);
+        const int chunk = __shfl_sync(0xffffffffu, chj, k);
+        const int nch = __shfl_sync(0xffffffffu, nchj, k);
+        const int64_t beg = __shfl_sync(0xffffffffu, begj, k);
+        const int64_t end = __shfl_sync(0xffffffffu, endj, k);
+        double w = nw_, d = nd_;
+        int32_t cc = nc_;
+        if (k + 1 < nv) {   // lookahead: first batch of the next item
+          const int64_t bn = __shfl_sync(0xffffffffu, begj, k + 1);
+          const int64_t en = __shfl_sync(0xffffffffu, endj, k + 1);
+          load(bn + lane, en, nw_, nd_, nc_);
+        }
+        // one entry of lookahead so that the item's last nonzero carries kFlagLast
+        bool pend = false;
+        double pw = 0.0, pd = 0.0;
+        int32_t pc = 0;
+        for (int64_t e0 = beg; e0 < end; e0 += 32) {
+          if (e0 != beg) load(e0 + lane, end, w, d, cc);
+          const bool keep = (e0 + lane < end) && ((w != 0.0) || (d != 0.0));
+          unsigned m = __ballot_sync(0xffffffffu, keep);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const double ws = __shfl_sync(0xffffffffu, w, src);
+            const double ds = __shfl_sync(0xffffffffu, d, src);
+            const int32_t cs = __shfl_sync(0xffffffffu, cc, src);
+            if (pend) emit(pw, pd, pc, kFlagData, r, chunk, nch);
+            pend = true;
+            pw = ws;
+            pd = ds;
+            pc = cs;
+          }
+        }
+        if (pend) emit(pw, pd, pc, kFlagData | kFlagLast, r, chunk, nch);
+        else emit(0.0, 0.0, 0, kFlagLast, r, chunk, nch);
+      }
+    }
+    emit(0.0, 0.0, 0, kFlagEnd, 0, 0, 0);
+    return;
+  }
+
+  // ================================ consumers ===============================
+  const int t = threadIdx.x - 32;
+  const int64_t c0 = (int64_t)t * 8;
+  const bool active = c0 < ldk;
+  double ay[8], ad[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+  int stage = 0;
+  uint32_t phase = 0;
+  double* sh_red = red;                                   // [16] per-warp partials x 4
+  volatile int* sh_flag = reinterpret_cast<volatile int*>(red + 64);
+  for (;;) {
+    tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
+    const StageMeta m = meta[stage];
+    if (m.flags & kFlagEnd) break;
+    if ((m.flags & kFlagData) && active) {
+      const float* xs = data + (size_t)stage * ldk + c0;
+      const float4 x0 = *reinterpret_cast<const float4*>(xs);
+      const float4 x1 = *reinterpret_cast<const float4*>(xs + 4);
+      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        ay[v] = fma(m.w, (double)xv[v], ay[v]);
+        ad[v] = fma(m.d, (double)xv[v], ad[v]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[stage]));
+    if (++stage == stages) { stage = 0; phase ^= 1; }
+    if (!(m.flags & kFlagLast)) continue;
+
+    // ---------------- item complete: finalize the row (or its partial) ----
+    const int64_t r = m.row;
+    bool finish = true;
+    if (m.nch > 1) {
+      const int64_t slot0 = items.slot_ptr[r];
+      if (active) {
+        double* py = items.part_y + (slot0 + m.chunk) * ldk + c0;
+        double* pd = items.part_d + (slot0 + m.chunk) * ldk + c0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
+      }
+      __threadfence();
+      named_sync(1, nct);
+      if (t == 0) *sh_flag = (atomicAdd(&items.row_done[r], 1) == m.nch - 1) ? 1 : 0;
+      named_sync(1, nct);
+      finish = *sh_flag != 0;
+      if (finish) {
+        __threadfence();
+        if (active) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+          for (int k = 0; k < m.nch; ++k) {   // chunk order: deterministic sum
+            const double* py = items.part_y + (slot0 + k) * ldk + c0;
+            const double* pd = items.part_d + (slot0 + k) * ldk + c0;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              ay[v] += __ldcg(py + v);
+              ad[v] += __ldcg(pd + v);
+            }
+          }
+        }
+        if (t == 0) items.row_done[r] = 0;   // ready for the next trial
+      }
+    }
+    if (finish) {
+      double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0;
+      if (active) {
+        float yt[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          d2 += ad[v] * ad[v];
+          y2 += ay[v] * ay[v];
+          yt[v] = (float)ay[v];
+        }
+        float* yo = Yout + r * ldk + c0;
+        *reinterpret_cast<float4*>(yo) = make_float4(yt[0], yt[1], yt[2], yt[3]);
+        *reinterpret_cast<float4*>(yo + 4) = make_float4(yt[4], yt[5], yt[6], yt[7]);
+        if (Yhi) {
+          __nv_bfloat16 h[8], l[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            h[v] = __float2bfloat16_rn(yt[v]);
+            const float hf = __bfloat162float(h[v]);
+            l[v] = __float2bfloat16_rn(yt[v] - hf);
+            const double e = (double)yt[v] - (double)hf;
+            a2 += e * e;
+            b2 += (double)yt[v] * (double)yt[v];
+          }
+          *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = *reinterpret_cast<const uint4*>(h);
+          if (Ylo) *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = *reinterpret_cast<const uint4*>(l);
+        }
+      }
+      d2 = wsum(d2);
+      y2 = wsum(y2);
+      a2 = wsum(a2);
+      b2 = wsum(b2);
+      const int cw = warp - 1;
+      if (lane == 0) {
+        sh_red[cw] = d2;
+        sh_red[16 + cw] = y2;
+        sh_red[32 + cw] = a2;
+        sh_red[48 + cw] = b2;
+      }
+      named_sync(1, nct);
+      if (t == 0) {
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        for (int q = 0; q < ncw; ++q) {   // fixed order
+          s0 += sh_red[q];
+          s1 += sh_red[16 + q];
+          s2 += sh_red[32 + q];
+          s3 += sh_red[48 + q];
+        }
+        if (row_D2) row_D2[r] = s0;
+        if (row_Y2) row_Y2[r] = s1;
+        if (Yhi) {
+          // rounded up: these enter an upper bound (the GEMM filter)
+          if (row_A) row_A[r] = __double2float_ru(sqrt(s2) * (1.0 + 1e-12));
+          if (row_B) row_B[r] = __double2float_ru(sqrt(s3) * (1.0 + 1e-12));
+        }
+      }
+      named_sync(1, nct);
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+  }
+}
+
+// per row: work items (chunks of <= L entries, >= 1) and scratch slots
+// (multi-chunk rows only)
+__global__ void item_count_kernel(int64_t rows, const int64_t* __restrict__ ptr, int64_t L,
+                                  int32_t* __restrict__ nitem, int32_t* __restrict__ nslot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = ptr[i + 1] - ptr[i];
+    const int64_t c = len <= L ? 1 : (len + L - 1) / L;
+    nitem[i] = (int32_t)c;
+    nslot[i] = c > 1 ? (int32_t)c : 0;
+  }
+}
+
+// item -> row (thread per row writes its items)
+__global__ void item_row_kernel(int64_t rows, const int64_t* __restrict__ itm_ptr,
+                                int32_t* __restrict__ item_row) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t it = itm_ptr[i]; it < itm_ptr[i + 1]; ++it) item_row[it] = (int32_t)i;
+}
+
+}  // namespace
+
+int launch_item_rows(int64_t rows, const int64_t* itm_ptr, int32_t* item_row, cudaStream_t st) {
+  const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (rows + 255) / 256));
+  item_row_kernel<<<g, 256, 0, st>>>(rows, itm_ptr, item_row);
+  return 1;
+}
+
+size_t spmm_tma_smem(int64_t ldk, int* stages) {
+  const int64_t sb = ldk * 4;
+  int s = (int)std::min<int64_t>(16, std::max<int64_t>(4, (64 * 1024) / sb));
+  *stages = s;
+  return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 65 * 8 + 64;
+}
+
+bool spmm_tma_supported(int dtype, int64_t ldk) {
+  return dtype == ACCORD_F32 && ldk % 8 == 0 && ldk / 8 <= kSpmmTmaMaxConsumers;
+}
+
+int launch_item_map(int64_t rows, const int64_t* ptr, int64_t L, int32_t* nitem, int32_t* nslot,
+                    int64_t* itm_ptr, int64_t* slot_ptr, void* scan_tmp, size_t scan_tmp_bytes,
+                    cudaStream_t st) {
+  const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (rows + 255) / 256));
+  item_count_kernel<<<g, 256, 0, st>>>(rows, ptr, L, nitem, nslot);
+  int l = 1;
+  l += launch_scan_i32(nitem, itm_ptr, rows, scan_tmp, scan_tmp_bytes, st);
+  l += launch_scan_i32(nslot, slot_ptr, rows, scan_tmp, scan_tmp_bytes, st);
+  return l;
+}
+
+int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* col,
+                    const float* wn, const float* wo, const float* Xt, float* Yout,
+                    __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
+                    double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
+                    cudaStream_t st) {
+  if (pk == 0) return 0;
+  int stages = 0;
+  const size_t smem = spmm_tma_smem(ldk, &stages);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(spmm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         100 * 1024);
+    attr = true;
+  }
+  const int consumers = (int)round_up(ldk / 8, 32);
+  const int per_sm = std::max(1, (int)((200 * 1024) / (smem + 1024)));
+  spmm_tma_kernel<<<sm_count * std::min(per_sm, 4), 32 + consumers, smem, st>>>(
+      pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2, items);
+  return 1;
+}
+
+}  // namespace accord
