@@ -154,7 +154,7 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 // the fixed-support gradient of the refit.
 // Work items over a CSR (row chunks of <= L entries; rows longer than L
 // become several items) for the TMA-staged SpMM and the refine.
-constexpr int kSpmmTmaMaxConsumers = 512;
+constexpr int kSpmmTmaMaxConsumers = 256;   // ldk <= 2048
 constexpr int64_t kItemEntries = 2048;
 struct SpmmItems {
   const int64_t* itm_ptr;     // [rows + 1] exclusive scan of items per row

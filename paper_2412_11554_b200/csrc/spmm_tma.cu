@@ -52,7 +52,7 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(32 + kSpmmTmaMaxConsumers)
+__global__ void __launch_bounds__(32 + kSpmmTmaMaxConsumers, 2)
 spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__ ptr,
                 const int32_t* __restrict__ col, const float* __restrict__ wn,
                 const float* __restrict__ wo, const float* __restrict__ Xt, float* __restrict__ Yout,
@@ -190,25 +190,63 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
   uint32_t phase = 0;
   double* sh_red = red;                                   // [16] per-warp partials x 4
   volatile int* sh_flag = reinterpret_cast<volatile int*>(red + 64);
-  for (;;) {
-    tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
-    const StageMeta m = meta[stage];
-    if (m.flags & kFlagEnd) break;
-    if ((m.flags & kFlagData) && active) {
-      const float* xs = data + (size_t)stage * ldk + c0;
-      const float4 x0 = *reinterpret_cast<const float4*>(xs);
-      const float4 x1 = *reinterpret_cast<const float4*>(xs + 4);
-      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  auto accumulate = [&](double w, double d, float4 x0, float4 x1) {
+    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        ay[v] = fma(m.w, (double)xv[v], ay[v]);
-        ad[v] = fma(m.d, (double)xv[v], ad[v]);
+    for (int v = 0; v < 8; ++v) {
+      ay[v] = fma(w, (double)xv[v], ay[v]);
+      ad[v] = fma(d, (double)xv[v], ad[v]);
+    }
+  };
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (;;) {
+    // two stages per round when the item continues: both waits and both
+    // shared-memory loads are issued before the arithmetic (halves the
+    // dependent latency chain per staged row)
+    tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
+    const int f0 = meta[stage].flags;
+    if (f0 & kFlagEnd) break;
+    const double w0 = meta[stage].w, d0 = meta[stage].d;
+    float4 a0 = z4, b0 = z4;
+    if ((f0 & kFlagData) && active) {
+      const float* xs = data + (size_t)stage * ldk + c0;
+      a0 = *reinterpret_cast<const float4*>(xs);
+      b0 = *reinterpret_cast<const float4*>(xs + 4);
+    }
+    const int s1 = stage + 1 == stages ? 0 : stage + 1;
+    const uint32_t ph1 = stage + 1 == stages ? phase ^ 1 : phase;
+    const bool two = !(f0 & kFlagLast);   // the item goes on: stage s1 belongs to it
+    int f1 = 0;
+    double w1 = 0.0, d1 = 0.0;
+    float4 a1 = z4, b1 = z4;
+    if (two) {
+      tc::mbar_wait(tc::smem_u32(&full[s1]), ph1);
+      f1 = meta[s1].flags;
+      w1 = meta[s1].w;
+      d1 = meta[s1].d;
+      if ((f1 & kFlagData) && active) {
+        const float* xs = data + (size_t)s1 * ldk + c0;
+        a1 = *reinterpret_cast<const float4*>(xs);
+        b1 = *reinterpret_cast<const float4*>(xs + 4);
       }
     }
+    const bool last = (f0 & kFlagLast) || (f1 & kFlagLast);
+    const int ls = (f0 & kFlagLast) ? stage : s1;
+    StageMeta m;
+    if (last) m = meta[ls];   // row / chunk of the finished item (before the release)
+    accumulate(w0, d0, a0, b0);
+    if (two) accumulate(w1, d1, a1, b1);
     __syncwarp();
-    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[stage]));
-    if (++stage == stages) { stage = 0; phase ^= 1; }
-    if (!(m.flags & kFlagLast)) continue;
+    if (lane == 0) {
+      tc::mbar_arrive(tc::smem_u32(&empty[stage]));
+      if (two) tc::mbar_arrive(tc::smem_u32(&empty[s1]));
+    }
+    stage = s1;
+    phase = ph1;
+    if (two) {
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+    }
+    if (!last) continue;
 
     // ---------------- item complete: finalize the row (or its partial) ----
     const int64_t r = m.row;
@@ -258,18 +296,21 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         *reinterpret_cast<float4*>(yo) = make_float4(yt[0], yt[1], yt[2], yt[3]);
         *reinterpret_cast<float4*>(yo + 4) = make_float4(yt[4], yt[5], yt[6], yt[7]);
         if (Yhi) {
-          __nv_bfloat16 h[8], l[8];
+          uint32_t hp[4], lp[4];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            h[v] = __float2bfloat16_rn(yt[v]);
-            const float hf = __bfloat162float(h[v]);
-            l[v] = __float2bfloat16_rn(yt[v] - hf);
-            const double e = (double)yt[v] - (double)hf;
-            a2 += e * e;
-            b2 += (double)yt[v] * (double)yt[v];
+          for (int v = 0; v < 8; v += 2) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(yt[v], yt[v + 1]);
+            const float2 hf = __bfloat1622float2(h2);
+            const __nv_bfloat162 l2 = __floats2bfloat162_rn(yt[v] - hf.x, yt[v + 1] - hf.y);
+            hp[v / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+            lp[v / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+            const double e0 = (double)yt[v] - (double)hf.x, e1 = (double)yt[v + 1] - (double)hf.y;
+            a2 += e0 * e0 + e1 * e1;
+            b2 += (double)yt[v] * (double)yt[v] + (double)yt[v + 1] * (double)yt[v + 1];
           }
-          *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = *reinterpret_cast<const uint4*>(h);
-          if (Ylo) *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = *reinterpret_cast<const uint4*>(l);
+          *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+          if (Ylo)
+            *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
         }
       }
       d2 = wsum(d2);
@@ -338,7 +379,7 @@ int launch_item_rows(int64_t rows, const int64_t* itm_ptr, int32_t* item_row, cu
 
 size_t spmm_tma_smem(int64_t ldk, int* stages) {
   const int64_t sb = ldk * 4;
-  int s = (int)std::min<int64_t>(16, std::max<int64_t>(4, (64 * 1024) / sb));
+  int s = (int)std::min<int64_t>(8, std::max<int64_t>(4, (32 * 1024) / sb));
   *stages = s;
   return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 65 * 8 + 64;
 }
@@ -373,8 +414,12 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
     attr = true;
   }
   const int consumers = (int)round_up(ldk / 8, 32);
-  const int per_sm = std::max(1, (int)((200 * 1024) / (smem + 1024)));
-  spmm_tma_kernel<<<sm_count * std::min(per_sm, 4), 32 + consumers, smem, st>>>(
+  // persistent: exactly the resident blocks (items are dealt round-robin)
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_tma_kernel, 32 + consumers,
+                                                    smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  spmm_tma_kernel<<<sm_count * std::min(per_sm, 8), 32 + consumers, smem, st>>>(
       pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2, items);
   return 1;
 }
