@@ -381,9 +381,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             const int64_t left = ep.col_end - c0;                     // ragged p / slab
             if (left < 32) mask &= left <= 0 ? 0u : ((1u << left) - 1u);
           }
+          // common case: no candidate in these 32 columns of the warp's 32 rows
+          // (one vote instead of a REDUX round trip)
+          if (__ballot_sync(0xffffffffu, mask != 0u) == 0u) continue;
           const int cnt = __popc(mask);
           const int total = __reduce_add_sync(0xffffffffu, cnt);
-          if (total == 0) continue;
           int incl = cnt;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {

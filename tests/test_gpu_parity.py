@@ -143,3 +143,34 @@ def test_parity_dense_candidate_rows(p, n, lam, T):
     csr, stats, info = run_gpu(pr.Xt, lam, T, inv_L, A.GEMM_AUTO)
     assert stats[-1]["max_row_cand"] > (16384 if p > 16384 else 1024)
     compare_full(pr.Xt, lam, T, inv_L, csr.to_dense(p), stats, "f32")
+
+
+@pytest.mark.parametrize("p,n,lam,T", [(4000, 60, 0.05, 3), (1100, 333, 0.1, 8)])
+def test_tma_spmm_matches_block_per_row_spmm(p, n, lam, T, monkeypatch):
+    """The TMA-staged SpMM (producer warp + cp.async.bulk ring, hub rows split
+    into work items with a deterministic last-block sum) and the block-per-row
+    SpMM compute the same Y+ and D (both float64-accumulated): identical tau
+    schedule, objective and Omega to rounding, on a case whose candidate rows
+    exceed one work item (2048 entries)."""
+    _cuda()
+    rng = np.random.default_rng(5 + p)
+    Xt = rng.standard_normal((p, n)).astype(np.float32)
+    Xt -= Xt.mean(axis=1, keepdims=True)
+    inv_L = 1.0 / O.spectral_bound(Xt.astype(np.float64))
+    out = {}
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("ACCORD_SPMM_PLAIN", "1")
+        else:
+            monkeypatch.delenv("ACCORD_SPMM_PLAIN", raising=False)
+        with A.AccordSolver(torch.from_numpy(Xt).cuda(), lam, inv_L=inv_L) as s:
+            st = s.step(T)
+            out[plain] = ([x["tau"] for x in st], [x["f"] for x in st], s.export_csr(),
+                          max(x["max_row_cand"] for x in st))
+    (t0, f0, c0, m0), (t1, f1, c1, m1) = out[False], out[True]
+    assert t0 == t1
+    np.testing.assert_allclose(f0, f1, rtol=1e-12)
+    assert np.array_equal(c0.row_ptr, c1.row_ptr) and np.array_equal(c0.col, c1.col)
+    assert np.abs(c0.val - c1.val).max() <= 1e-6 * np.abs(c1.val).max()
+    if p == 4000:
+        assert m0 > 2048   # multi-item rows were exercised
