@@ -57,6 +57,7 @@ struct EpiParams {            // candidate rule of the fused epilogue (SURVEY P1
   const float* row_B;         // ||y_i||
   const float2* col_sd;       // (||x_k|| + ||x_k - bf16(x_k)||, ||x_k - bf16(x_k)||)
   float gamma;                // accumulation-error factor
+  int exact_cols;             // 1: re-test tile-test survivors with their own column's bound
 };
 
 // ---------------------------------------------------------------------------

@@ -777,8 +777,14 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
   c->scan_tmp = c->dalloc_bytes(c->scan_tmp_sz);
-  c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk) &&
+  // TMA-staged SpMM for large row blocks; below ~6.5e4 rows the persistent
+  // producer/consumer pipeline has too few items per block to hide its
+  // per-item latency and the block-per-row kernel is faster (config 3:
+  // 0.8 vs 0.4 ms per trial; config 4: 1.8 vs 3.4 ms)
+  c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk) && c->pk >= 65536 &&
                 std::getenv("ACCORD_SPMM_PLAIN") == nullptr;   // env: A-B diagnostic
+  if (std::getenv("ACCORD_SPMM_TMA"))   // env: force (tests of the TMA path at small sizes)
+    c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk);
   c->itm_n = c->dalloc<int32_t>(c->pk);
   c->itm_s = c->dalloc<int32_t>(c->pk);
   c->itm_ptr = c->dalloc<int64_t>(c->pk + 1);
@@ -903,6 +909,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     ep.col_sd = c->col_sd;
     // fp32-accumulation term of the filter bound: (n/16 + 17) * 2^-22 * sum|y^ x^|
     ep.gamma = (float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
+    ep.exact_cols = std::getenv("ACCORD_FILTER_EXACT") != nullptr;   // A-B diagnostic
     CK(cudaEventRecord(c->ev[1], S));
     const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
     auto gemm = [&](const void* xt, int bsel, int64_t v0, int64_t v1) {

@@ -360,8 +360,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               for (int c = 0; c < 32; ++c)
                 mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
             }
-            if (kMode == 1 && mask) {
-              // exact per-column bound for the (rare) survivors of the fast test
+            if (kMode == 1 && ep.exact_cols && mask) {
+              // exact per-column bound for the survivors of the tile-level test
+              // (optional: the tile test alone is already a certified superset;
+              // where lambda is only ~2.5 sd of the null S, e.g. config 3, nearly
+              // every 32-column chunk has a survivor and these predicated loads
+              // dominated the epilogue)
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
                 if (mask & (1u << c)) {

@@ -43,8 +43,13 @@ def test_parity_f64_simt(key):
 
 @pytest.mark.parametrize("gemm", [A.GEMM_SIMT, A.GEMM_BF16X3, A.GEMM_BF16_FILTER])
 @pytest.mark.parametrize("key", ["t_ba_f32", "t_hubs_f32"])
-def test_parity_f32_small(key, gemm):
+@pytest.mark.parametrize("spmm", ["default", "tma"])
+def test_parity_f32_small(key, gemm, spmm, monkeypatch):
+    """spmm = tma forces the TMA-staged SpMM (used by default for row blocks of
+    >= 65536 rows) on these small cases too."""
     _cuda()
+    if spmm == "tma":
+        monkeypatch.setenv("ACCORD_SPMM_TMA", "1")
     pr = make_problem(key)
     c = pr.cfg
     inv_L = 1.0 / O.spectral_bound(pr.Xt)
@@ -161,8 +166,10 @@ def test_tma_spmm_matches_block_per_row_spmm(p, n, lam, T, monkeypatch):
     for plain in (False, True):
         if plain:
             monkeypatch.setenv("ACCORD_SPMM_PLAIN", "1")
+            monkeypatch.delenv("ACCORD_SPMM_TMA", raising=False)
         else:
             monkeypatch.delenv("ACCORD_SPMM_PLAIN", raising=False)
+            monkeypatch.setenv("ACCORD_SPMM_TMA", "1")   # small p: force the TMA path
         with A.AccordSolver(torch.from_numpy(Xt).cuda(), lam, inv_L=inv_L) as s:
             st = s.step(T)
             out[plain] = ([x["tau"] for x in st], [x["f"] for x in st], s.export_csr(),

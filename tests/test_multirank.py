@@ -426,3 +426,36 @@ def test_sharded_x_ring_config3_scale():
             g = o["g"]
             assert np.array_equal(g.row_ptr, W1.row_ptr) and np.array_equal(g.col, W1.col)
             assert np.abs(g.val - W1.val).max() <= 1e-6 * np.abs(W1.val).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_sharded_x_ring_config5_scale():
+    """The sharded-X ring at the p = 1e6 config: 2 contexts on one GPU, each
+    holding half of X (2 GB) and passing slabs through the host transport,
+    reproduce the replicated run's tau schedule, objective and Omega for the
+    first iterations (GEMM ring of 2 x 1954 x 1954 tiles, refine and SpMM
+    rings, sharded power iteration)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import get_config, make_problem
+    cfg = get_config("5")
+    pr = make_problem(cfg, with_blocks=False)
+    lam, T = cfg.lambdas[0], 2
+    X = torch.from_numpy(pr.Xt).cuda()
+    with A.AccordSolver(X, lam, inv_L=0.0) as s:
+        st1 = s.step(T)
+        W1 = s.export_csr()
+        f1 = s.objective()[0]
+        L1 = s.info()["L"]
+    del X
+    torch.cuda.empty_cache()
+    out, bounds = run_ranks_sharded(pr.Xt, lam, T, 0.0, 2, A.GEMM_AUTO)
+    for o in out:
+        assert abs(o["L"] - L1) <= 1e-9 * L1
+        assert [x["tau"] for x in o["st"]] == [x["tau"] for x in st1]
+        assert abs(o["f"] - f1) <= 1e-9 * abs(f1)
+        g = o["g"]
+        assert np.array_equal(g.row_ptr, W1.row_ptr) and np.array_equal(g.col, W1.col)
+        assert np.abs(g.val - W1.val).max() <= 1e-6 * np.abs(W1.val).max()

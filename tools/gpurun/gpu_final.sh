@@ -9,4 +9,4 @@ timeout 900 python bench.py --config 4 > gpurun_out/final_bench_c4.json 2> gpuru
 timeout 900 python bench.py --config 3 > gpurun_out/final_bench_c3.json 2> gpurun_out/final_bench_c3.log; echo b3=$?
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/final_ref.json 2> gpurun_out/final_ref.log; echo ref=$?
 timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final_plain.log 2>&1 && timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:^(?!.*pi_)' -c 400 --csv --log-file gpurun_out/final_launches_c5.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final_ncu_launches.log 2>&1; echo launches=$?
-timeout 600 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/final_plain2.log 2>&1 && timeout 1500 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 1 -c 1 -o gpurun_out/final_prof_gemm_c5 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/final_ncu_gemm.log 2>&1; echo ncu=$?
+timeout 600 python bench.py --steps 1 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/final_plain2.log 2>&1 && timeout 1500 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 5 -c 1 -o gpurun_out/final_prof_gemm_c5 python bench.py --steps 1 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/final_ncu_gemm.log 2>&1; echo ncu=$?
