@@ -455,7 +455,10 @@ def test_sharded_x_ring_config5_scale():
     for o in out:
         assert abs(o["L"] - L1) <= 1e-9 * L1
         assert [x["tau"] for x in o["st"]] == [x["tau"] for x in st1]
-        assert abs(o["f"] - f1) <= 1e-9 * abs(f1)
+        # the replicated run uses the TMA SpMM (hub rows summed in chunk order),
+        # the ring the block-per-row kernel (slabs in ring order): Y+ agrees to
+        # f32 rounding, the objective to ~1e-8 relative
+        assert abs(o["f"] - f1) <= 1e-7 * abs(f1)
         g = o["g"]
         assert np.array_equal(g.row_ptr, W1.row_ptr) and np.array_equal(g.col, W1.col)
         assert np.abs(g.val - W1.val).max() <= 1e-6 * np.abs(W1.val).max()
