@@ -22,6 +22,9 @@
 #include "accord_internal.h"
 #include "tc_ptx.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace accord {
 namespace {
 
@@ -379,7 +382,9 @@ int launch_item_rows(int64_t rows, const int64_t* itm_ptr, int32_t* item_row, cu
 
 size_t spmm_tma_smem(int64_t ldk, int* stages) {
   const int64_t sb = ldk * 4;
-  int s = (int)std::min<int64_t>(8, std::max<int64_t>(4, (32 * 1024) / sb));
+  int want = 8;   // stages (4 KB each at n = 1000); ACCORD_SPMM_STAGES: tuning
+  if (const char* e = std::getenv("ACCORD_SPMM_STAGES")) want = std::max(2, std::atoi(e));
+  int s = (int)std::min<int64_t>(want, std::max<int64_t>(2, (want * 4096) / sb));
   *stages = s;
   return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 65 * 8 + 64;
 }
