@@ -969,9 +969,16 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
   CK(cudaMemsetAsync(c->long_rows, 0, 4, S));
   TR(c, "memset");
   PoolView pv = pool_view(c);
-  if (c->gemm == ACCORD_GEMM_BF16_FILTER) pv.g = nullptr;   // values come from the refine
+  const bool filt = c->gemm == ACCORD_GEMM_BF16_FILTER;
+  if (filt) {          // the epilogue emits positions only
+    pv.g = nullptr;    // values come from the refine
+    pv.w = nullptr;    // omega_ik from a lookup in Omega's sorted rows
+  }
   c->launches += launch_finalize(c->dtype, c->pk, pv, c->c_ptr, c->rcur, c->keys,
                                  c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S);
+  if (filt)
+    c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
+                                 c->om_val, c->c_w, S);
   c->items_of = nullptr;   // C changed
   CK(cudaEventRecord(c->ev[3], S));
   TR(c, "finalize");

@@ -336,6 +336,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
         tc::tmem_ld32(tbase + ch2 * 64, v2[0]);
         tc::tmem_ld32(tbase + ch2 * 64 + 32, v2[1]);
         tc::tmem_ld_wait();
+        if (dbg >= 3) {   // diagnostics: 3 = TMEM reads only, 4 = reads + max test only
+          if (dbg == 4) {   // the max test of both halves (kept alive by an opaque compare)
+            float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v2[0][c])), fabsf(__uint_as_float(v2[0][c + 1]))));
+              m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v2[1][c])), fabsf(__uint_as_float(v2[1][c + 1]))));
+            }
+            if (__float_as_uint(fmaxf(m0, m1)) == 0x7f7ffff1u) pool.row[0] = 0;
+          } else if (v2[0][0] == 0xffffffffu && v2[1][31] == 0xffffffffu) {
+            pool.row[0] = 0;                  // keep the loads alive (never true)
+          }
+          continue;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t* v = v2[h];
@@ -409,17 +423,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           fill += total;
           row_count += cnt;
           if constexpr (kMode == 1) {
-            // candidate positions only; the exact values come from the refine SDDMM
+            // candidate positions only: the exact values come from the refine
+            // SDDMM and omega_ik from a lookup in Omega's CSR after the sort
+            // (no dependent load of Omega's values on the epilogue's path)
             uint32_t m = mask;
             while (m) {
               const int c = __ffs(m) - 1;
               m &= m - 1;
-              float w = 0.f;
-              if (sup & (1u << c)) w = omv[sp0 + __popc(sup & ((1u << c) - 1u))];
               if (writable) {
                 pool.row[pos] = (int32_t)r;
                 pool.col[pos] = c0 + c;
-                ((float*)pool.w)[pos] = w;
               }
               ++pos;
             }

@@ -329,7 +329,7 @@ __global__ void gather_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
     const uint32_t idx = (uint32_t)(k & 0xffffffffu);
     c_col[e] = (int32_t)(k >> 32);
     if (pg) c_g[e] = pg[idx];   // NULL for BF16_FILTER: the refine SDDMM writes c_g
-    c_w[e] = pw[idx];
+    if (pw) c_w[e] = pw[idx];   // NULL for BF16_FILTER: looked up in Omega after the sort
   }
 }
 
