@@ -316,6 +316,8 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
         "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]], shard),
         "effective_tflops": flops_iter * value / 1e12,
+        # whole step against the same peak (2 p_k p n / Peak / t_iter)
+        "step_roofline_frac": flops_iter * value / 1e12 / peak,
         "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel<1> (bf16 filter + epilogue)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -433,8 +433,10 @@ void grow(accord_ctx* c, int64_t cap, int64_t keep_nnz) {
   c->dfree(c->keys_tmp, oc * 8); c->keys_tmp = c->dalloc<uint64_t>(cap);
   c->dfree(c->pool_row, oc * 4); c->pool_row = c->dalloc<int32_t>(cap);
   c->dfree(c->pool_col, oc * 4); c->pool_col = c->dalloc<int32_t>(cap);
-  c->dfree(c->pool_g, oc * T);  c->pool_g = c->dalloc_bytes(cap * T);
-  c->dfree(c->pool_w, oc * T);  c->pool_w = c->dalloc_bytes(cap * T);
+  // the BF16 filter's epilogue emits positions only (values: refine + lookup)
+  const bool vals = c->gemm != ACCORD_GEMM_BF16_FILTER;
+  c->dfree(c->pool_g, oc * T);  c->pool_g = vals ? c->dalloc_bytes(cap * T) : nullptr;
+  c->dfree(c->pool_w, oc * T);  c->pool_w = vals ? c->dalloc_bytes(cap * T) : nullptr;
   c->cap = cap;
   // chunking: the SIMT GEMM uses one chunk; the tcgen05 epilogue warps take
   // private chunks of 1024..8192 entries (>= one 32x32 emission batch)
