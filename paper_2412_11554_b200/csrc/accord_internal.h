@@ -133,6 +133,11 @@ int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const i
                 const void* c_g, const void* c_w, void* c_wn, double tau, double lam,
                 double* row_dd, double* row_l1, double* row_logd, int32_t* row_nnz,
                 cudaStream_t st, const ProxItems* items = nullptr);
+// c_w[e] = omega_{i, c_col[e]} (0 if absent) on the structure (c_ptr, c_col);
+// warp per row, or per work item when `items` is given.
+int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
+                  const int64_t* om_ptr, const int32_t* om_col, const void* om_val, void* c_w,
+                  cudaStream_t st, const ProxItems* items = nullptr);
 
 // SpMM Y+ = Omega+ X^T and D = Delta X^T over a CSR (ptr/col/wn/wo); wo may be
 // NULL (Delta = 0). Accumulates in double; writes Y (T), optionally its bf16
@@ -187,10 +192,7 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                   const int64_t* itm_ptr = nullptr, int64_t n_items = 0, int64_t L = 0,
                   const int32_t* item_row = nullptr);
 
-// c_w[e] = omega_{i, c_col[e]} (0 if absent) on the structure (c_ptr, c_col).
-int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
-                  const int64_t* om_ptr, const int32_t* om_col, const void* om_val, void* c_w,
-                  cudaStream_t st);
+
 
 // KKT residual (Eq. 3.3) over C with penalty lam: row maxima -> *out (device).
 int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,

@@ -978,10 +978,19 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
   }
   c->launches += launch_finalize(c->dtype, c->pk, pv, c->c_ptr, c->rcur, c->keys,
                                  c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S);
-  if (filt)
-    c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
-                                 c->om_val, c->c_w, S);
   c->items_of = nullptr;   // C changed
+  if (filt) {
+    const ProxItems* pit = nullptr;
+    ProxItems pitems{};
+    if (!c->sharded) {   // work items of C (also used by the refine and the trials)
+      build_items(c, c->c_ptr);
+      pitems = ProxItems{c->itm_ptr, c->item_row, c->n_items, kItemEntries, nullptr, nullptr,
+                         nullptr, nullptr};
+      pit = &pitems;
+    }
+    c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
+                                 c->om_val, c->c_w, S, pit);
+  }
   CK(cudaEventRecord(c->ev[3], S));
   TR(c, "finalize");
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) {

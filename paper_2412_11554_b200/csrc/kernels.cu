@@ -673,12 +673,22 @@ template <typename T>
 __global__ void lookup_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
                               const int32_t* __restrict__ c_col, const int64_t* __restrict__ om_ptr,
                               const int32_t* __restrict__ om_col, const T* __restrict__ om_val,
-                              T* __restrict__ c_w) {
+                              T* __restrict__ c_w, ProxItems pi) {
   const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= pk) return;
+  const int64_t w_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t r = w_id, beg, end;
+  if (pi.itm_ptr) {   // warp per work item (hub rows split)
+    if (w_id >= pi.n_items) return;
+    r = pi.item_row[w_id];
+    beg = c_ptr[r] + (w_id - pi.itm_ptr[r]) * pi.L;
+    end = min(c_ptr[r + 1], beg + pi.L);
+  } else {
+    if (r >= pk) return;
+    beg = c_ptr[r];
+    end = c_ptr[r + 1];
+  }
   const int64_t ob = om_ptr[r], oe = om_ptr[r + 1];
-  for (int64_t e = c_ptr[r] + lane; e < c_ptr[r + 1]; e += 32) {
+  for (int64_t e = beg + lane; e < end; e += 32) {
     const int32_t k = c_col[e];
     int64_t lo = ob, hi = oe;
     while (lo < hi) {
@@ -1101,14 +1111,17 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
 
 int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
                   const int64_t* om_ptr, const int32_t* om_col, const void* om_val, void* c_w,
-                  cudaStream_t st) {
-  const unsigned g = (unsigned)((pk + 7) / 8);
+                  cudaStream_t st, const ProxItems* items) {
+  const ProxItems pi = items ? *items
+                            : ProxItems{nullptr, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr};
+  const int64_t nw = pi.itm_ptr ? pi.n_items : pk;
+  const unsigned g = (unsigned)std::max<int64_t>(1, (nw + 7) / 8);
   if (dtype == ACCORD_F64)
     lookup_kernel<double><<<g, 256, 0, st>>>(pk, c_ptr, c_col, om_ptr, om_col,
-                                             (const double*)om_val, (double*)c_w);
+                                             (const double*)om_val, (double*)c_w, pi);
   else
     lookup_kernel<float><<<g, 256, 0, st>>>(pk, c_ptr, c_col, om_ptr, om_col,
-                                            (const float*)om_val, (float*)c_w);
+                                            (const float*)om_val, (float*)c_w, pi);
   return 1;
 }
 

@@ -181,3 +181,47 @@ def test_tma_spmm_matches_block_per_row_spmm(p, n, lam, T, monkeypatch):
     assert np.abs(c0.val - c1.val).max() <= 1e-6 * np.abs(c1.val).max()
     if p == 4000:
         assert m0 > 2048   # multi-item rows were exercised
+
+
+@pytest.mark.parametrize("gemm", [A.GEMM_SIMT, A.GEMM_BF16X3, A.GEMM_BF16_FILTER])
+@pytest.mark.parametrize("p,n,lam", [(1, 7, 0.1), (2, 1, 0.3), (3, 5, 0.2), (257, 65, 0.05),
+                                     (5, 300, 0.0)])
+def test_degenerate_and_ragged_shapes(p, n, lam, gemm):
+    """Edge cases of the method and of the tiling: p = 1 (Omega is the single
+    diagonal root), n = 1 (rank-one S), lambda = 0 with n > p
+    (no shrinkage), one more row/column than a 256 tile and one more sample
+    than a 64-sample K block, against the oracle."""
+    _cuda()
+    rng = np.random.default_rng(1000 * p + n)
+    Xt = rng.standard_normal((p, n))
+    if n > 1:
+        Xt -= Xt.mean(axis=1, keepdims=True)
+    Xt = Xt.astype(np.float32)
+    inv_L = 1.0 / max(O.spectral_bound(Xt.astype(np.float64)), 1e-12)
+    T = 6
+    csr, stats, info = run_gpu(Xt, lam, T, inv_L, gemm)
+    assert info["gemm"] == gemm
+    compare_full(Xt, lam, T, inv_L, csr.to_dense(p), stats, "f32")
+    if p == 1:
+        # converged, the single entry is the closed form (-lam + sqrt(lam^2 + 4s)) / (2s)
+        s = float(Xt[0].astype(np.float64) @ Xt[0].astype(np.float64)) / n
+        w_hat = (-lam + np.sqrt(lam ** 2 + 4 * s)) / (2 * s)
+        X1 = torch.from_numpy(Xt).cuda()
+        with A.AccordSolver(X1, lam, inv_L=inv_L, gemm=gemm) as sv:
+            sv.solve(max_iter=500, tol=1e-9)
+            c1 = sv.export_csr()
+        assert c1.col.tolist() == [0]
+        assert abs(c1.val[0] - w_hat) <= 1e-6 * w_hat
+
+
+def test_empty_rank_block_rejected_and_bad_params():
+    _cuda()
+    X = torch.ones((8, 4), dtype=torch.float32).cuda()
+    with pytest.raises(A.AccordError):
+        A.AccordSolver(X, 0.1, row_begin=4, row_end=4)      # empty row block
+    with pytest.raises(A.AccordError):
+        A.AccordSolver(X, 0.1, tau0=0.0)
+    with pytest.raises(A.AccordError):
+        A.AccordSolver(X, 0.1, beta=1.5)
+    with pytest.raises(A.AccordError):
+        A.AccordSolver(X.double(), 0.1, gemm=A.GEMM_BF16_FILTER)   # tensor cores need F32
