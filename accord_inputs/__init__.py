@@ -78,6 +78,14 @@ CONFIGS = {
             dtype="f32", structure="ba_hubs", block=1000, lambdas=(0.1,), T=50),
     5: _cfg(5, name="c5_ba1000x1000_p1000000_n1000_f32", p=1000000, n=1000,
             dtype="f32", structure="ba", block=1000, lambdas=(0.15,), T=20),
+    # Optional "TCGA-shaped" stand-in: the shape and lambda of
+    # the paper's TCGA LIHC case study (p = 285,358 probes, n = 365 samples,
+    # lambda = 0.45) on synthetic block-diagonal data with
+    # small local blocks (genome-ordered probes), standardized
+    # columns. No TCGA values are used.
+    6: _cfg(6, name="c6_tcga_shaped_p285358_n365_f32", p=285358, n=365,
+            dtype="f32", structure="ba", block=500, lambdas=(0.45,), T=20,
+            extra={"standardize": True}),
 }
 
 # Small cases of the same recipes, for tests that must finish in seconds.
@@ -218,19 +226,18 @@ def _chain_block(b, rho):
 def make_omega0(cfg: Config, wlo=0.3, whi=0.6):
     """List of diagonal blocks of the ground-truth Omega0 (block-diagonal)."""
     rng = np.random.default_rng(cfg.graph_seed)
-    if cfg.p % cfg.block:
-        raise ValueError("p must be a multiple of the block size")
-    nb = cfg.p // cfg.block
+    # equal blocks; a smaller last block when the block size does not divide p
+    nb = -(-cfg.p // cfg.block)
+    sizes = [cfg.block] * (nb - 1) + [cfg.p - (nb - 1) * cfg.block]
     blocks = []
-    for _ in range(nb):
+    for b in sizes:
         if cfg.structure == "chain":
-            blocks.append(_chain_block(cfg.block, cfg.rho))
+            blocks.append(_chain_block(b, cfg.rho))
         elif cfg.structure == "ba":
-            blocks.append(_ba_block(cfg.block, rng, wlo, whi))
+            blocks.append(_ba_block(b, rng, wlo, whi))
         elif cfg.structure == "ba_hubs":
-            nh = max(1, int(round(cfg.hub_frac * cfg.block)))
-            blocks.append(_ba_block(cfg.block, rng, wlo, whi, nh,
-                                    min(cfg.hub_degree, cfg.block - 1)))
+            nh = max(1, int(round(cfg.hub_frac * b)))
+            blocks.append(_ba_block(b, rng, wlo, whi, nh, min(cfg.hub_degree, b - 1)))
         else:
             raise ValueError(cfg.structure)
     return blocks
@@ -331,6 +338,8 @@ def make_problem(cfg, with_blocks: bool = True) -> Problem:
     cfg = get_config(cfg) if not isinstance(cfg, Config) else cfg
     blocks = make_omega0(cfg)
     Xt = center_rows(sample_xt(cfg, blocks))
+    if cfg.extra.get("standardize"):   # unit-variance variables (c6)
+        Xt /= np.sqrt((Xt * Xt).mean(axis=1, keepdims=True))
     dt = np.float64 if cfg.dtype == "f64" else np.float32
     Xt = np.ascontiguousarray(Xt.astype(dt))
     return Problem(cfg, Xt, blocks if with_blocks else [])

@@ -1,4 +1,5 @@
-"""Parity at BASELINE.json's full sizes (configs 3, 4, 5), in the launch
+"""Parity at BASELINE.json's full sizes (configs 3, 4, 5, and the optional
+TCGA-shaped config 6 of SURVEY.md §8(d)), in the launch
 configuration bench.py times (default tensor-core path, L from the device
 power iteration, one GPU).
 
@@ -41,7 +42,7 @@ def sample_rows(pr, k=48, seed=0):
     return np.array(sorted(rows))
 
 
-@pytest.mark.parametrize("key", [3, 4, 5])
+@pytest.mark.parametrize("key", [3, 4, 5, 6])
 def test_fullsize_sampled_rows(key):
     if not torch.cuda.is_available():
         pytest.fail("CUDA not available on a -m gpu run")

@@ -77,6 +77,6 @@ if __name__ == "__main__":
         out.append(full(1, lam))
     for lam in get_config(2).lambdas:
         out.append(full(2, lam))
-    for key in (3, 4, 5):
+    for key in (3, 4, 5, 6):
         out.append(sampled(key))
     print(json.dumps(out, indent=1))
