@@ -161,6 +161,7 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 // Work items over a CSR (row chunks of <= L entries; rows longer than L
 // become several items) for the TMA-staged SpMM and the refine.
 constexpr int kSpmmTmaMaxConsumers = 256;   // ldk <= 2048
+constexpr int kSpmmPairMaxConsumers = 128;  // paired-trial variant: ldk <= 1024
 constexpr int64_t kItemEntries = 2048;
 struct SpmmItems {
   const int64_t* itm_ptr;     // [rows + 1] exclusive scan of items per row
@@ -168,6 +169,7 @@ struct SpmmItems {
   const int64_t* slot_ptr;    // [rows + 1] scratch slots of multi-item rows
   double* part_y;             // [slots x ldk] partial Y+ of multi-item rows
   double* part_d;             // [slots x ldk] partial D
+  double* part_d2;            // [slots x ldk] partial D' (paired trial; may be NULL otherwise)
   int32_t* row_done;          // [rows] items finished (reset to 0 by the finisher)
   int64_t L;
 };
@@ -182,7 +184,7 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                     const float* wn, const float* wo, const float* Xt, float* Yout,
                     __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
                     double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
-                    cudaStream_t st);
+                    cudaStream_t st, const float* wn2 = nullptr, double* row_D2b = nullptr);
 
 // Columns [v0, v1) only, Xt row 0 = column v0 (one ring step of the sharded mode).
 // itm_ptr != NULL: one block per work item (row chunk of <= L candidates).

@@ -124,7 +124,7 @@ struct accord_ctx {
   bool tma_spmm = false;
   int32_t *itm_n = nullptr, *itm_s = nullptr, *row_done = nullptr;
   int64_t *itm_ptr = nullptr, *slot_ptr = nullptr;
-  double *part_y = nullptr, *part_d = nullptr;
+  double *part_y = nullptr, *part_d = nullptr, *part_d2 = nullptr;
   int64_t part_slots = 0, n_items = 0, n_slots = 0;
   double *itm_dd = nullptr, *itm_l1 = nullptr, *itm_logd = nullptr;   // per-item prox sums
   int32_t* itm_nnz = nullptr;
@@ -149,6 +149,10 @@ struct accord_ctx {
   int64_t* c_ptr = nullptr;
   int32_t* c_col = nullptr;
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
+  void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
+  bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
+  double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
+  int32_t* row_nnz2 = nullptr;
   uint64_t *keys = nullptr, *keys_tmp = nullptr;
   int32_t *pool_row = nullptr, *pool_col = nullptr;
   void *pool_g = nullptr, *pool_w = nullptr;
@@ -342,9 +346,11 @@ void build_items(accord_ctx* c, const int64_t* ptr) {
     const size_t b = (size_t)c->part_slots * c->ldk * 8;
     c->dfree(c->part_y, b);
     c->dfree(c->part_d, b);
+    c->dfree(c->part_d2, b);
     c->part_slots = c->n_slots + c->n_slots / 4 + 16;
     c->part_y = c->dalloc<double>((size_t)c->part_slots * c->ldk);
     c->part_d = c->dalloc<double>((size_t)c->part_slots * c->ldk);
+    c->part_d2 = c->dalloc<double>((size_t)c->part_slots * c->ldk);
   }
   if (c->n_items > c->itm_cap) {
     c->dfree(c->itm_dd, c->itm_cap * 8);
@@ -364,8 +370,8 @@ void build_items(accord_ctx* c, const int64_t* ptr) {
 }
 
 SpmmItems items_view(accord_ctx* c) {
-  return SpmmItems{c->itm_ptr, c->item_row, c->slot_ptr, c->part_y, c->part_d, c->row_done,
-                   kItemEntries};
+  return SpmmItems{c->itm_ptr, c->item_row, c->slot_ptr, c->part_y, c->part_d, c->part_d2,
+                   c->row_done, kItemEntries};
 }
 
 // SpMM Y+ = W X^T (and D = (W - Wold) X^T) over all of X: one launch, or a
@@ -429,6 +435,7 @@ void grow(accord_ctx* c, int64_t cap, int64_t keep_nnz) {
   c->dfree(c->c_g, oc * T);     c->c_g = c->dalloc_bytes(cap * T);
   c->dfree(c->c_w, oc * T);     c->c_w = c->dalloc_bytes(cap * T);
   c->dfree(c->c_wn, oc * T);    c->c_wn = c->dalloc_bytes(cap * T);
+  c->dfree(c->c_wn2, oc * T);   c->c_wn2 = c->dalloc_bytes(cap * T);
   c->dfree(c->keys, oc * 8);    c->keys = c->dalloc<uint64_t>(cap);
   c->dfree(c->keys_tmp, oc * 8); c->keys_tmp = c->dalloc<uint64_t>(cap);
   c->dfree(c->pool_row, oc * 4); c->pool_row = c->dalloc<int32_t>(cap);
@@ -776,6 +783,15 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->row_l1 = c->dalloc<double>(c->pk);
   c->row_logd = c->dalloc<double>(c->pk);
   c->row_nnz = c->dalloc<int32_t>(c->pk);
+  c->row_dd2 = c->dalloc<double>(c->pk);
+  c->row_l1_2 = c->dalloc<double>(c->pk);
+  c->row_logd2 = c->dalloc<double>(c->pk);
+  c->row_D2b = c->dalloc<double>(c->pk);
+  c->row_nnz2 = c->dalloc<int32_t>(c->pk);
+  {
+    const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
+    c->pair_ls = !(e && e[0] == '0');
+  }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
   c->scan_tmp = c->dalloc_bytes(c->scan_tmp_sz);
@@ -1015,46 +1031,95 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   const int nb = c->cur ^ 1;
   double tau = c->tau0;
   double r[8];
-  for (;;) {
-    st.trials++;
+  // One line-search pass: prox at ta (and at beta*ta when paired), SpMM, the
+  // per-trial sums reduced and all-reduced into h_red[0..7] (and [8..15]).
+  // Paired: the same gather pass also accumulates D' for beta*ta, so a
+  // rejected first step costs no second pass (the sums of the second step are
+  // bitwise those of its own pass: the extra entries carry Delta' = 0).
+  auto run_trial = [&](double ta, bool paired) {
     CK(cudaEventRecord(c->ev[4], S));
     const ProxItems pitems{c->itm_ptr, c->item_row, c->n_items, kItemEntries, c->itm_dd,
                            c->itm_l1, c->itm_logd, c->itm_nnz};
+    const ProxItems* pit = c->items_of == c->c_ptr ? &pitems : nullptr;
     c->launches += launch_prox(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, c->c_w,
-                               c->c_wn, tau, lam, c->row_dd, c->row_l1, c->row_logd,
-                               c->row_nnz, S, c->items_of == c->c_ptr ? &pitems : nullptr);
+                               c->c_wn, ta, lam, c->row_dd, c->row_l1, c->row_logd,
+                               c->row_nnz, S, pit);
+    if (paired)
+      c->launches += launch_prox(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, c->c_w,
+                                 c->c_wn2, ta * c->beta, lam, c->row_dd2, c->row_l1_2,
+                                 c->row_logd2, c->row_nnz2, S, pit);
     CK(cudaEventRecord(c->ev[5], S));
     TR(c, "prox");
-    spmm_all(c, c->c_ptr, c->c_col, c->c_wn, c->c_w, nb, c->row_D2, c->row_Y2);
+    if (paired) {
+      if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
+      c->launches += launch_spmm_tma(c->pk, c->ldk, c->c_ptr, c->c_col, (const float*)c->c_wn,
+                                     (const float*)c->c_w, (const float*)c->Xt,
+                                     (float*)c->Y[nb], c->Yhi[nb], c->Ylo[nb], c->row_A[nb],
+                                     c->row_B[nb], c->row_D2, c->row_Y2, items_view(c),
+                                     c->sm_count, S, (const float*)c->c_wn2, c->row_D2b);
+    } else {
+      spmm_all(c, c->c_ptr, c->c_col, c->c_wn, c->c_w, nb, c->row_D2, c->row_Y2);
+    }
     CK(cudaEventRecord(c->ev[6], S));
     TR(c, "spmm");
     c->launches += launch_reduce_rows(c->pk, c->row_D2, c->row_dd, c->row_logd, c->row_Y2,
                                       c->row_l1, c->row_nnz, c->c_ptr, c->red_d, S);
+    if (paired)
+      c->launches += launch_reduce_rows(c->pk, c->row_D2b, c->row_dd2, c->row_logd2, nullptr,
+                                        c->row_l1_2, c->row_nnz2, c->c_ptr, c->red_d + 8, S);
     CK(cudaGetLastError());
-    allreduce(c, c->red_d, c->h_red, 8);
+    allreduce(c, c->red_d, c->h_red, paired ? 16 : 8);
     CK(cudaEventRecord(c->ev[7], S));
     TR(c, "reduce+decide");
     CK(cudaEventSynchronize(c->ev[7]));
     st.ms_prox += ev_ms(c, 4, 5);
     st.ms_spmm += ev_ms(c, 5, 6);
     st.ms_reduce += ev_ms(c, 6, 7);
-    std::memcpy(r, c->h_red, sizeof(r));
-    for (int k = 0; k < 7; ++k)
-      if (!std::isfinite(r[k])) {
+    for (int k = 0; k < (paired ? 15 : 7); ++k)
+      if (k != 7 && !std::isfinite(c->h_red[k])) {
         char m[128];
         std::snprintf(m, sizeof m, "non-finite line-search sum at iteration %lld",
                       (long long)c->iters);
         throw Fail{ACCORD_E_NUMERIC, m};
       }
+  };
+  const bool pair_ok = c->pair_ls && c->tma_spmm && !c->sharded && c->beta < 1.0 &&
+                       c->ldk <= 8 * kSpmmPairMaxConsumers;
+  for (;;) {
+    // a trial at or below the 1/L floor is accepted whatever the test says
+    const bool paired = pair_ok && !(tau <= c->inv_L);
+    run_trial(tau, paired);
+    std::memcpy(r, c->h_red, sizeof(r));
+    st.trials++;
     // Sufficient decrease in the exact-quadratic form (reading R8):
     // ||Delta X^T||^2 / n <= ||Delta||^2 / tau, or tau <= 1/L.
-    const double lhs = r[0] / (double)c->n, rhs = r[1] / tau;
+    double lhs = r[0] / (double)c->n, rhs = r[1] / tau;
     st.ls_lhs = lhs;
     st.ls_rhs = rhs;
-    const bool floor_hit = tau <= c->inv_L;
+    bool floor_hit = tau <= c->inv_L;
     if (c->beta >= 1.0 || lhs <= rhs || floor_hit) {
       st.floor_hit = (!(lhs <= rhs) && floor_hit) ? 1 : 0;
       break;
+    }
+    if (paired) {   // the second step of the pair, from the same pass
+      const double tb = tau * c->beta;
+      st.trials++;
+      const double lb = c->h_red[8] / (double)c->n, rb = c->h_red[9] / tb;
+      if (lb <= rb || tb <= c->inv_L) {
+        // accepted: its Y+ (and the committed sums) from a pass of its own
+        tau = tb;
+        run_trial(tau, false);
+        std::memcpy(r, c->h_red, sizeof(r));
+        lhs = r[0] / (double)c->n;
+        rhs = r[1] / tau;
+        st.ls_lhs = lhs;
+        st.ls_rhs = rhs;
+        floor_hit = tau <= c->inv_L;
+        st.floor_hit = (!(lhs <= rhs) && floor_hit) ? 1 : 0;
+        break;
+      }
+      tau = tb * c->beta;
+      continue;
     }
     tau *= c->beta;
   }

@@ -31,7 +31,7 @@ namespace {
 constexpr int kFlagData = 1, kFlagLast = 2, kFlagEnd = 4;
 
 struct StageMeta {
-  double w, d;
+  double w, d, d2;                  // d2: Delta of the second step size (kPair)
   int64_t row;
   int32_t chunk, nch;
   int32_t flags, pad;
@@ -55,20 +55,26 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(32 + kSpmmTmaMaxConsumers, 2)
+// kPair: also D' = (W' - Wold) X^T for a second trial step (weights wn2),
+// of which only the row norms ||D'_i||^2 are kept (row_D2b): one gather pass
+// serves two line-search trials.
+template <bool kPair>
+__global__ void __launch_bounds__(kPair ? 32 + kSpmmPairMaxConsumers : 32 + kSpmmTmaMaxConsumers,
+                                  kPair ? 3 : 2)
 spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__ ptr,
                 const int32_t* __restrict__ col, const float* __restrict__ wn,
                 const float* __restrict__ wo, const float* __restrict__ Xt, float* __restrict__ Yout,
                 __nv_bfloat16* __restrict__ Yhi, __nv_bfloat16* __restrict__ Ylo,
                 float* __restrict__ row_A, float* __restrict__ row_B, double* __restrict__ row_D2,
-                double* __restrict__ row_Y2, SpmmItems items) {
+                double* __restrict__ row_Y2, const float* __restrict__ wn2,
+                double* __restrict__ row_D2b, SpmmItems items) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t stage_bytes = (uint32_t)(ldk * 4);
   float* data = reinterpret_cast<float*>(sm);
   StageMeta* meta = reinterpret_cast<StageMeta*>(sm + (size_t)stages * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + stages);
   uint64_t* empty = full + stages;
-  double* red = reinterpret_cast<double*>(empty + stages);   // [4][16] + flag
+  double* red = reinterpret_cast<double*>(empty + stages);   // [5][16] + flag
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncw = (blockDim.x >> 5) - 1;                     // consumer warps
   const int nct = ncw * 32;
@@ -86,12 +92,14 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     // ============================== producer ==============================
     int stage = 0;
     uint32_t phase = 0;
-    auto emit = [&](double w, double d, int32_t c, int flags, int64_t row, int chunk, int nch) {
+    auto emit = [&](double w, double d, double d2, int32_t c, int flags, int64_t row, int chunk,
+                    int nch) {
       tc::mbar_wait(tc::smem_u32(&empty[stage]), phase ^ 1);
       if (lane == 0) {
         StageMeta& m = meta[stage];
         m.w = w;
         m.d = d;
+        m.d2 = d2;
         m.row = row;
         m.chunk = chunk;
         m.nch = nch;
@@ -125,20 +133,22 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       const int64_t endj = min(p1, begj + items.L);
       const int nv = __popc(__ballot_sync(0xffffffffu, vj));
       // entries of the first item
-      auto load = [&](int64_t e, int64_t end, double& w, double& d, int32_t& cc) {
+      auto load = [&](int64_t e, int64_t end, double& w, double& d, double& d2, int32_t& cc) {
         if (e < end) {
           w = (double)__ldg(wn + e);
-          d = wo ? w - (double)__ldg(wo + e) : 0.0;
+          const double o = wo ? (double)__ldg(wo + e) : 0.0;
+          d = wo ? w - o : 0.0;
+          d2 = kPair ? (double)__ldg(wn2 + e) - o : 0.0;
           cc = __ldg(col + e);
         } else {
-          w = 0.0; d = 0.0; cc = 0;
+          w = 0.0; d = 0.0; d2 = 0.0; cc = 0;
         }
       };
-      double nw_ = 0.0, nd_ = 0.0;
+      double nw_ = 0.0, nd_ = 0.0, nd2_ = 0.0;
       int32_t nc_ = 0;
       {
         const int64_t b0 = __shfl_sync(0xffffffffu, begj, 0), e0_ = __shfl_sync(0xffffffffu, endj, 0);
-        load(b0 + lane, e0_, nw_, nd_, nc_);
+        load(b0 + lane, e0_, nw_, nd_, nd2_, nc_);
       }
       for (int k = 0; k < nv; ++k) {
         const int64_t r = __shfl_sync(0xffffffffu, rj, k);
@@ -146,39 +156,41 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         const int nch = __shfl_sync(0xffffffffu, nchj, k);
         const int64_t beg = __shfl_sync(0xffffffffu, begj, k);
         const int64_t end = __shfl_sync(0xffffffffu, endj, k);
-        double w = nw_, d = nd_;
+        double w = nw_, d = nd_, d2 = nd2_;
         int32_t cc = nc_;
         if (k + 1 < nv) {   // lookahead: first batch of the next item
           const int64_t bn = __shfl_sync(0xffffffffu, begj, k + 1);
           const int64_t en = __shfl_sync(0xffffffffu, endj, k + 1);
-          load(bn + lane, en, nw_, nd_, nc_);
+          load(bn + lane, en, nw_, nd_, nd2_, nc_);
         }
         // one entry of lookahead so that the item's last nonzero carries kFlagLast
         bool pend = false;
-        double pw = 0.0, pd = 0.0;
+        double pw = 0.0, pd = 0.0, pd2 = 0.0;
         int32_t pc = 0;
         for (int64_t e0 = beg; e0 < end; e0 += 32) {
-          if (e0 != beg) load(e0 + lane, end, w, d, cc);
-          const bool keep = (e0 + lane < end) && ((w != 0.0) || (d != 0.0));
+          if (e0 != beg) load(e0 + lane, end, w, d, d2, cc);
+          const bool keep = (e0 + lane < end) && ((w != 0.0) || (d != 0.0) || (d2 != 0.0));
           unsigned m = __ballot_sync(0xffffffffu, keep);
           while (m) {
             const int src = __ffs(m) - 1;
             m &= m - 1;
             const double ws = __shfl_sync(0xffffffffu, w, src);
             const double ds = __shfl_sync(0xffffffffu, d, src);
+            const double ds2 = kPair ? __shfl_sync(0xffffffffu, d2, src) : 0.0;
             const int32_t cs = __shfl_sync(0xffffffffu, cc, src);
-            if (pend) emit(pw, pd, pc, kFlagData, r, chunk, nch);
+            if (pend) emit(pw, pd, pd2, pc, kFlagData, r, chunk, nch);
             pend = true;
             pw = ws;
             pd = ds;
+            pd2 = ds2;
             pc = cs;
           }
         }
-        if (pend) emit(pw, pd, pc, kFlagData | kFlagLast, r, chunk, nch);
-        else emit(0.0, 0.0, 0, kFlagLast, r, chunk, nch);
+        if (pend) emit(pw, pd, pd2, pc, kFlagData | kFlagLast, r, chunk, nch);
+        else emit(0.0, 0.0, 0.0, 0, kFlagLast, r, chunk, nch);
       }
     }
-    emit(0.0, 0.0, 0, kFlagEnd, 0, 0, 0);
+    emit(0.0, 0.0, 0.0, 0, kFlagEnd, 0, 0, 0);
     return;
   }
 
@@ -186,19 +198,20 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
   const int t = threadIdx.x - 32;
   const int64_t c0 = (int64_t)t * 8;
   const bool active = c0 < ldk;
-  double ay[8], ad[8];
+  double ay[8], ad[8], ae[8];   // Y+, D, and D' (kPair)
 #pragma unroll
-  for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+  for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
   int stage = 0;
   uint32_t phase = 0;
-  double* sh_red = red;                                   // [16] per-warp partials x 4
-  volatile int* sh_flag = reinterpret_cast<volatile int*>(red + 64);
-  auto accumulate = [&](double w, double d, float4 x0, float4 x1) {
+  double* sh_red = red;                                   // [16] per-warp partials x 5
+  volatile int* sh_flag = reinterpret_cast<volatile int*>(red + 80);
+  auto accumulate = [&](double w, double d, double d2, float4 x0, float4 x1) {
     const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
       ay[v] = fma(w, (double)xv[v], ay[v]);
       ad[v] = fma(d, (double)xv[v], ad[v]);
+      if constexpr (kPair) ae[v] = fma(d2, (double)xv[v], ae[v]);
     }
   };
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -210,6 +223,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     const int f0 = meta[stage].flags;
     if (f0 & kFlagEnd) break;
     const double w0 = meta[stage].w, d0 = meta[stage].d;
+    const double e0d = kPair ? meta[stage].d2 : 0.0;
     float4 a0 = z4, b0 = z4;
     if ((f0 & kFlagData) && active) {
       const float* xs = data + (size_t)stage * ldk + c0;
@@ -220,13 +234,14 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     const uint32_t ph1 = stage + 1 == stages ? phase ^ 1 : phase;
     const bool two = !(f0 & kFlagLast);   // the item goes on: stage s1 belongs to it
     int f1 = 0;
-    double w1 = 0.0, d1 = 0.0;
+    double w1 = 0.0, d1 = 0.0, e1d = 0.0;
     float4 a1 = z4, b1 = z4;
     if (two) {
       tc::mbar_wait(tc::smem_u32(&full[s1]), ph1);
       f1 = meta[s1].flags;
       w1 = meta[s1].w;
       d1 = meta[s1].d;
+      if constexpr (kPair) e1d = meta[s1].d2;
       if ((f1 & kFlagData) && active) {
         const float* xs = data + (size_t)s1 * ldk + c0;
         a1 = *reinterpret_cast<const float4*>(xs);
@@ -237,8 +252,8 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     const int ls = (f0 & kFlagLast) ? stage : s1;
     StageMeta m;
     if (last) m = meta[ls];   // row / chunk of the finished item (before the release)
-    accumulate(w0, d0, a0, b0);
-    if (two) accumulate(w1, d1, a1, b1);
+    accumulate(w0, d0, e0d, a0, b0);
+    if (two) accumulate(w1, d1, e1d, a1, b1);
     __syncwarp();
     if (lane == 0) {
       tc::mbar_arrive(tc::smem_u32(&empty[stage]));
@@ -261,6 +276,11 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         double* pd = items.part_d + (slot0 + m.chunk) * ldk + c0;
 #pragma unroll
         for (int v = 0; v < 8; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
+        if constexpr (kPair) {
+          double* pe = items.part_d2 + (slot0 + m.chunk) * ldk + c0;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) pe[v] = ae[v];
+        }
       }
       __threadfence();
       named_sync(1, nct);
@@ -271,7 +291,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         __threadfence();
         if (active) {
 #pragma unroll
-          for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+          for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
           for (int k = 0; k < m.nch; ++k) {   // chunk order: deterministic sum
             const double* py = items.part_y + (slot0 + k) * ldk + c0;
             const double* pd = items.part_d + (slot0 + k) * ldk + c0;
@@ -280,19 +300,25 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
               ay[v] += __ldcg(py + v);
               ad[v] += __ldcg(pd + v);
             }
+            if constexpr (kPair) {
+              const double* pe = items.part_d2 + (slot0 + k) * ldk + c0;
+#pragma unroll
+              for (int v = 0; v < 8; ++v) ae[v] += __ldcg(pe + v);
+            }
           }
         }
         if (t == 0) items.row_done[r] = 0;   // ready for the next trial
       }
     }
     if (finish) {
-      double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0;
+      double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0, e2 = 0.0;
       if (active) {
         float yt[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           d2 += ad[v] * ad[v];
           y2 += ay[v] * ay[v];
+          if constexpr (kPair) e2 += ae[v] * ae[v];
           yt[v] = (float)ay[v];
         }
         float* yo = Yout + r * ldk + c0;
@@ -320,23 +346,27 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       y2 = wsum(y2);
       a2 = wsum(a2);
       b2 = wsum(b2);
+      if constexpr (kPair) e2 = wsum(e2);
       const int cw = warp - 1;
       if (lane == 0) {
         sh_red[cw] = d2;
         sh_red[16 + cw] = y2;
         sh_red[32 + cw] = a2;
         sh_red[48 + cw] = b2;
+        sh_red[64 + cw] = e2;
       }
       named_sync(1, nct);
       if (t == 0) {
-        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
         for (int q = 0; q < ncw; ++q) {   // fixed order
           s0 += sh_red[q];
           s1 += sh_red[16 + q];
           s2 += sh_red[32 + q];
           s3 += sh_red[48 + q];
+          s4 += sh_red[64 + q];
         }
         if (row_D2) row_D2[r] = s0;
+        if (kPair && row_D2b) row_D2b[r] = s4;
         if (row_Y2) row_Y2[r] = s1;
         if (Yhi) {
           // rounded up: these enter an upper bound (the GEMM filter)
@@ -347,7 +377,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       named_sync(1, nct);
     }
 #pragma unroll
-    for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; }
+    for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
   }
 }
 
@@ -386,7 +416,7 @@ size_t spmm_tma_smem(int64_t ldk, int* stages) {
   if (const char* e = std::getenv("ACCORD_SPMM_STAGES")) want = std::max(2, std::atoi(e));
   int s = (int)std::min<int64_t>(want, std::max<int64_t>(2, (want * 4096) / sb));
   *stages = s;
-  return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 65 * 8 + 64;
+  return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 81 * 8 + 64;
 }
 
 bool spmm_tma_supported(int dtype, int64_t ldk) {
@@ -408,24 +438,32 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                     const float* wn, const float* wo, const float* Xt, float* Yout,
                     __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
                     double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
-                    cudaStream_t st) {
+                    cudaStream_t st, const float* wn2, double* row_D2b) {
   if (pk == 0) return 0;
   int stages = 0;
   const size_t smem = spmm_tma_smem(ldk, &stages);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(spmm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spmm_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         100 * 1024);
+    cudaFuncSetAttribute(spmm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          100 * 1024);
     attr = true;
   }
   const int consumers = (int)round_up(ldk / 8, 32);
   // persistent: exactly the resident blocks (items are dealt round-robin)
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_tma_kernel, 32 + consumers,
-                                                    smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  spmm_tma_kernel<<<sm_count * std::min(per_sm, 8), 32 + consumers, smem, st>>>(
-      pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2, items);
+  auto launch = [&](auto kern) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 + consumers, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    kern<<<sm_count * std::min(per_sm, 8), 32 + consumers, smem, st>>>(
+        pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2,
+        wn2, row_D2b, items);
+  };
+  if (wn2) launch(spmm_tma_kernel<true>);
+  else launch(spmm_tma_kernel<false>);
   return 1;
 }
 

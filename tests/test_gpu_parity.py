@@ -225,3 +225,27 @@ def test_empty_rank_block_rejected_and_bad_params():
         A.AccordSolver(X, 0.1, beta=1.5)
     with pytest.raises(A.AccordError):
         A.AccordSolver(X.double(), 0.1, gemm=A.GEMM_BF16_FILTER)   # tensor cores need F32
+
+
+@pytest.mark.parametrize("p,n,lam,T", [(4000, 60, 0.05, 4), (1100, 333, 0.1, 10)])
+def test_paired_line_search_is_bitwise_sequential(p, n, lam, T, monkeypatch):
+    """Paired trials (one gather pass evaluates tau and beta*tau) take exactly
+    the sequential decisions of Algorithm 1: same tau
+    schedule, trial counts and bitwise-identical iterates."""
+    _cuda()
+    rng = np.random.default_rng(17 + p)
+    Xt = rng.standard_normal((p, n)).astype(np.float32)
+    Xt -= Xt.mean(axis=1, keepdims=True)
+    inv_L = 1.0 / O.spectral_bound(Xt.astype(np.float64))
+    monkeypatch.setenv("ACCORD_SPMM_TMA", "1")
+    out = {}
+    for pairs in ("1", "0"):
+        monkeypatch.setenv("ACCORD_LS_PAIRS", pairs)
+        with A.AccordSolver(torch.from_numpy(Xt).cuda(), lam, inv_L=inv_L, tau0=4.0) as s:
+            st = s.step(T)
+            out[pairs] = ([(x["tau"], x["trials"], x["f"]) for x in st], s.export_csr())
+    (s1, c1), (s0, c0) = out["1"], out["0"]
+    assert s1 == s0
+    assert max(t for _, t, _ in s1) >= 2          # rejected trials were exercised
+    assert np.array_equal(c1.row_ptr, c0.row_ptr) and np.array_equal(c1.col, c0.col)
+    assert np.array_equal(c1.val, c0.val)
