@@ -621,7 +621,9 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   const int grid = tc_grid_size(plan, sm_count);
   // A group of <= 64 N-blocks (<= 32 MB of X^T_hi at n = 1000) stays in L2;
   // units small enough that the per-cluster imbalance is <= ~6% of its work
-  int gn = 32;   // measured best of 16..64 at c5 (tools/gemm_sweep.py)
+  // X^T group of gn N-blocks (gn x 256 rows x ldk bf16 stay L2-resident):
+  // measured best 48 at ldk = 1024 (c5, 6 alternating reps), 32 at ldk = 2048
+  int gn = plan->ldk <= 1024 ? 48 : 32;
   if (const char* e = std::getenv("ACCORD_GEMM_GN")) gn = std::max(1, std::atoi(e));   // tuning
   const int group_n = num_n < gn ? num_n : gn;
   const long long tiles = (long long)num_m * num_n;

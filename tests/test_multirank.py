@@ -153,7 +153,7 @@ def test_p_invariance_one_gpu(gemm):
     ref, _ = run_ranks(pr.Xt, c.lambdas[0], c.T, inv_L, 1, gemm)
     taus1 = [s["tau"] for s in ref[0][0]]
     W1 = ref[0][1].to_dense(c.p)
-    for P, align in [(2, 256), (3, 1)]:
+    for P, align in [(2, 256), (3, 1), (4, 256), (8, 1)]:   # P in {1, 2, 4, 8}
         out, bounds = run_ranks(pr.Xt, c.lambdas[0], c.T, inv_L, P, gemm, align)
         for r in range(P):
             st, g, loc, f = out[r]

@@ -24,7 +24,7 @@ X = torch.from_numpy(pr.Xt).cuda()
 
 def run(solver, tag):
     res = {st: [] for st in settings}
-    for rep in range(3):
+    for rep in range(int(os.environ.get("SWEEP_REPS", "3"))):
         for st in settings:
             os.environ["ACCORD_GEMM_VARIANT"] = str(st[0])
             os.environ["ACCORD_GEMM_GN"] = str(st[1])
