@@ -219,7 +219,7 @@ namespace {
 
 void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
   // d_buf (device) -> h_buf (host), summed over ranks. Synchronizes the stream.
-  if (c->world > 1 && c->comm == ACCORD_COMM_NCCL) {
+  if (c->comm == ACCORD_COMM_NCCL) {   // (a 1-rank communicator is exercised by the tests)
     NK(nccl_api()->AllReduce(d_buf, d_buf, count, ncclDouble, ncclSum, c->nccl, c->st));
   }
   CK(cudaMemcpyAsync(h_buf, d_buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -232,7 +232,7 @@ void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
 // Global maximum of one value per rank (KKT certificate).
 double allreduce_max(accord_ctx* c, double* d_val) {
   double h = 0;
-  if (c->world > 1 && c->comm == ACCORD_COMM_NCCL)
+  if (c->comm == ACCORD_COMM_NCCL)
     NK(nccl_api()->AllReduce(d_val, d_val, 1, ncclDouble, ncclMax, c->nccl, c->st));
   CK(cudaMemcpyAsync(&h, d_val, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -516,7 +516,7 @@ void validate(const accord_init_params* prm) {
     bad("bad row range");
   if (prm->world < 1 || prm->rank < 0 || prm->rank >= prm->world) bad("bad rank/world");
   if (prm->world > 1 && prm->comm == ACCORD_COMM_NONE) bad("world > 1 needs a communicator");
-  if (prm->comm == ACCORD_COMM_NCCL && prm->world > 1 && !prm->nccl_id) bad("nccl_id is NULL");
+  if (prm->comm == ACCORD_COMM_NCCL && !prm->nccl_id) bad("nccl_id is NULL");
   if (prm->comm == ACCORD_COMM_HOST && !prm->allreduce) bad("allreduce callback is NULL");
   if (shard && prm->comm == ACCORD_COMM_HOST && !prm->sendrecv)
     bad("x_sharded with the host communicator needs a sendrecv callback");
@@ -579,7 +579,9 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->beta = prm->beta;
   c->rank = prm->rank;
   c->world = prm->world;
-  c->comm = prm->world > 1 ? prm->comm : ACCORD_COMM_NONE;
+  // world = 1 with NCCL keeps a 1-rank communicator (the collectives then run
+  // for real: the single-GPU tests exercise the NCCL code path)
+  c->comm = (prm->world > 1 || prm->comm == ACCORD_COMM_NCCL) ? prm->comm : ACCORD_COMM_NONE;
   c->ar = prm->allreduce;
   c->agv = prm->allgatherv;
   c->cu = prm->comm_user;
@@ -1338,7 +1340,7 @@ accord_status accord_export_csr(accord_ctx* c, int32_t scope, int64_t* row_ptr, 
   return guard(c, [&] {
     const size_t T = c->tsz;
     const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (scope == ACCORD_SCOPE_LOCAL || c->world == 1) {
+    if (scope == ACCORD_SCOPE_LOCAL || (c->world == 1 && c->comm != ACCORD_COMM_NCCL)) {
       *nnz_out = c->nnz_local;
       if (!row_ptr) return;
       if (capacity < c->nnz_local) throw Fail{ACCORD_E_CAPACITY, "capacity too small"};

@@ -462,3 +462,31 @@ def test_sharded_x_ring_config5_scale():
         g = o["g"]
         assert np.array_equal(g.row_ptr, W1.row_ptr) and np.array_equal(g.col, W1.col)
         assert np.abs(g.val - W1.val).max() <= 1e-6 * np.abs(W1.val).max()
+
+
+@pytest.mark.gpu
+def test_nccl_code_path_with_one_rank():
+    """The NCCL path of the library (dlopen'ed libnccl, CommInitRank, the
+    per-trial AllReduce of the line-search sums, the KKT max-AllReduce, the
+    Broadcast gather of the export) run for real on a 1-rank communicator and
+    must reproduce the communicator-free run exactly."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import make_problem
+    from oracle import accord_oracle as O
+    pr = make_problem("t_hubs_f32")
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    X = torch.from_numpy(pr.Xt).cuda()
+    res = {}
+    for comm in (A.COMM_NONE, A.COMM_NCCL):
+        kw = dict(comm=comm, nccl_id=A.nccl_unique_id()) if comm == A.COMM_NCCL else {}
+        with A.AccordSolver(X, c.lambdas[0], inv_L=inv_L, **kw) as s:
+            st = s.step(c.T)
+            res[comm] = ([(x["tau"], x["f"]) for x in st], s.export_csr(A.SCOPE_GATHER),
+                         s.kkt_residual())
+    (a, ca, ka), (b, cb, kb) = res[A.COMM_NONE], res[A.COMM_NCCL]
+    assert a == b and ka == kb
+    assert np.array_equal(ca.row_ptr, cb.row_ptr) and np.array_equal(ca.col, cb.col)
+    assert np.array_equal(ca.val, cb.val)
