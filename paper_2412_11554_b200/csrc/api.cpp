@@ -938,7 +938,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
       if (tc) {
         const int l = launch_gemm_tc(c->plan, c->gemm, c->cur, bsel, c->sm_count, ep,
                                      omega_view(c), pool_view(c), S);
-        if (l < 0) throw Fail{ACCORD_E_CUDA, "GEMM grid / pool segment mismatch"};
+        if (l < 0) throw Fail{ACCORD_E_CUDA, "tcgen05 GEMM launch failed"};
         c->launches += l;
       } else {
         c->launches += launch_gemm_simt(c->dtype, c->Y[c->cur], xt, c->ldk, c->ldk, ep,
