@@ -277,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(Xh_all.nbytes // args.steps),
                "d2h_bytes_per_step": int(d2h // args.steps),
                "note": "one solve through the C ABI from pinned host X: create (H2D copy, "
-                       "power iteration for L, operand split) + K iterations + CSR export "
+                       "Lanczos for L, operand split) + K iterations + CSR export "
                        "to host; bytes amortized per step"}
 
     if rank != 0:

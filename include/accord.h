@@ -120,7 +120,9 @@ typedef struct {
   double tau0;              /* > 0, initial step of every outer iteration (Alg. 1) */
   double beta;              /* in (0, 1]; 1 = fixed step tau0 (Alg. 1, Thm 3.3 case i) */
   double inv_L;             /* > 0: 1/L given by the caller; 0: computed on device
-                               (power iteration v <- X^T X v / n, inflated by 1e-3) */
+                               (Lanczos on the samples' Gram X X^T / n, whose top eigenvalue
+                               is sigma_max(S); inflated by 2e-3, SPEC.md:85:
+                               overestimating L is safe) */
   int64_t row_begin, row_end;  /* this rank's rows [row_begin, row_end) of Omega; 0 <= begin < end <= p */
   int32_t rank, world;      /* 0 <= rank < world */
   int32_t comm;             /* accord_comm */

@@ -73,15 +73,12 @@ int launch_load_xt(int dtype, const void* X, int64_t ldx, int layout, int64_t n,
 int launch_split_bf16(const float* src, int64_t elems, __nv_bfloat16* hi,
                       __nv_bfloat16* lo, cudaStream_t st);
 
-// Power iteration for L = lambda_max(X^T X / n) on Xt (p x ldk). Deterministic.
-// Returns launches; writes the estimate to *L_host (synchronizes).
-// With X sharded by variables (NEXT(3)), p = this rank's variables, p_global
-// = all, and `ar` sums a device vector of doubles across ranks in place
-// (stream-ordered; returns false on failure).
-using DevAllreduce = std::function<bool(double* dev, int count)>;
-int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk,
-                    int max_iter, double tol, double* L_host, cudaStream_t st,
-                    std::string* err, int64_t p_global = 0, const DevAllreduce* ar = nullptr);
+// w = X (X^T u) / n (the samples' Gram operator; its top eigenvalue is L =
+// sigma_max(S)) on this rank's Xt (p x ldk). t: p doubles,
+// part: nsplit x ldk doubles of scratch. Deterministic.
+int launch_gram_apply(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk,
+                      const double* u, double* t, double* part, int64_t nsplit, double* w,
+                      cudaStream_t st);
 
 // Exclusive scan: out[0..N] (out[N] = total) from int32 counts.
 int launch_scan_i32(const int32_t* in, int64_t* out, int64_t N, void* tmp, size_t tmp_bytes,

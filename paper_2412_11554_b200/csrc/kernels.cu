@@ -916,32 +916,8 @@ __global__ void pi_xtu_kernel(const T* __restrict__ Xt, int64_t p, int64_t ldk, 
   if (lane == 0) w[j] = s / (double)n;
 }
 
-__global__ void __launch_bounds__(1024) pi_dots(const double* __restrict__ v, const double* __restrict__ w, int64_t p,
-                        double* out) {
-  __shared__ double sh[32];
-  double a = 0, b = 0;
-  for (int64_t j = threadIdx.x; j < p; j += blockDim.x) {
-    a += v[j] * w[j];
-    b += w[j] * w[j];
-  }
-  a = block_sum(a, sh);
-  b = block_sum(b, sh);
-  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
-}
 
-__global__ void pi_normalize(const double* __restrict__ w, int64_t p, const double* dots,
-                             double* __restrict__ v) {
-  const double inv = dots[1] > 0 ? 1.0 / sqrt(dots[1]) : 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p;
-       j += (int64_t)gridDim.x * blockDim.x)
-    v[j] = w[j] * inv;
-}
 
-__global__ void fill_d(double* v, int64_t n, double x) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    v[j] = x;
-}
 
 inline int grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
@@ -1192,80 +1168,29 @@ int launch_identity(int dtype, int64_t pk, int64_t r0, int64_t* om_ptr, int32_t*
   return 1;
 }
 
-int power_iteration(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk, int max_iter,
-                    double tol, double* L_host, cudaStream_t st, std::string* err,
-                    int64_t p_global, const DevAllreduce* ar) {
-  // Sharded X (NEXT(3)): this rank holds p of the p_global variables; X v is
-  // summed over ranks (allreduce of the n-vector u) and so are the two dots.
-  if (p_global <= 0) p_global = p;
-  int launches = 0;
-  const int64_t nsplit = std::min<int64_t>(256, std::max<int64_t>(1, p / 256));
+// w = X (X^T u) / n for an n-vector u (ldk entries, zero past n): the Gram
+// operator of the samples, whose nonzero spectrum is that of S = X^T X / n
+// (L = sigma_max(S)). t: scratch of p doubles; part: nsplit x ldk.
+int launch_gram_apply(int dtype, const void* Xt, int64_t p, int64_t n, int64_t ldk,
+                      const double* u, double* t, double* part, int64_t nsplit, double* w,
+                      cudaStream_t st) {
+  if (p <= 0) {
+    cudaMemsetAsync(w, 0, ldk * sizeof(double), st);
+    return 0;
+  }
+  const unsigned g3 = (unsigned)((p + 7) / 8);
+  if (dtype == ACCORD_F64)
+    pi_xtu_kernel<double><<<g3, 256, 0, st>>>((const double*)Xt, p, ldk, n, u, t);
+  else
+    pi_xtu_kernel<float><<<g3, 256, 0, st>>>((const float*)Xt, p, ldk, n, u, t);
   const int64_t rows_per = (p + nsplit - 1) / nsplit;
-  double *v = nullptr, *w = nullptr, *u = nullptr, *part = nullptr, *dots = nullptr;
-  cudaError_t e = cudaSuccess;
-  e = cudaMallocAsync(&v, p * sizeof(double), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&w, p * sizeof(double), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&u, ldk * sizeof(double), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&part, nsplit * ldk * sizeof(double), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dots, 2 * sizeof(double), st);
-  if (e != cudaSuccess) {
-    *err = std::string("power iteration alloc: ") + cudaGetErrorString(e);
-    return -1;
-  }
-  fill_d<<<grid_for(p, 256), 256, 0, st>>>(v, p, 1.0 / std::sqrt((double)p_global));
-  ++launches;
-  double rq_prev = -1.0, rq = 0.0, h[2];
-  const int check_every = 10;
-  for (int it = 0; it < max_iter; ++it) {
-    dim3 g1((unsigned)((ldk + 255) / 256), (unsigned)nsplit);
-    if (dtype == ACCORD_F64)
-      pi_xv_kernel<double><<<g1, 256, 0, st>>>((const double*)Xt, p, ldk, rows_per, v, part);
-    else
-      pi_xv_kernel<float><<<g1, 256, 0, st>>>((const float*)Xt, p, ldk, rows_per, v, part);
-    pi_sum_parts<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(part, nsplit, ldk, u);
-    if (ar && !(*ar)(u, (int)ldk)) {
-      e = cudaErrorUnknown;
-      *err = "power iteration: allreduce failed";
-      break;
-    }
-    const unsigned g3 = (unsigned)((p + 7) / 8);
-    if (dtype == ACCORD_F64)
-      pi_xtu_kernel<double><<<g3, 256, 0, st>>>((const double*)Xt, p, ldk, n, u, w);
-    else
-      pi_xtu_kernel<float><<<g3, 256, 0, st>>>((const float*)Xt, p, ldk, n, u, w);
-    pi_dots<<<1, 1024, 0, st>>>(v, w, p, dots);
-    if (ar && !(*ar)(dots, 2)) {
-      e = cudaErrorUnknown;
-      *err = "power iteration: allreduce failed";
-      break;
-    }
-    pi_normalize<<<grid_for(p, 256), 256, 0, st>>>(w, p, dots, v);
-    launches += 5;
-    if ((it + 1) % check_every == 0 || it + 1 == max_iter) {
-      cudaMemcpyAsync(h, dots, sizeof(h), cudaMemcpyDeviceToHost, st);
-      e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) break;
-      rq = h[0];
-      if (rq_prev > 0 && std::fabs(rq - rq_prev) <= tol * rq) break;
-      rq_prev = rq;
-    }
-  }
-  if (e == cudaSuccess) {
-    cudaMemcpyAsync(h, dots, sizeof(h), cudaMemcpyDeviceToHost, st);
-    e = cudaStreamSynchronize(st);
-    rq = h[0];
-  }
-  cudaFreeAsync(v, st);
-  cudaFreeAsync(w, st);
-  cudaFreeAsync(u, st);
-  cudaFreeAsync(part, st);
-  cudaFreeAsync(dots, st);
-  if (e != cudaSuccess) {
-    if (err->empty()) *err = std::string("power iteration: ") + cudaGetErrorString(e);
-    return -1;
-  }
-  *L_host = rq;
-  return launches;
+  dim3 g1((unsigned)((ldk + 255) / 256), (unsigned)nsplit);
+  if (dtype == ACCORD_F64)
+    pi_xv_kernel<double><<<g1, 256, 0, st>>>((const double*)Xt, p, ldk, rows_per, t, part);
+  else
+    pi_xv_kernel<float><<<g1, 256, 0, st>>>((const float*)Xt, p, ldk, rows_per, t, part);
+  pi_sum_parts<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(part, nsplit, ldk, w);
+  return 3;
 }
 
 }  // namespace accord
