@@ -278,6 +278,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     const float gam = ep.gamma;
     const float* omv = (const float*)om.val;
     const uint32_t tempty_leader = tc::smem_u32(&tempty[0]);
+    const int64_t col_end = ep.col_end;
     // this warp's private pool chunk (warp-uniform); taken on first use
     long long chunk_id = -1;
     int64_t fill = pool.chunk;
@@ -355,21 +356,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           const uint32_t* v = v2[h];
           const int c0 = n0 + ch2 * 64 + h * 32;
           const int64_t sp0 = sp;
-          uint32_t mask = 0, sup = 0;
-          if (row_ok) {
-            // common case first: no |acc| in these 32 columns passes the fast
-            // test (one FMNMX per value instead of a compare + select + add)
-            float m0 = 0.f, m1 = 0.f;
-            if constexpr (kFast) {
+          // common case first, one vote per 32 columns: no lane has an |acc|
+          // above the tile's threshold (one FMNMX3 per two values), its
+          // diagonal or a support entry of Omega in these columns
+          float m0 = 0.f, m1 = 0.f;
+          if constexpr (kFast) {
 #pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
-                m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
-              }
-            } else {
-              m0 = INFINITY;
+            for (int c = 0; c < 32; c += 2) {
+              m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
+              m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
             }
-            if (fmaxf(m0, m1) > tfast) {
+          } else {
+            m0 = INFINITY;
+          }
+          const bool over = fmaxf(m0, m1) > tfast;
+          const bool hot = row_ok && (over || nxt < c0 + 32 || (gi >= c0 && gi < c0 + 32));
+          if (!__any_sync(0xffffffffu, hot)) continue;
+          uint32_t mask = 0, sup = 0;
+          if (hot) {
+            if (over) {
 #pragma unroll
               for (int c = 0; c < 32; ++c)
                 mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
@@ -396,11 +401,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               nxt = sp < se ? om.col[sp] : INT_MAX;
             }
             mask |= sup;
-            const int64_t left = ep.col_end - c0;                     // ragged p / slab
+            const int64_t left = col_end - c0;                        // ragged p / slab
             if (left < 32) mask &= left <= 0 ? 0u : ((1u << left) - 1u);
           }
-          // common case: no candidate in these 32 columns of the warp's 32 rows
-          // (one vote instead of a REDUX round trip)
           if (__ballot_sync(0xffffffffu, mask != 0u) == 0u) continue;
           const int cnt = __popc(mask);
           const int total = __reduce_add_sync(0xffffffffu, cnt);
