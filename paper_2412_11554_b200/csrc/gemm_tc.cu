@@ -331,29 +331,38 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
         continue;
       }
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      // TMEM -> registers 32 columns at a time, one load ahead: the next
+      // 32 columns are in flight while these are tested
+      uint32_t va[32], vb[32];
+      tc::tmem_ld32(tbase, va);
 #pragma unroll 1
       for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
-        uint32_t v2[2][32];
-        tc::tmem_ld32(tbase + ch2 * 64, v2[0]);
-        tc::tmem_ld32(tbase + ch2 * 64 + 32, v2[1]);
-        tc::tmem_ld_wait();
+        tc::tmem_ld_wait();                                   // va = columns 64 ch2 + [0, 32)
+        tc::tmem_ld32(tbase + ch2 * 64 + 32, vb);             // in flight: 64 ch2 + [32, 64)
         if (dbg >= 3) {   // diagnostics: 3 = TMEM reads only, 4 = reads + max test only
+          tc::tmem_ld_wait();
           if (dbg == 4) {   // the max test of both halves (kept alive by an opaque compare)
             float m0 = 0.f, m1 = 0.f;
 #pragma unroll
             for (int c = 0; c < 32; c += 2) {
-              m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v2[0][c])), fabsf(__uint_as_float(v2[0][c + 1]))));
-              m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v2[1][c])), fabsf(__uint_as_float(v2[1][c + 1]))));
+              m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(va[c])), fabsf(__uint_as_float(va[c + 1]))));
+              m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(vb[c])), fabsf(__uint_as_float(vb[c + 1]))));
             }
             if (__float_as_uint(fmaxf(m0, m1)) == 0x7f7ffff1u) pool.row[0] = 0;
-          } else if (v2[0][0] == 0xffffffffu && v2[1][31] == 0xffffffffu) {
+          } else if (va[0] == 0xffffffffu && vb[31] == 0xffffffffu) {
             pool.row[0] = 0;                  // keep the loads alive (never true)
           }
+          if (ch2 + 1 < BN / 64) tc::tmem_ld32(tbase + (ch2 + 1) * 64, va);
           continue;
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t* v = v2[h];
+          if (h == 1) {
+            tc::tmem_ld_wait();                               // vb ready
+            if (ch2 + 1 < BN / 64)                            // in flight: next 64 ch2 + [0, 32)
+              tc::tmem_ld32(tbase + (ch2 + 1) * 64, va);
+          }
+          const uint32_t* v = h ? vb : va;
           const int c0 = n0 + ch2 * 64 + h * 32;
           const int64_t sp0 = sp;
           // common case first, one vote per 32 columns: no lane has an |acc|
