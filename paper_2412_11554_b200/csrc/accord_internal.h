@@ -17,6 +17,19 @@ constexpr int kRowPad = 256;    // operand rows padded to the GEMM tile (M and N
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// Kernel attributes (dynamic shared-memory limits) are set once per device and
+// call site: `seen` holds one bit per device, set only AFTER the attributes
+// were applied, so a concurrent caller can at worst set them twice.
+inline int attr_device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 63;
+}
+inline bool attr_needed(const unsigned long long& seen) {
+  return !(seen & (1ull << attr_device_bit()));
+}
+inline void attr_done(unsigned long long& seen) { seen |= 1ull << attr_device_bit(); }
+
 // ---------------------------------------------------------------------------
 // Device-side views of the per-rank state (plain pointers, no ownership).
 // ---------------------------------------------------------------------------

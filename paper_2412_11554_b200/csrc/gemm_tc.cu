@@ -583,8 +583,8 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
     return nullptr;
   }
   cudaMemset(p->blk_sdmax, 0, (p_pad / BN) * sizeof(float2));
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_seen = 0;
+  if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(gemm_tc_kernel<0, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg<0, 3>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -593,7 +593,7 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                          (int)Cfg<1, 7>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<1, 6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg<1, 6>::kSmemBytes);
-    attr = true;
+    attr_done(attr_seen);
   }
   return p;
 }

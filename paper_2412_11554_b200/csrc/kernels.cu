@@ -973,13 +973,13 @@ int launch_rowsort(int64_t rows, const int64_t* ptr, uint64_t* keys, uint64_t* t
   if (rows <= 0) return 0;
   const int warps = 8;
   const size_t smem = (size_t)warps * kWarpSortMax * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_seen = 0;
+  if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(rowsort_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaFuncSetAttribute(rowsort_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(kBlockSortMax * sizeof(uint64_t)));
-    attr = true;
+    attr_done(attr_seen);
   }
   rowsort_warp_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, smem, st>>>(
       rows, ptr, keys, long_rows);
@@ -1066,13 +1066,13 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
   const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
   const size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_seen = 0;
+  if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(refine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     cudaFuncSetAttribute(refine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr = true;
+    attr_done(attr_seen);
   }
   if (dtype == ACCORD_F64)
     refine_kernel<double><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,

@@ -442,13 +442,13 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
   if (pk == 0) return 0;
   int stages = 0;
   const size_t smem = spmm_tma_smem(ldk, &stages);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_seen = 0;
+  if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(spmm_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          100 * 1024);
     cudaFuncSetAttribute(spmm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          100 * 1024);
-    attr = true;
+    attr_done(attr_seen);
   }
   const int consumers = (int)round_up(ldk / 8, 32);
   // persistent: exactly the resident blocks (items are dealt round-robin)
