@@ -15,6 +15,33 @@ namespace accord {
 constexpr int kKPad = 64;       // samples padded to a multiple of 64 (one 128-B bf16 TMA row)
 constexpr int kRowPad = 256;    // operand rows padded to the GEMM tile (M and N)
 
+#ifdef __CUDACC__
+// bf16 rounding of the filter GEMM's operands (hi = rn(x)); the filter bound
+// uses the residual x - hi of exactly this rounding (col_norms, the SpMM
+// epilogues), so the candidate set stays certified for any rounding here.
+// ACCORD_BF16_DROP = k (diagnostic builds only) rounds to 7 - k mantissa bits.
+#ifndef ACCORD_BF16_DROP
+#define ACCORD_BF16_DROP 0
+#endif
+__device__ __forceinline__ __nv_bfloat16 filter_bf16(float x) {
+#if ACCORD_BF16_DROP == 0
+  return __float2bfloat16_rn(x);
+#else
+  constexpr int s = 16 + ACCORD_BF16_DROP;
+  uint32_t u = __float_as_uint(x);
+  u += ((1u << (s - 1)) - 1) + ((u >> s) & 1u);
+  return __ushort_as_bfloat16((unsigned short)((u & ~((1u << s) - 1)) >> 16));
+#endif
+}
+__device__ __forceinline__ __nv_bfloat162 filter_bf16x2(float a, float b) {
+#if ACCORD_BF16_DROP == 0
+  return __floats2bfloat162_rn(a, b);
+#else
+  return __halves2bfloat162(filter_bf16(a), filter_bf16(b));
+#endif
+}
+#endif
+
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 // Kernel attributes (dynamic shared-memory limits) are set once per device and

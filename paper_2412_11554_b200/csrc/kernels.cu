@@ -95,8 +95,8 @@ __global__ void split_bf16_kernel(const float4* __restrict__ src, int64_t n4,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 v = src[i];
-    __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y);
-    __nv_bfloat162 h1 = __floats2bfloat162_rn(v.z, v.w);
+    __nv_bfloat162 h0 = filter_bf16x2(v.x, v.y);
+    __nv_bfloat162 h1 = filter_bf16x2(v.z, v.w);
     float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
     hi[2 * i] = h0;
     hi[2 * i + 1] = h1;
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const float y = (float)yt[v];
-          const __nv_bfloat16 h = __float2bfloat16_rn(y);
+          const __nv_bfloat16 h = filter_bf16(y);
           const float hf = __bfloat162float(h);
           Yhi[r * ldk + c + v] = h;
           if (Ylo) Ylo[r * ldk + c + v] = __float2bfloat16_rn(y - hf);
@@ -747,7 +747,7 @@ __global__ void col_norms_kernel(int64_t p, int64_t ldk, const float* __restrict
   double xx = 0, ee = 0;
   for (int64_t m = lane; m < ldk; m += 32) {
     const float x = Xt[k * ldk + m];
-    const double e = (double)x - (double)__bfloat162float(__float2bfloat16_rn(x));
+    const double e = (double)x - (double)__bfloat162float(filter_bf16(x));
     xx += (double)x * x;
     ee += e * e;
   }

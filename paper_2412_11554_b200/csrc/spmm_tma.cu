@@ -328,7 +328,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
           uint32_t hp[4], lp[4];
 #pragma unroll
           for (int v = 0; v < 8; v += 2) {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(yt[v], yt[v + 1]);
+            const __nv_bfloat162 h2 = filter_bf16x2(yt[v], yt[v + 1]);
             const float2 hf = __bfloat1622float2(h2);
             const __nv_bfloat162 l2 = __floats2bfloat162_rn(yt[v] - hf.x, yt[v + 1] - hf.y);
             hp[v / 2] = *reinterpret_cast<const uint32_t*>(&h2);
