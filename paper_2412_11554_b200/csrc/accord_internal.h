@@ -98,6 +98,10 @@ struct EpiParams {            // candidate rule of the fused epilogue (SURVEY P1
   const float2* col_sd;       // (||x_k|| + ||x_k - bf16(x_k)||, ||x_k - bf16(x_k)||)
   float gamma;                // accumulation-error factor
   int exact_cols;             // 1: re-test tile-test survivors with their own column's bound
+  // 1: Omega is exactly I on one rank (the first iteration of a solve), so
+  // G = X^T X / n is symmetric: only tiles with N-block >= M-block run, and an
+  // off-diagonal tile emits every survivor (i,k) also as (k,i) (BF16_FILTER)
+  int sym;
 };
 
 // ---------------------------------------------------------------------------

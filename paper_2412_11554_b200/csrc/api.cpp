@@ -151,6 +151,7 @@ struct accord_ctx {
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
+  bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   int32_t* row_nnz2 = nullptr;
   uint64_t *keys = nullptr, *keys_tmp = nullptr;
@@ -446,14 +447,15 @@ void grow(accord_ctx* c, int64_t cap, int64_t keep_nnz) {
   c->dfree(c->pool_w, oc * T);  c->pool_w = vals ? c->dalloc_bytes(cap * T) : nullptr;
   c->cap = cap;
   // chunking: the SIMT GEMM uses one chunk; the tcgen05 epilogue warps take
-  // private chunks of 1024..8192 entries (>= one 32x32 emission batch)
+  // private chunks of 2048..8192 entries (>= one emission batch: 32 rows x 32
+  // columns, twice that when the symmetric first GEMM mirrors its survivors)
   c->dfree(c->chunk_fill, c->nchunks * 8);
   if (c->gemm_warps == 0) {
     c->chunk = cap;
     c->nchunks = 1;
   } else {
     int64_t ch = 8192;
-    while (ch > 1024 && cap / ch < 4 * (int64_t)c->gemm_warps) ch >>= 1;
+    while (ch > 2048 && cap / ch < 4 * (int64_t)c->gemm_warps) ch >>= 1;
     c->chunk = ch;
     c->nchunks = std::max<int64_t>(1, cap / ch);
   }
@@ -489,6 +491,7 @@ void refresh_objective(accord_ctx* c) {
 
 // Y = Omega X^T for the current Omega into Y[cur] (+ row norms).
 void recompute_y(accord_ctx* c) {
+  c->omega_identity = false;   // every change of Omega comes through here
   c->items_of = nullptr;   // Omega's structure may have been replaced (warm start, path)
   spmm_all(c, c->om_ptr, c->om_col, c->om_val, nullptr, c->cur, nullptr, c->row_Y2);
 }
@@ -901,6 +904,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   // ---- Omega^{(0)} = I, Y^{(0)} = rows of X^T, f^{(0)} ----
   c->launches += launch_identity(c->dtype, c->pk, c->r0, c->om_ptr, c->om_col, c->om_val, c->st);
   recompute_y(c);
+  c->omega_identity = true;
   refresh_objective(c);
 }
 
@@ -1002,6 +1006,9 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     // fp32-accumulation term of the filter bound: (n/16 + 17) * 2^-22 * sum|y^ x^|
     ep.gamma = (float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
     ep.exact_cols = std::getenv("ACCORD_FILTER_EXACT") != nullptr;   // A-B diagnostic
+    // Omega = I on one rank: G = S is symmetric, half the tiles (ACCORD_GEMM_NOSYM: off)
+    ep.sym = c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && c->world == 1 &&
+             !c->sharded && c->r0 == 0 && c->pk == c->p && !std::getenv("ACCORD_GEMM_NOSYM");
     CK(cudaEventRecord(c->ev[1], S));
     const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
     auto gemm = [&](const void* xt, int bsel, int64_t v0, int64_t v1) {
@@ -1202,6 +1209,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   c->launches += launch_compact(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_wn, c->om_ptr,
                                 c->om_col, c->om_val, S);
   if (c->items_of == c->om_ptr) c->items_of = nullptr;   // Omega changed
+  c->omega_identity = false;
   TR(c, "compact");
   c->cur = nb;
   int64_t nnz_loc = 0;

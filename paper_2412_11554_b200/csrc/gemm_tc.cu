@@ -87,7 +87,9 @@ struct Sched {
   int num_m, num_n, GN, U;
   int full_groups, rem, spu, spu_last;
   long long units_full, units;
-  __device__ Sched(int nm, int nn, int gn, int u) : num_m(nm), num_n(nn), GN(gn), U(u) {
+  bool sym;   // upper triangle only (N-block >= M-block), see EpiParams::sym
+  __device__ Sched(int nm, int nn, int gn, int u, bool sy)
+      : num_m(nm), num_n(nn), GN(gn), U(u), sym(sy) {
     full_groups = num_n / GN;
     rem = num_n - full_groups * GN;
     spu = (GN + U - 1) / U;
@@ -116,23 +118,33 @@ struct Sched {
 };
 
 // Iterate this cluster's tiles in schedule order: for (TileIt it(...); it.ok; it.next())
+// (sym: the tiles below the diagonal are skipped identically by every role)
 struct TileIt {
   const Sched& S;
   long long u;
   int stride, m, n0, cnt, ni;
-  bool ok;
+  bool ok, start;
   __device__ TileIt(const Sched& s, int cluster, int nclusters)
       : S(s), u(cluster), stride(nclusters), ni(0) { load(); }
   __device__ void load() {
-    ok = u < S.units;
-    if (ok) S.unit(u, m, n0, cnt);
-    ni = 0;
+    for (;;) {
+      ok = u < S.units;
+      ni = 0;
+      start = true;
+      if (!ok) return;
+      S.unit(u, m, n0, cnt);
+      if (!S.sym) return;
+      if (n0 + cnt - 1 < m) { u += stride; continue; }   // whole unit below the diagonal
+      if (n0 < m) ni = m - n0;
+      return;
+    }
   }
   __device__ void next() {
+    start = false;
     if (++ni == cnt) { u += stride; load(); }
   }
   __device__ int n() const { return n0 + ni; }
-  __device__ bool unit_start() const { return ni == 0; }
+  __device__ bool unit_start() const { return start; }
 };
 
 template <int kMode, int kStagesT, bool kFast>
@@ -160,7 +172,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const Sched sched(num_m, num_n, group_n, unit_n);
+  const Sched sched(num_m, num_n, group_n, unit_n, kMode == 1 && ep.sym != 0);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&mA_hi);
@@ -414,7 +426,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             if (left < 32) mask &= left <= 0 ? 0u : ((1u << left) - 1u);
           }
           if (__ballot_sync(0xffffffffu, mask != 0u) == 0u) continue;
-          const int cnt = __popc(mask);
+          // sym, off-diagonal tile: each survivor (i,k) is also (k,i) (G = G^T;
+          // the bound on |acc_ik - G_ik| is one on |acc_ik - G_ki|)
+          const bool mirror = kMode == 1 && sched.sym && it.n() != it.m;
+          const int cnt = __popc(mask) << (mirror ? 1 : 0);
           const int total = __reduce_add_sync(0xffffffffu, cnt);
           int incl = cnt;
 #pragma unroll
@@ -447,7 +462,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                 pool.col[pos] = c0 + c;
               }
               ++pos;
+              if (mirror) {
+                if (writable) {
+                  pool.row[pos] = c0 + c;
+                  pool.col[pos] = (int32_t)r;
+                }
+                ++pos;
+                atomicAdd(&pool.row_cnt[c0 + c], 1);
+              }
             }
+            if (mirror) row_count -= cnt >> 1;   // row r gained only the direct half
           } else if (cnt) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) {

@@ -250,3 +250,39 @@ def test_paired_line_search_is_bitwise_sequential(p, n, lam, T, monkeypatch):
     assert max(t for _, t, _ in s1) >= 2          # rejected trials were exercised
     assert np.array_equal(c1.row_ptr, c0.row_ptr) and np.array_equal(c1.col, c0.col)
     assert np.array_equal(c1.val, c0.val)
+
+
+@pytest.mark.parametrize("p,n,lam,T", [(4000, 60, 0.3, 3), (700, 250, 0.1, 3), (257, 65, 0.08, 3),
+                                       (1100, 333, 0.02, 2)])
+def test_symmetric_first_gemm_matches_full(p, n, lam, T, monkeypatch):
+    """At Omega^(0) = I the gradient is S = X^T X / n (symmetric; PAPER.md:54-57,
+    Alg. 1 at t = 0), so the first GEMM runs only the tiles on and above the
+    diagonal and mirrors each filter survivor. The candidate set is a
+    different certified superset, the refine recomputes every value exactly,
+    so the iterates, tau schedule and objective are bitwise those of the full
+    GEMM (ACCORD_GEMM_NOSYM=1); ragged p (not a multiple of 256) included.
+    (Rows stay below one work item, 2048 candidates, so the extra zero-valued
+    candidates cannot regroup any partial sum.)"""
+    _cuda()
+    rng = np.random.default_rng(29 + p)
+    Xt = rng.standard_normal((p, n)).astype(np.float32)
+    Xt[1::3] += 0.6 * Xt[0::3][: Xt[1::3].shape[0]]      # correlated pairs: real off-diagonals
+    Xt -= Xt.mean(axis=1, keepdims=True)
+    inv_L = 1.0 / O.spectral_bound(Xt.astype(np.float64))
+    out = {}
+    for nosym in ("0", "1"):
+        if nosym == "1":
+            monkeypatch.setenv("ACCORD_GEMM_NOSYM", "1")
+        else:
+            monkeypatch.delenv("ACCORD_GEMM_NOSYM", raising=False)
+        with A.AccordSolver(torch.from_numpy(Xt).cuda(), lam, inv_L=inv_L,
+                            gemm=A.GEMM_BF16_FILTER) as s:
+            st = s.step(T)
+            out[nosym] = ([(x["tau"], x["trials"], x["f"], x["nnz"]) for x in st],
+                          st[0]["n_cand"], s.export_csr())
+    (s1, nc1, c1), (s0, nc0, c0) = out["0"], out["1"]
+    assert s1 == s0
+    assert s1[0][3] > p                          # off-diagonal support after iteration 1
+    assert nc1 >= s1[0][3] and nc0 >= s0[0][3]
+    assert np.array_equal(c1.row_ptr, c0.row_ptr) and np.array_equal(c1.col, c0.col)
+    assert np.array_equal(c1.val, c0.val)
