@@ -1,7 +1,7 @@
 """Parity at BASELINE.json's full sizes (configs 3, 4, 5, and the optional
 TCGA-shaped config 6 of SURVEY.md §8(d)), in the launch
 configuration bench.py times (default tensor-core path, L from the device
-power iteration, one GPU).
+Lanczos, one GPU).
 
 The full oracle is too slow at these sizes (2 p^2 n = 2e15 FLOP per iteration
 at config 5), so the checks are:

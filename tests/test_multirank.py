@@ -366,7 +366,7 @@ def test_sharded_x_ring_matches_replicated(key, gemm):
 
 @pytest.mark.gpu
 def test_sharded_x_power_iteration_refit_kkt_and_layout():
-    """Sharded mode end to end: L by the sharded power iteration (allreduce of
+    """Sharded mode end to end: L by the sharded Lanczos iteration (allreduce of
     X v), samples-major slabs, refit (refine ring) and the KKT certificate."""
     import torch
     if not torch.cuda.is_available():
@@ -435,7 +435,7 @@ def test_sharded_x_ring_config5_scale():
     holding half of X (2 GB) and passing slabs through the host transport,
     reproduce the replicated run's tau schedule, objective and Omega for the
     first iterations (GEMM ring of 2 x 1954 x 1954 tiles, refine and SpMM
-    rings, sharded power iteration)."""
+    rings, sharded Lanczos iteration)."""
     import torch
     if not torch.cuda.is_available():
         pytest.fail("CUDA not available on a -m gpu run")
