@@ -253,6 +253,18 @@ int launch_omega_stats(int dtype, int64_t pk, int64_t r0, const int64_t* ptr,
 // Fixed-order reduction of the per-row partials into out[8] =
 // {D2, dd, logd, Y2, l1, nnz, ncand, max candidates in a row}. Any pointer may
 // be NULL (-> 0).
+// line search from Omega = I (kernels.cu): T on C, row dots, per-trial norms, apply
+int launch_diag_t(int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                  const float* c_g, double lam, float* c_t, cudaStream_t st);
+int launch_diag_dots(int64_t pk, int64_t ldk, int64_t xrow0, const float* Xt, const float* Z,
+                     double* xx, double* xz, double* zz, cudaStream_t st);
+int launch_diag_trial(int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                      const float* c_w, const float* c_wn, double tau, const double* xx,
+                      const double* xz, const double* zz, double* row_Y2, double* row_D2,
+                      double* row_a, cudaStream_t st);
+int launch_diag_apply(int64_t pk, int64_t ldk, int64_t xrow0, const float* Xt, float* Y,
+                      __nv_bfloat16* Yhi, const double* row_a, double tau, float* row_A,
+                      float* row_B, cudaStream_t st);
 int launch_reduce_rows(int64_t pk, const double* row_D2, const double* row_dd,
                        const double* row_logd, const double* row_Y2, const double* row_l1,
                        const int32_t* row_nnz, const int64_t* c_ptr, double* out,

@@ -153,6 +153,7 @@ struct accord_ctx {
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
+  double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
   int32_t* row_nnz2 = nullptr;
   uint64_t *keys = nullptr, *keys_tmp = nullptr;
   int32_t *pool_row = nullptr, *pool_col = nullptr;
@@ -864,6 +865,10 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->row_l1_2 = c->dalloc<double>(c->pk);
   c->row_logd2 = c->dalloc<double>(c->pk);
   c->row_D2b = c->dalloc<double>(c->pk);
+  c->diag_xx = c->dalloc<double>(c->pk);   // line search from Omega = I
+  c->diag_xz = c->dalloc<double>(c->pk);
+  c->diag_zz = c->dalloc<double>(c->pk);
+  c->diag_a = c->dalloc<double>(c->pk);
   c->row_nnz2 = c->dalloc<int32_t>(c->pk);
   {
     const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
@@ -1112,6 +1117,27 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   const int nb = c->cur ^ 1;
   double tau = c->tau0;
   double r[8];
+  // From Omega = I every trial's Y+ is a_i(tau) x_i + tau z_i (kernels.cu,
+  // diag_t_kernel): one SpMM of T = S_lam(-G) off the diagonal, then O(p)
+  // per trial. Needs power-of-two tau (tau0, beta), where omega+ = tau t is
+  // exact. ACCORD_LS_NODIAG=1: plain trials.
+  auto pow2 = [](double v) { int e; return v > 0 && std::frexp(v, &e) == 0.5; };
+  const bool diag_ls = c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && !c->refit &&
+                       c->beta < 1.0 && pow2(c->tau0) && pow2(c->beta) &&
+                       !std::getenv("ACCORD_LS_NODIAG");
+  const int64_t xrow0 = c->sharded ? 0 : c->r0;   // X^T row of local row 0
+  if (diag_ls) {
+    CK(cudaEventRecord(c->ev[4], S));
+    c->launches += launch_diag_t(c->pk, c->r0, c->c_ptr, c->c_col, (const float*)c->c_g, lam,
+                                 (float*)c->c_wn2, S);
+    spmm_all(c, c->c_ptr, c->c_col, c->c_wn2, nullptr, nb, nullptr, c->row_Y2);   // Z -> Y[nb]
+    c->launches += launch_diag_dots(c->pk, c->ldk, xrow0, (const float*)c->Xt,
+                                    (const float*)c->Y[nb], c->diag_xx, c->diag_xz, c->diag_zz, S);
+    CK(cudaEventRecord(c->ev[5], S));
+    CK(cudaEventSynchronize(c->ev[5]));
+    st.ms_spmm += ev_ms(c, 4, 5);
+    TR(c, "diag_z");
+  }
   // One line-search pass: prox at ta (and at beta*ta when paired), SpMM, the
   // per-trial sums reduced and all-reduced into h_red[0..7] (and [8..15]).
   // Paired: the same gather pass also accumulates D' for beta*ta, so a
@@ -1131,7 +1157,11 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
                                  c->row_logd2, c->row_nnz2, S, pit);
     CK(cudaEventRecord(c->ev[5], S));
     TR(c, "prox");
-    if (paired) {
+    if (diag_ls) {
+      c->launches += launch_diag_trial(c->pk, c->r0, c->c_ptr, c->c_col, (const float*)c->c_w,
+                                       (const float*)c->c_wn, ta, c->diag_xx, c->diag_xz,
+                                       c->diag_zz, c->row_Y2, c->row_D2, c->diag_a, S);
+    } else if (paired) {
       if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
       c->launches += launch_spmm_tma(c->pk, c->ldk, c->c_ptr, c->c_col, (const float*)c->c_wn,
                                      (const float*)c->c_w, (const float*)c->Xt,
@@ -1165,7 +1195,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
       }
   };
   const bool pair_ok = c->pair_ls && c->tma_spmm && !c->sharded && c->beta < 1.0 &&
-                       c->ldk <= 8 * kSpmmPairMaxConsumers;
+                       c->ldk <= 8 * kSpmmPairMaxConsumers && !diag_ls;
   for (;;) {
     // a trial at or below the 1/L floor is accepted whatever the test says
     const bool paired = pair_ok && !(tau <= c->inv_L);
@@ -1205,6 +1235,9 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
     tau *= c->beta;
   }
   // ---------------- accept: Omega <- Omega+, Y <- Y+ ----------------
+  if (diag_ls)
+    c->launches += launch_diag_apply(c->pk, c->ldk, xrow0, (const float*)c->Xt, (float*)c->Y[nb],
+                                     c->Yhi[nb], c->diag_a, tau, c->row_A[nb], c->row_B[nb], S);
   c->launches += launch_scan_i32(c->row_nnz, c->om_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
   c->launches += launch_compact(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_wn, c->om_ptr,
                                 c->om_col, c->om_val, S);

@@ -1193,4 +1193,142 @@ int launch_gram_apply(int dtype, const void* Xt, int64_t p, int64_t n, int64_t l
   return 3;
 }
 
+// ---------------------------------------------------------------------------
+// Line search from Omega = I (the first iteration of a solve).
+// Off the diagonal omega_ik = 0, so prox gives omega+_ik(tau) =
+// S_{tau lam}(-tau g_ik) = tau t_ik with t_ik = S_lam(-g_ik): exactly, for a
+// power-of-two tau (the scaling commutes with every rounding in prox_kernel).
+// Hence Y+_i(tau) = a_i(tau) x_i + tau z_i with z = T X^T (T = off-diagonal
+// t), and every trial's ||Y+_i||^2 and ||D_i||^2 follow from three dot
+// products per row: one SpMM pass serves all trials of the iteration.
+// ---------------------------------------------------------------------------
+__global__ void diag_t_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
+                              const int32_t* __restrict__ c_col, const float* __restrict__ c_g,
+                              double lam, float* __restrict__ c_t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const int64_t gi = r0 + r;
+  for (int64_t e = c_ptr[r] + lane; e < c_ptr[r + 1]; e += 32) {
+    const double y = -(double)c_g[e];     // prox_kernel's y at tau = 1, omega = 0
+    const double m = fabs(y) - lam;
+    c_t[e] = (c_col[e] == gi || !(m > 0.0)) ? 0.f : (float)copysign(m, y);
+  }
+}
+
+// per row: ||x_i||^2, <x_i, z_i>, ||z_i||^2 (float64), warp per row
+__global__ void diag_dots_kernel(int64_t pk, int64_t ldk, int64_t xrow0,
+                                 const float* __restrict__ Xt, const float* __restrict__ Z,
+                                 double* __restrict__ xx, double* __restrict__ xz,
+                                 double* __restrict__ zz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const float4* x = reinterpret_cast<const float4*>(Xt + (xrow0 + r) * ldk);
+  const float4* z = reinterpret_cast<const float4*>(Z + r * ldk);
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int64_t m = lane; m < ldk / 4; m += 32) {
+    const float4 xv = x[m], zv = z[m];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double xd = vget(xv, v), zd = vget(zv, v);
+      a += xd * xd;
+      b += xd * zd;
+      c += zd * zd;
+    }
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  c = warp_sum(c);
+  if (lane == 0) {
+    xx[r] = a;
+    xz[r] = b;
+    zz[r] = c;
+  }
+}
+
+// one trial: a_i = omega+_ii(tau) from the prox output on C (diagonal always
+// in C), ||Y+_i||^2 and ||D_i||^2 = ||(a_i - omega_ii) x_i + tau z_i||^2
+__global__ void diag_trial_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
+                                  const int32_t* __restrict__ c_col,
+                                  const float* __restrict__ c_w, const float* __restrict__ c_wn,
+                                  double tau, const double* __restrict__ xx,
+                                  const double* __restrict__ xz, const double* __restrict__ zz,
+                                  double* __restrict__ row_Y2, double* __restrict__ row_D2,
+                                  double* __restrict__ row_a) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < pk;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = lower_bound_col(c_col, c_ptr[r], c_ptr[r + 1], (int32_t)(r0 + r));
+    const double a = c_wn[e], d = a - (double)c_w[e];
+    const double X2 = xx[r], XZ = xz[r], Z2 = zz[r];
+    row_Y2[r] = fmax(0.0, a * a * X2 + 2.0 * a * tau * XZ + tau * tau * Z2);
+    row_D2[r] = fmax(0.0, d * d * X2 + 2.0 * d * tau * XZ + tau * tau * Z2);
+    row_a[r] = a;
+  }
+}
+
+// the accepted trial: Y+_i = a_i x_i + tau z_i (in place over Z), the bf16
+// operand and the filter's row norms, as the SpMM epilogue writes them
+__global__ void diag_apply_kernel(int64_t pk, int64_t ldk, int64_t xrow0,
+                                  const float* __restrict__ Xt, float* __restrict__ Y,
+                                  __nv_bfloat16* __restrict__ Yhi,
+                                  const double* __restrict__ row_a, double tau,
+                                  float* __restrict__ row_A, float* __restrict__ row_B) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const double a = row_a[r];
+  const float* x = Xt + (xrow0 + r) * ldk;
+  float* y = Y + r * ldk;
+  double a2 = 0.0, b2 = 0.0;
+  for (int64_t m = lane; m < ldk; m += 32) {
+    const float v = (float)(a * (double)x[m] + tau * (double)y[m]);
+    y[m] = v;
+    const __nv_bfloat16 h = filter_bf16(v);
+    Yhi[r * ldk + m] = h;
+    const double e = (double)v - (double)__bfloat162float(h);
+    a2 += e * e;
+    b2 += (double)v * (double)v;
+  }
+  a2 = warp_sum(a2);
+  b2 = warp_sum(b2);
+  if (lane == 0) {
+    row_A[r] = __double2float_ru(sqrt(a2) * (1.0 + 1e-12));
+    row_B[r] = __double2float_ru(sqrt(b2) * (1.0 + 1e-12));
+  }
+}
+
+int launch_diag_t(int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                  const float* c_g, double lam, float* c_t, cudaStream_t st) {
+  if (pk == 0) return 0;
+  diag_t_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, r0, c_ptr, c_col, c_g, lam, c_t);
+  return 1;
+}
+
+int launch_diag_dots(int64_t pk, int64_t ldk, int64_t xrow0, const float* Xt, const float* Z,
+                     double* xx, double* xz, double* zz, cudaStream_t st) {
+  if (pk == 0) return 0;
+  diag_dots_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, ldk, xrow0, Xt, Z, xx, xz, zz);
+  return 1;
+}
+
+int launch_diag_trial(int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
+                      const float* c_w, const float* c_wn, double tau, const double* xx,
+                      const double* xz, const double* zz, double* row_Y2, double* row_D2,
+                      double* row_a, cudaStream_t st) {
+  if (pk == 0) return 0;
+  diag_trial_kernel<<<grid_for(pk, 256, 148 * 8), 256, 0, st>>>(
+      pk, r0, c_ptr, c_col, c_w, c_wn, tau, xx, xz, zz, row_Y2, row_D2, row_a);
+  return 1;
+}
+
+int launch_diag_apply(int64_t pk, int64_t ldk, int64_t xrow0, const float* Xt, float* Y,
+                      __nv_bfloat16* Yhi, const double* row_a, double tau, float* row_A,
+                      float* row_B, cudaStream_t st) {
+  if (pk == 0) return 0;
+  diag_apply_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, ldk, xrow0, Xt, Y, Yhi, row_a,
+                                                               tau, row_A, row_B);
+  return 1;
+}
+
 }  // namespace accord

@@ -286,3 +286,38 @@ def test_symmetric_first_gemm_matches_full(p, n, lam, T, monkeypatch):
     assert nc1 >= s1[0][3] and nc0 >= s0[0][3]
     assert np.array_equal(c1.row_ptr, c0.row_ptr) and np.array_equal(c1.col, c0.col)
     assert np.array_equal(c1.val, c0.val)
+
+
+@pytest.mark.parametrize("p,n,lam,tau0", [(1100, 333, 0.05, 4.0), (700, 250, 0.1, 0.5),
+                                          (4000, 60, 0.3, 1.0)])
+def test_first_iteration_line_search_from_identity(p, n, lam, tau0, monkeypatch):
+    """From Omega^(0) = I every trial of iteration 1 is
+    Y+_i = a_i(tau) x_i + tau z_i with one SpMM z = S_lam(-G) X^T (exact for
+    power-of-two tau, Eq. 3.5). Against the per-trial SpMM passes
+    (ACCORD_LS_NODIAG=1): the same tau schedule and trial counts; objective
+    and iterates equal to f32 rounding (z is stored in f32 before the
+    expansion, the plain pass rounds Y+ once from float64 accumulators, and
+    the later iterations start from Y that differ in the last bit)."""
+    _cuda()
+    rng = np.random.default_rng(41 + p)
+    Xt = rng.standard_normal((p, n)).astype(np.float32)
+    Xt[1::3] += 0.6 * Xt[0::3][: Xt[1::3].shape[0]]
+    Xt -= Xt.mean(axis=1, keepdims=True)
+    inv_L = 1.0 / O.spectral_bound(Xt.astype(np.float64))
+    out = {}
+    for nodiag in ("0", "1"):
+        if nodiag == "1":
+            monkeypatch.setenv("ACCORD_LS_NODIAG", "1")
+        else:
+            monkeypatch.delenv("ACCORD_LS_NODIAG", raising=False)
+        with A.AccordSolver(torch.from_numpy(Xt).cuda(), lam, inv_L=inv_L, tau0=tau0,
+                            gemm=A.GEMM_BF16_FILTER) as s:
+            st = s.step(4)
+            out[nodiag] = ([(x["tau"], x["trials"]) for x in st], [x["f"] for x in st],
+                           s.export_csr(), s.export_csr().to_dense(p))
+    (s1, f1, c1, d1), (s0, f0, c0, d0) = out["0"], out["1"]
+    assert s1 == s0
+    assert s1[0][1] >= 2 or tau0 <= 1.0          # rejected trials exercised where tau0 is large
+    np.testing.assert_allclose(f1, f0, rtol=1e-8, atol=0)
+    assert abs(len(c1.col) - len(c0.col)) <= max(2, len(c0.col) // 10000)
+    assert np.abs(d1 - d0).max() <= 1e-6 * np.abs(d0).max()
