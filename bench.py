@@ -5,20 +5,26 @@ iterations/s and effective TFLOP/s of Omega S at p = 1e6).
 
 One step = one accepted outer iteration of Algorithm 1:
 gradient GEMM + fused epilogue, candidate finalize + exact refine, all line-
-search trials (prox, SpMM, allreduce), compaction. N > 1: launched by torchrun,
-one rank per GPU, rows of Omega sharded (strong scaling of one problem; NCCL
-allreduce of 8 doubles per trial). Rank 0 prints ONE JSON line on stdout.
+search trials (prox, SpMM, allreduce), compaction. N > 1: one rank per GPU
+(launched by torchrun, or re-launched through torch.distributed.run by this
+script when WORLD_SIZE is unset), rows of Omega sharded (strong scaling of one
+problem; NCCL allreduce of 8-16 doubles per trial). Rank 0 prints ONE JSON
+line on stdout. X is generated once per node and shared through /dev/shm.
 
 --impl reference times the float64 oracle (oracle/accord_oracle.py) on the
-host cores on a bounded sample of the same workload (sampled-row replay,
-exact per-row Algorithm 1 given the step; PAPER.md:948-957 row separability),
-extrapolated to full iterations/s.
+host cores on a bounded sample of the same workload: Algorithm 1 on a sample
+of rows, every line-search trial evaluated, the sufficient-decrease test taken
+on the sample's sums (oracle.fbs_rows_ls), extrapolated to iterations/s of
+the full problem (x p / |R|). Our arm's cpu_baseline replays the GPU's own
+trial schedule on a row sample (oracle.fbs_rows with trial_taus).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,6 +39,7 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                   "sm_max_mhz": 1965.0}
+L2_BYTES = 126e6
 
 
 def log(*a):
@@ -84,7 +91,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        sm, smax, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in self.lines:
             parts = [x.strip() for x in l.split(",")]
@@ -93,6 +100,7 @@ class ClockSampler:
             try:
                 sm.append(float(parts[1]))
                 smax.append(float(parts[2]))
+                pw.append(float(parts[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, parts[5:9]):
@@ -100,57 +108,137 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
+                "power_w_median": statistics.median(pw) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# --------------------------------------------------------------------------- oracle
-def oracle_sample(Xt, lam, tau0, rows, steps):
-    """Time the oracle's exact per-row Algorithm 1 (row-replay mode) on a
-    bounded sample; returns seconds per full iteration (extrapolated)."""
-    from oracle import accord_oracle as O
-    from threadpoolctl import threadpool_info
-    times = []
-    Om0 = None
-    for s in range(steps):
-        t0 = time.perf_counter()
-        r = O.fbs_rows(Xt, rows, lam, [tau0], Omega0_rows=Om0)
-        times.append(time.perf_counter() - t0)
-        Om0 = r["Omega_rows"]
-    cores = 0
-    for d in threadpool_info():
-        cores = max(cores, int(d.get("num_threads", 0)))
-    p = Xt.shape[0]
-    per_iter = statistics.median(times) * p / len(rows)
-    return per_iter, cores or os.cpu_count(), times
+# --------------------------------------------------------------------------- inputs
+def _inputs_tag():
+    h = hashlib.sha256(open(os.path.join(ROOT, "accord_inputs", "__init__.py"), "rb").read())
+    return h.hexdigest()[:12]
 
 
-def cfg_problem(key):
+def cfg_problem(key, local_rank=0, local_world=1, barrier=None):
+    """The seeded X of BASELINE config `key`, generated once per node: local
+    rank 0 generates it and publishes it in /dev/shm (atomic rename), the
+    others map it read-only after `barrier` (a 4 GB X generated per rank would
+    cost ~40 s and ~20 GB of transient host memory each)."""
     from accord_inputs import get_config, make_problem
     cfg = get_config(key)
-    t0 = time.perf_counter()
-    pr = make_problem(cfg, with_blocks=False)
-    log(f"generated {cfg.name}: Xt {pr.Xt.shape} {pr.Xt.dtype} in "
-        f"{time.perf_counter() - t0:.1f}s")
-    return cfg, pr
+    shm = "/dev/shm"
+    path = os.path.join(shm, f"accord_{cfg.name}_{_inputs_tag()}_np{np.__version__}.npy")
+    Xt = None
+    if local_rank == 0:
+        if os.path.exists(path):
+            try:
+                Xt = np.load(path, mmap_mode="r")
+                log(f"inputs: mapped {path}")
+            except Exception:
+                Xt = None
+        if Xt is None:
+            t0 = time.perf_counter()
+            Xt = make_problem(cfg, with_blocks=False).Xt
+            log(f"generated {cfg.name}: Xt {Xt.shape} {Xt.dtype} in "
+                f"{time.perf_counter() - t0:.1f}s")
+            if local_world > 1 or Xt.nbytes > 256e6:
+                try:
+                    tmp = path + f".tmp{os.getpid()}"
+                    np.save(tmp, Xt)
+                    os.replace(tmp + ".npy" if not tmp.endswith(".npy") else tmp, path)
+                except Exception as e:
+                    log(f"inputs: /dev/shm publish failed ({e}); ranks generate their own")
+    if barrier is not None:
+        barrier()
+    if Xt is None:
+        try:
+            Xt = np.load(path, mmap_mode="r")
+        except Exception:
+            Xt = make_problem(cfg, with_blocks=False).Xt
+    return cfg, Xt
+
+
+def metric_name(cfg):
+    return f"prox-grad iterations/s (ACCORD-FBS, p={cfg.p}, n={cfg.n})"
+
+
+def workload_config(cfg, world, gemm, sharded=False, flushed=False):
+    xb = cfg.p * cfg.n * (8 if cfg.dtype == "f64" else 4)
+    if xb > L2_BYTES:
+        l2 = (f"inputs larger than L2 (X^T {xb / 1e9:.2f} GB {cfg.dtype} + bf16 copy vs "
+              f"126 MB L2)")
+    elif flushed:
+        l2 = (f"L2 flushed between steps (X^T {xb / 1e6:.0f} MB fits in L2; a 512 MB buffer "
+              f"is written on the stream before every timed step)")
+    else:
+        l2 = f"L2 warm (X^T {xb / 1e6:.0f} MB fits in L2; not flushed)"
+    return {"workload": cfg.name, "p": cfg.p, "n": cfg.n, "lambda": cfg.lambdas[0],
+            "tau0": cfg.tau0, "beta": cfg.beta, "x_dtype": cfg.dtype, "gemm": gemm,
+            "parallelism": f"row-block x{world} (X {'sharded, ring' if sharded else 'replicated'})",
+            "l2": l2}
+
+
+def all_host_cores():
+    """torchrun sets OMP_NUM_THREADS=1 per rank; the oracle legs run on rank 0
+    alone and get every host core."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([int(d.get("num_threads", 0)) for d in threadpool_info()] or [0]) or \
+            os.cpu_count()
+    except Exception:
+        return os.cpu_count()
 
 
 # --------------------------------------------------------------------------- reference arm
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, local_rank, local_world, barrier):
+    """The float64 oracle, as it stands, on the host cores: Algorithm 1 on a
+    seeded sample of rows with every trial evaluated (oracle.fbs_rows_ls),
+    W untimed iterations, then K timed ones; extrapolated x p / |R|."""
+    cfg, Xt = cfg_problem(args.config, local_rank, local_world, barrier)
     if rank != 0:
         return
-    cfg, pr = cfg_problem(args.config)
+    with all_host_cores():
+        _reference_rank0(args, world, cfg, Xt)
+
+
+def _reference_rank0(args, world, cfg, Xt):
+    from oracle import accord_oracle as O
     lam = cfg.lambdas[0]
     p = cfg.p
     rng = np.random.default_rng(7)
-    R = args.ref_rows
-    rows = np.sort(rng.choice(p, size=min(R, p), replace=False))
-    # warmup
-    for _ in range(max(0, args.warmup)):
-        oracle_sample(pr.Xt, lam, cfg.tau0, rows[:max(2, R // 8)], 1)
-    per_iter, cores, times = oracle_sample(pr.Xt, lam, cfg.tau0, rows, args.steps)
+    rows = np.sort(rng.choice(p, size=min(args.ref_rows, p), replace=False))
+    # 1/L as the GPU arm computes it (sigma_max(S), PAPER.md:240): the oracle's
+    # eigvalsh of the n x n Gram (n <= 2000 for every config)
+    t0 = time.perf_counter()
+    inv_L = 1.0 / O.spectral_bound(Xt)
+    t_L = time.perf_counter() - t0
+    Om = None
+    if args.warmup:
+        r = O.fbs_rows_ls(Xt, rows, lam, cfg.tau0, cfg.beta, inv_L, T=args.warmup)
+        Om = r["Omega_rows"]
+    times, taus, trials = [], [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = O.fbs_rows_ls(Xt, rows, lam, cfg.tau0, cfg.beta, inv_L, T=1, Omega0_rows=Om)
+        times.append(time.perf_counter() - t0)
+        Om = r["Omega_rows"]
+        taus.append(float(r["taus"][0]))
+        trials.append(int(r["trials"][0]))
+    per_iter = float(np.mean(times)) * p / len(rows)
     value = 1.0 / per_iter
-    sample = (f"{len(rows)} seeded rows of {cfg.name}, {args.steps} row-replay iterations "
-              f"(exact per-row Algorithm 1, float64), extrapolated x p/{len(rows)}")
+    cores = threads_used()
+    sample = (f"{len(rows)} seeded rows of {cfg.name}: Algorithm 1 on the rows (every "
+              f"line-search trial evaluated, the test on the sample's sums; "
+              f"oracle.fbs_rows_ls), {args.warmup} untimed + {args.steps} timed iterations, "
+              f"float64, mean time per iteration x p/{len(rows)} (extrapolated)")
     out = {
         "impl": "reference",
         "metric": metric_name(cfg), "value": value, "unit": "iterations/s",
@@ -158,30 +246,51 @@ def run_reference(args, rank, world):
         "ms_per_step": per_iter * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json recipe, seeded)",
-        "config": workload_config(cfg, world, "oracle (numpy/OpenBLAS host)"),
+        "config": workload_config(cfg, 1, "oracle (numpy/OpenBLAS host, float64)"),
         "effective_tflops": 2.0 * p * p * cfg.n * value / 1e12,
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores,
                          "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "iterate": {"tau": taus, "trials": trials},
+        "row_iteration_s": float(np.mean(times)) / len(rows),
+        "setup_s_L": t_L,
+        "fits_in_driver_run": False,
+        "note": "extrapolated: a full oracle iteration at this size would take "
+                f"{per_iter:.3g} s; only the sampled rows are computed",
     }
     print(json.dumps(out), flush=True)
 
 
-def metric_name(cfg):
-    return f"prox-grad iterations/s (ACCORD-FBS, p={cfg.p}, n={cfg.n})"
-
-
-def workload_config(cfg, world, gemm, sharded=False):
-    return {"workload": cfg.name, "p": cfg.p, "n": cfg.n, "lambda": cfg.lambdas[0],
-            "tau0": cfg.tau0, "beta": cfg.beta, "x_dtype": cfg.dtype, "gemm": gemm,
-            "parallelism": f"row-block x{world} (X {'sharded, ring' if sharded else 'replicated'})",
-            "l2": "inputs larger than L2 (X^T 4 GB f32 + bf16 copy vs 126 MB L2)"
-            if cfg.p * cfg.n * 4 > 126e6 else "L2 flushed between steps"}
+def cpu_baseline_leg(Xt, cfg, lam, stats_all, n_warm, args):
+    """The oracle replaying the GPU's own trial schedule (every trial paid
+    for, oracle.fbs_rows with trial_taus) on a seeded row sample: the warm-up
+    iterations untimed, then up to 5 of the timed ones."""
+    from oracle import accord_oracle as O
+    p = cfg.p
+    rng = np.random.default_rng(7)
+    rows = np.sort(rng.choice(p, size=min(args.cpu_rows, p), replace=False))
+    taus = [s["tau"] for s in stats_all]
+    tt = [[cfg.tau0 * cfg.beta ** j for j in range(s["trials"])] for s in stats_all]
+    Om = None
+    if n_warm:
+        Om = O.fbs_rows(Xt, rows, lam, taus[:n_warm], trial_taus=tt[:n_warm])["Omega_rows"]
+    k = min(5, len(taus) - n_warm)
+    t0 = time.perf_counter()
+    O.fbs_rows(Xt, rows, lam, taus[n_warm:n_warm + k], Omega0_rows=Om,
+               trial_taus=tt[n_warm:n_warm + k])
+    el = (time.perf_counter() - t0) / k
+    per_iter = el * p / len(rows)
+    return {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": threads_used(),
+            "kind": "oracle",
+            "sample": f"{len(rows)} seeded rows of {cfg.name}: row replay of the GPU's "
+                      f"iterations {n_warm + 1}..{n_warm + k} with its tau schedule and every "
+                      f"trial evaluated (oracle.fbs_rows, trial_taus), float64, "
+                      f"x p/{len(rows)} (extrapolated)"}
 
 
 # --------------------------------------------------------------------------- our arm
-def run_ours(args, rank, world, local_rank):
+def run_ours(args, rank, world, local_rank, local_world, barrier):
     import torch
     import paper_2412_11554_b200 as A
 
@@ -190,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    cfg, pr = cfg_problem(args.config)
+    cfg, Xt = cfg_problem(args.config, local_rank, local_world, barrier)
     lam = cfg.lambdas[0]
     p, n = cfg.p, cfg.n
     r0, r1 = A.partition_rows(p, world)[rank]
@@ -204,7 +313,7 @@ def run_ours(args, rank, world, local_rank):
     # --x-sharded (N > 1): each rank holds only its variables' slab of X and
     # every pass over X runs as a ring (Alg. 2); default: X replicated
     shard = bool(args.x_sharded and world > 1)
-    Xh_all = pr.Xt[r0:r1] if shard else pr.Xt
+    Xh_all = Xt[r0:r1] if shard else Xt
     skw = dict(x_sharded=True, p_global=p) if shard else {}
     Xd = torch.from_numpy(np.ascontiguousarray(Xh_all)).to(f"cuda:{dev}")
     t_setup = time.perf_counter()
@@ -215,8 +324,9 @@ def run_ours(args, rank, world, local_rank):
     t_setup = time.perf_counter() - t_setup
     del Xd
     info0 = solver.info()
-    log(f"rank {rank}: rows [{r0},{r1}) gemm={A.GEMM_NAMES[info0['gemm']]} L={info0['L']:.4f} "
-        f"setup {t_setup:.2f}s")
+    log(f"rank {rank}/{world}: rows [{r0},{r1}) gemm={A.GEMM_NAMES[info0['gemm']]} "
+        f"L={info0['L']:.4f} setup {t_setup:.2f}s nRanks={world}")
+    ws = []
     if args.warmup:
         ws = solver.step(args.warmup)
         log(f"rank {rank}: warmup taus {[s['tau'] for s in ws]} nnz {ws[-1]['nnz']} "
@@ -224,26 +334,58 @@ def run_ours(args, rank, world, local_rank):
     props = torch.cuda.get_device_properties(dev)
     sampler = ClockSampler(f"GPU-{props.uuid}" if getattr(props, "uuid", None) else dev)
     launches0 = solver.info()["kernel_launches"]
+    xbytes = p * n * (8 if cfg.dtype == "f64" else 4)
+    flush = xbytes <= L2_BYTES and not args.no_flush
+    flush_buf = torch.empty(int(512e6) // 4, dtype=torch.float32, device=f"cuda:{dev}") \
+        if flush else None
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    stats = solver.step(args.steps)
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    if not flush:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        stats = solver.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+    else:
+        # inputs fit in L2: flush it (write a 512 MB buffer) before every step,
+        # and time the steps only (events around each step on the same stream)
+        stats, ms = [], 0.0
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush_buf.fill_(float(len(stats)))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            stats += solver.step(1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
     if dist:
         dist.barrier()
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1)
     launches = solver.info()["kernel_launches"] - launches0
     ms_gemm = float(np.mean([s["ms_gemm"] for s in stats]))
+    per_rank = None
     if dist:
-        t = torch.tensor([ms, ms_gemm], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_gemm_max = float(t[0]), float(t[1])
+        mine = torch.tensor([ms, ms_gemm, float(sum(s["trials"] for s in stats)),
+                             float(np.mean([s["ms_spmm"] for s in stats])),
+                             float(np.mean([s["ms_refine"] for s in stats]))],
+                            dtype=torch.float64, device=f"cuda:{dev}")
+        allv = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allv, mine)
+        allv = [v.cpu().numpy().tolist() for v in allv]
+        per_rank = [{"rank": q, "ms": v[0], "ms_gemm": v[1], "trials": int(v[2]),
+                     "ms_spmm": v[3], "ms_refine": v[4]} for q, v in enumerate(allv)]
+        ms = max(v[0] for v in allv)
+        slow = max(range(world), key=lambda q: allv[q][0])
+        ms_gemm_max = max(v[1] for v in allv)
+        if rank == 0:
+            log("per-rank: " + " ".join(f"r{q}:{v[0]:.1f}ms(gemm {v[1]:.1f})"
+                                        for q, v in enumerate(allv)) + f" slowest r{slow}")
     else:
         ms_gemm_max = ms_gemm
     final = stats[-1]
@@ -277,8 +419,9 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(Xh_all.nbytes // args.steps),
                "d2h_bytes_per_step": int(d2h // args.steps),
                "note": "one solve through the C ABI from pinned host X: create (H2D copy, "
-                       "Lanczos for L, operand split) + K iterations + CSR export "
-                       "to host; bytes amortized per step"}
+                       "Lanczos for L, operand split) + K iterations from Omega = I + CSR "
+                       "export to host; bytes amortized per step; host wall clock, max over "
+                       "ranks"}
 
     if rank != 0:
         return
@@ -289,6 +432,10 @@ def run_ours(args, rank, world, local_rank):
     # the slowest rank's GEMM (max over ranks; rank 0's row block is the largest)
     achieved = 2.0 * pk0 * p * n / (ms_gemm_max / 1e3) / 1e12
     peak = float(pk_.get("bf16_tflops_sustained", pk_.get("bf16_tflops")))
+    # the same peak at the clock this run held (the measured sustained figure
+    # was taken at MEASURED_PEAKS' median clock under load)
+    ref_mhz = (pk_.get("clocks_under_load") or {}).get("sm_mhz_median")
+    peak_clk = peak * clocks["sm_mhz"] / ref_mhz if (ref_mhz and clocks.get("sm_mhz")) else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tf):
@@ -301,12 +448,8 @@ def run_ours(args, rank, world, local_rank):
             traffic = None
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rng = np.random.default_rng(7)
-        rows = np.sort(rng.choice(p, size=min(args.cpu_rows, p), replace=False))
-        per_iter, cores, _ = oracle_sample(pr.Xt, lam, cfg.tau0, rows, 2)
-        cpu = {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": cores, "kind": "oracle",
-               "sample": f"{len(rows)} seeded rows of {cfg.name}, 2 row-replay iterations "
-                         f"(exact per-row Algorithm 1, float64), extrapolated x p/{len(rows)}"}
+        with all_host_cores():
+            cpu = cpu_baseline_leg(Xt, cfg, lam, list(ws) + list(stats), len(ws), args)
     out = {
         "metric": metric_name(cfg), "value": value, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -314,14 +457,16 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "f32",
         "gemm_arith": "bf16 x bf16 -> fp32 TMEM (certified filter) + f64-accumulated refine",
         "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
-        "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]], shard),
+        "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]], shard, flush),
         "effective_tflops": flops_iter * value / 1e12,
         # whole step against the same peak (2 p_k p n / Peak / t_iter)
         "step_roofline_frac": flops_iter * value / 1e12 / peak,
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel<1> (bf16 filter + epilogue)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel<1,6,true> (bf16 filter + epilogue)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"bf16_tflops_sustained, {pdata}",
+                     "peak_at_run_clock": peak_clk,
+                     "frac_at_run_clock": achieved / peak_clk if peak_clk else None,
                      "algorithmic": f"2*p_k*p*n = {2.0 * pk0 * p * n:.3e} FLOP per launch",
                      "ms_per_launch": ms_gemm_max},
         "step_split_ms": {k: float(np.mean([s[k] for s in stats])) for k in
@@ -334,8 +479,17 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "setup_s": t_setup,
+        "per_rank": per_rank,
     }
     print(json.dumps(out), flush=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
@@ -347,16 +501,27 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=16)
-    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--no-flush", action="store_true",
+                    help="do not flush L2 between steps when X fits in L2")
+    ap.add_argument("--cpu-rows", type=int, default=64)
+    ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--x-sharded", action="store_true",
                     help="N > 1: shard X by variables (ring passes, NEXT(3)) instead of replicating")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: one rank per GPU through torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        log("spawning: " + " ".join(cmd))
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     if args.gpus != world and world > 1:
         log(f"--gpus {args.gpus} but WORLD_SIZE {world}: using WORLD_SIZE")
+    barrier = None
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -365,11 +530,12 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
         else:
             dist.init_process_group("gloo")
+        barrier = dist.barrier
     try:
         if args.impl == "reference":
-            run_reference(args, rank, world)
+            run_reference(args, rank, world, local_rank, local_world, barrier)
         else:
-            run_ours(args, rank, world, local_rank)
+            run_ours(args, rank, world, local_rank, local_world, barrier)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -285,6 +285,41 @@ accord_status accord_path(accord_ctx* ctx, const double* lambdas, int32_t k, int
                           double tol, double gamma, double* epbic, int64_t* nnz_off,
                           int32_t* iters, int32_t* best);
 
+/* lambda_max = max_{i != k} |S_ik|, S = X^T X / n, the top
+ * of the descending lambda grid of a path (§5.3, "an evenly spaced
+ * grid of lambda's in logarithmic scale"; SPEC.md
+ * lambda_grid). BF16_FILTER: the tensor-core gradient
+ * GEMM at Omega = I in max-reduce mode bounds it from below, a candidate pass
+ * at that bound keeps the maximiser, and the float64 refine makes the value
+ * exact for the f32 data; other kinds: float64 dot products on CUDA cores.
+ * Does not change the iterate. Collective. Errors: ACCORD_E_NUMERIC when
+ * lambda_max is 0 (all-zero or exactly uncorrelated data). */
+accord_status accord_lambda_max(accord_ctx* ctx, double* lambda_max);
+
+/* lambdas[j] = lambda_max * ratio^(j / (k-1)), j = 0..k-1: k log-evenly
+ * spaced values from lambda_max down to ratio * lambda_max (descending, the
+ * order accord_path expects). k >= 1, 0 < ratio < 1. Collective. */
+accord_status accord_lambda_grid(accord_ctx* ctx, int32_t k, double ratio, double* lambdas);
+
+/* DIAGNOSTIC (filter certification): run the gradient GEMM +
+ * fused epilogue + candidate finalize of the NEXT iteration exactly as
+ * accord_step would (same tiles, same bf16 operands, same thresholds, the
+ * symmetric schedule at Omega = I included), and additionally write the raw
+ * fp32 tensor-core accumulator acc_ik (~ n G_ik) of every (local row i,
+ * column k) to `acc` (device, row-major, ld >= p floats per row; every entry
+ * of the p_k x p block is written). Also returns (each may be NULL): y
+ * (device, p_k x n, row stride ldy) = the f32 Y = Omega X^T the GEMM's bf16 A
+ * operand was rounded from; row_ab (host, 2 p_k floats) = ||y_i - bf16(y_i)||
+ * then ||y_i||; col_sd (host, 2 p floats, interleaved) = (||x_k|| +
+ * ||x_k - bf16(x_k)||, ||x_k - bf16(x_k)||); gamma = the accumulation factor;
+ * and the candidate set C (host CSR, sorted columns, two-call convention as
+ * accord_export_csr: *n_cand = |C|, ACCORD_E_CAPACITY if capacity < |C|).
+ * The iterate is not changed. BF16_FILTER contexts only (else
+ * ACCORD_E_UNSUPPORTED). */
+accord_status accord_filter_audit(accord_ctx* ctx, float* acc, int64_t ld, float* y, int64_t ldy,
+                                  float* row_ab, float* col_sd, double* gamma, int64_t* c_ptr,
+                                  int32_t* c_col, int64_t capacity, int64_t* n_cand);
+
 /* Per-row line-search summands of the LAST trial evaluated by accord_step
  * (||D_i||^2, ||Delta_i||^2, i = local row indices). For sampled-row parity. */
 accord_status accord_row_stats(accord_ctx* ctx, const int64_t* rows, int64_t count,

@@ -38,9 +38,9 @@ import numpy as np
 
 __all__ = [
     "prox_diag", "soft_threshold", "prox", "g_value", "objective", "gradient",
-    "spectral_bound", "kkt_residual", "fbs", "fbs_rows", "candidate_set",
+    "spectral_bound", "kkt_residual", "fbs", "fbs_rows", "fbs_rows_ls", "candidate_set",
     "penalty_matrix", "epbic", "fit_path", "omega_to_theta", "theta_to_omega",
-    "partial_correlations",
+    "partial_correlations", "lambda_max", "lambda_grid",
 ]
 
 
@@ -240,11 +240,16 @@ def fbs(Xt, lam, tau0=0.5, beta=0.5, inv_L=None, T=10, Omega0=None,
                 ncand=np.array(ncand), nnz=np.array(nnz))
 
 
-def fbs_rows(Xt, rows, lam, taus, Omega0_rows=None, chunk=16384):
+def fbs_rows(Xt, rows, lam, taus, Omega0_rows=None, chunk=16384, trial_taus=None):
     """Sampled-row replay: evolve rows R of Omega
     independently with a given step schedule tau_t. Exact because f separates
     over rows, f = sum_i [-log w_ii + (1/2n)||X w_i^T||^2 + lam ||w_i||_1]
      and Algorithm 1 couples rows only through tau_t.
+
+    trial_taus[t] (optional) lists every step size the line search of
+    iteration t evaluated, the accepted taus[t] last: the rejected trials are
+    evaluated too (forward step, prox, Delta X^T) and
+    discarded, so that a timing of the replay pays for every trial.
 
     Returns the final rows (|R| x p) and, per iteration, the per-row summands
     ||D_i||^2 and ||Delta_i||^2 of the line-search test."""
@@ -256,9 +261,15 @@ def fbs_rows(Xt, rows, lam, taus, Omega0_rows=None, chunk=16384):
     else:
         Om[:] = Omega0_rows
     dsum, ddsum, margins = [], [], None
-    for tau in taus:
+    for t, tau in enumerate(taus):
         Y = _times_xt(Om, Xt, chunk)                # rows of Omega X^T
         G = _y_times_x(Y, Xt, chunk) / n            # rows of (1/n) Y X
+        if trial_taus is not None:
+            assert trial_taus[t][-1] == tau
+            for tr in trial_taus[t][:-1]:           # rejected trials (evaluated, discarded)
+                Zr = Om - tr * G
+                Dr = _times_xt(prox(Zr, tr, lam, rows) - Om, Xt, chunk)
+                float((Dr * Dr).sum())
         Z = Om - tau * G
         On = prox(Z, tau, lam, rows)
         Delta = On - Om
@@ -271,6 +282,45 @@ def fbs_rows(Xt, rows, lam, taus, Omega0_rows=None, chunk=16384):
         Om = On
     return dict(Omega_rows=Om, D2=np.array(dsum), Delta2=np.array(ddsum),
                 margins=margins)
+
+
+def fbs_rows_ls(Xt, rows, lam, tau0=0.5, beta=0.5, inv_L=None, T=1, Omega0_rows=None,
+                chunk=16384):
+    """Algorithm 1 restricted to the rows R, with the
+    backtracking test ||Delta X^T||_F^2 / n <= ||Delta||_F^2 / tau (reading
+    R8) or tau <= 1/L evaluated on those rows' sums only. With R = all rows
+    this IS Algorithm 1 (the sums are the global ones; pinned against fbs);
+    with a sample of rows the test is an estimate of the global one. Used by
+    bench.py's reference arm to time the oracle on a bounded sample of the
+    workload with every line-search trial paid for.
+
+    Returns the rows, the accepted taus and the trial counts."""
+    rows = np.asarray(rows, dtype=np.int64)
+    p, n = Xt.shape
+    if inv_L is None:
+        inv_L = 1.0 / spectral_bound(Xt)
+    Om = np.zeros((len(rows), p))
+    if Omega0_rows is None:
+        Om[np.arange(len(rows)), rows] = 1.0
+    else:
+        Om[:] = Omega0_rows
+    taus, trials = [], []
+    for t in range(T):
+        Y = _times_xt(Om, Xt, chunk)
+        G = _y_times_x(Y, Xt, chunk) / n
+        tau, k = tau0, 0
+        while True:
+            k += 1
+            On = prox(Om - tau * G, tau, lam, rows)
+            Delta = On - Om
+            D = _times_xt(Delta, Xt, chunk)
+            if float((D * D).sum()) / n <= float((Delta * Delta).sum()) / tau or tau <= inv_L:
+                break
+            tau *= beta
+        Om = On
+        taus.append(tau)
+        trials.append(k)
+    return dict(Omega_rows=Om, taus=np.array(taus), trials=np.array(trials))
 
 
 def _times_xt(A, Xt, chunk):
@@ -306,6 +356,25 @@ def epbic(Omega, Xt, gamma=0.5):
     loss = -np.log(np.diag(Omega)).sum() + g_value(Omega, Xt)
     k = int((Omega != 0).sum() - np.count_nonzero(np.diag(Omega)))
     return float(2 * n * loss + k * np.log(n) + 4 * gamma * k * np.log(p))
+
+
+def lambda_max(Xt):
+    """lambda_max = max_{i != k} |S_ik|, S = X^T X / n: the
+    top of the lambda grid of a path (SPEC.md lambda_grid)."""
+    Xt = np.asarray(Xt, dtype=np.float64)
+    S = (Xt @ Xt.T) / Xt.shape[1]
+    np.fill_diagonal(S, 0.0)
+    return float(np.abs(S).max())
+
+
+def lambda_grid(Xt, k, ratio):
+    """k lambdas evenly spaced in log scale from lambda_max down to
+    ratio * lambda_max ("an evenly spaced grid of lambda's
+    in logarithmic scale"; SPEC.md lambda_grid)."""
+    lm = lambda_max(Xt)
+    if k == 1:
+        return np.array([lm])
+    return lm * ratio ** (np.arange(k) / (k - 1))
 
 
 def fit_path(Xt, lambdas, tau0=0.5, beta=0.5, inv_L=None, tol=1e-6, max_iter=500,

@@ -21,6 +21,8 @@ LIB_PATH = os.environ.get("ACCORD_LIB") or os.path.join(HERE, "libaccord.so")   
 OK = 0
 STATUS = {0: "ok", 1: "invalid", 2: "cuda", 3: "nccl", 4: "capacity", 5: "numeric",
           6: "domain", 7: "nomem", 8: "unsupported", 9: "comm"}
+(E_INVALID, E_CUDA, E_NCCL, E_CAPACITY, E_NUMERIC, E_DOMAIN, E_NOMEM, E_UNSUPPORTED,
+ E_COMM) = range(1, 10)
 LAYOUT_SAMPLES, LAYOUT_VARIABLES = 0, 1
 F32, F64 = 0, 1
 GEMM_AUTO, GEMM_BF16X3, GEMM_SIMT, GEMM_BF16_FILTER = 0, 1, 2, 3
@@ -107,7 +109,8 @@ EXPORTED = ["accord_default_params", "accord_create", "accord_step", "accord_obj
             "accord_get_info", "accord_nccl_unique_id", "accord_destroy",
             "accord_status_string", "accord_last_error", "accord_abi_version",
             "accord_set_lambda", "accord_refit", "accord_solve", "accord_kkt_residual",
-            "accord_path", "accord_export_transformed"]
+            "accord_path", "accord_export_transformed", "accord_lambda_max",
+            "accord_lambda_grid", "accord_filter_audit"]
 
 
 def lib():
@@ -142,6 +145,11 @@ def lib():
     L.accord_path.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double,
                               C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                               C.POINTER(C.c_int32)]
+    L.accord_lambda_max.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.accord_lambda_grid.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_void_p]
+    L.accord_filter_audit.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_void_p,
+                                      C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
     L.accord_nccl_unique_id.argtypes = [C.c_void_p]
     L.accord_destroy.argtypes = [C.c_void_p]
     L.accord_destroy.restype = None
@@ -372,6 +380,45 @@ class AccordSolver:
                                  float(gamma), e.ctypes.data, nz.ctypes.data, it.ctypes.data,
                                  C.byref(best)), self.ctx)
         return dict(epbic=e, nnz_off=nz, iters=it, best=best.value)
+
+    def lambda_max(self):
+        """max_{i != k} |S_ik| on the device (accord_lambda_max, NEXT(2))."""
+        v = C.c_double()
+        _check(lib().accord_lambda_max(self.ctx, C.byref(v)), self.ctx)
+        return v.value
+
+    def lambda_grid(self, k, ratio):
+        """k log-spaced lambdas from lambda_max down to ratio * lambda_max."""
+        out = np.zeros(int(k))
+        _check(lib().accord_lambda_grid(self.ctx, int(k), float(ratio), out.ctypes.data),
+               self.ctx)
+        return out
+
+    def filter_audit(self):
+        """Diagnostic: the next GEMM's raw fp32 accumulator (torch, device),
+        Y, the filter's row / column constants, gamma and the candidate set C
+        (accord_filter_audit)."""
+        import torch
+        pk = self.row_end - self.row_begin
+        dev = torch.device("cuda", torch.cuda.current_device())
+        acc = torch.full((pk, self.p), float("nan"), dtype=torch.float32, device=dev)
+        y = torch.empty((pk, self.n), dtype=torch.float32, device=dev)
+        ab = np.zeros(2 * pk, dtype=np.float32)
+        sd = np.zeros(2 * self.p, dtype=np.float32)
+        gam = C.c_double()
+        nc = C.c_int64()
+        L = lib()
+        _check(L.accord_filter_audit(self.ctx, acc.data_ptr(), self.p, None, 0, None, None, None,
+                                     None, None, 0, C.byref(nc)), self.ctx)
+        acc.fill_(float("nan"))
+        rp = np.zeros(pk + 1, dtype=np.int64)
+        col = np.zeros(max(1, nc.value), dtype=np.int32)
+        _check(L.accord_filter_audit(self.ctx, acc.data_ptr(), self.p, y.data_ptr(), self.n,
+                                     ab.ctypes.data, sd.ctypes.data, C.byref(gam),
+                                     rp.ctypes.data, col.ctypes.data, nc.value, C.byref(nc)),
+               self.ctx)
+        return dict(acc=acc, y=y, row_A=ab[:pk], row_B=ab[pk:], col_s=sd[0::2], col_d=sd[1::2],
+                    gamma=gam.value, c_ptr=rp, c_col=col[:nc.value])
 
     def row_stats(self, rows):
         r = np.ascontiguousarray(rows, dtype=np.int64)

@@ -102,6 +102,13 @@ struct EpiParams {            // candidate rule of the fused epilogue (SURVEY P1
   // G = X^T X / n is symmetric: only tiles with N-block >= M-block run, and an
   // off-diagonal tile emits every survivor (i,k) also as (k,i) (BF16_FILTER)
   int sym;
+  // diagnostics / NEXT(2) (nullptr in the product path): audit_acc != NULL
+  // writes every raw fp32 accumulator (row-major, audit_ld floats per local
+  // row) besides the normal emission; max_out != NULL emits nothing and
+  // atomically raises *max_out (float bits) to max_{i != k} (|acc_ik| - n delta)
+  float* audit_acc;
+  int64_t audit_ld;
+  unsigned int* max_out;
 };
 
 // ---------------------------------------------------------------------------
@@ -242,6 +249,19 @@ int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const in
                const void* c_g, const void* c_w, double lam, double* row_max, double* out,
                cudaStream_t st);
 
+// lambda_max (NEXT(2)): filter row constants of A = rows of X^T (Omega = I);
+// max |c_g| over the off-diagonal entries of C -> *out; direct max over
+// columns [v0, v1) of |<x_i, x_k>| / n (CUDA cores; out may be NULL: ring steps
+// accumulate into row_max with accumulate = 1, then launch once more or reduce).
+int launch_row_ab(int64_t pk, int64_t ldk, const float* Xt_rows, float* row_A, float* row_B,
+                  cudaStream_t st);
+int launch_cand_offdiag_max(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr,
+                            const int32_t* c_col, const void* c_g, double* row_max, double* out,
+                            cudaStream_t st);
+int launch_gram_offdiag_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
+                            const void* Xi, const void* Xt, int64_t v0, int64_t v1, int accumulate,
+                            double* row_max, double* out, cudaStream_t st);
+
 // Per-column constants of the filter bound from Xt (f32).
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st);
 
@@ -295,6 +315,10 @@ void tc_plan_destroy(TcGemmPlan*);
 // per-256-column maxima of the filter's column constants (after launch_col_norms)
 int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st);
 int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs
+// A operand idx 2 = this rank's rows of X^T_hi (the Omega = I operand of the
+// lambda_max pass); rows_pad rows from `hi`
+bool tc_plan_set_a(TcGemmPlan* plan, int idx, const __nv_bfloat16* hi, int64_t rows_pad,
+                   std::string* err);
 // B operand idx 1/2 = ring buffers of the sharded mode (rows_pad x ldk bf16)
 bool tc_plan_set_b(TcGemmPlan* plan, int idx, const __nv_bfloat16* hi, const __nv_bfloat16* lo,
                    int64_t rows_pad, std::string* err);

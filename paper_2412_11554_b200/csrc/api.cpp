@@ -174,6 +174,9 @@ struct accord_ctx {
   unsigned long long* h_seg = nullptr;     // pinned [2]: chunks handed out, chunk_fill[0]
   TcGemmPlan* plan = nullptr;
   cudaEvent_t ev[8] = {};
+  float* audit_acc = nullptr;              // accord_filter_audit (diagnostic)
+  int64_t audit_ld = 0;
+  bool plan_a_x = false;                   // plan A map 2 = X^T_hi rows (lambda_max)
 
   // bias-correction refit (Eq. 3.8): fixed support S_hat, penalty phi * lambda
   bool refit = false;
@@ -402,19 +405,21 @@ void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void*
   });
 }
 
-// Exact candidate values c_g = (1/n) <Y_i, X_k> over all of X.
-void refine_all(accord_ctx* c) {
+// Exact candidate values c_g = (1/n) <Y_i, X_k> over all of X (Y = the
+// current Y buffer, or `yrows` = the rank's rows of X^T for lambda_max).
+void refine_all(accord_ctx* c, const void* yrows = nullptr) {
+  const void* Y = yrows ? yrows : c->Y[c->cur];
   if (!c->sharded) {
     // hub rows (up to ~1.6e5 candidates) split over several blocks
     if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
-    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
-                                 c->Y[c->cur], c->Xt, c->c_g, c->st, 0, INT64_MAX, c->itm_ptr,
-                                 c->n_items, kItemEntries, c->item_row);
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
+                                 c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
+                                 kItemEntries, c->item_row);
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
-    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col,
-                                 c->Y[c->cur], slab, c->c_g, c->st, v0, v1);
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, slab,
+                                 c->c_g, c->st, v0, v1);
   });
 }
 
@@ -598,7 +603,23 @@ double lanczos_lmax(accord_ctx* c, int64_t pv) {
   double* t = c->dalloc<double>(std::max<int64_t>(pv, 1));
   double* part = c->dalloc<double>(nsplit * N);
   std::vector<double> Q((size_t)(mmax + 1) * N, 0.0), a(mmax), b(mmax), wv(N);
-  for (int64_t i = 0; i < c->n; ++i) Q[i] = 1.0 / std::sqrt((double)c->n);
+  // start vector: seeded pseudo-random (splitmix64), not the constant vector,
+  // which X X^T / n maps to 0 when the columns of X are centered exactly
+  {
+    double nrm = 0.0;
+    uint64_t z = 0x9E3779B97F4A7C15ull;
+    for (int64_t i = 0; i < c->n; ++i) {
+      z += 0x9E3779B97F4A7C15ull;
+      uint64_t x = z;
+      x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+      x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+      x ^= x >> 31;
+      Q[i] = (double)(x >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+      nrm += Q[i] * Q[i];
+    }
+    nrm = std::sqrt(nrm);
+    for (int64_t i = 0; i < c->n; ++i) Q[i] /= nrm;
+  }
   double theta = 0.0, prev = -1.0;
   for (int j = 0; j < mmax; ++j) {
     CK(cudaMemcpyAsync(u, &Q[(size_t)j * N], N * 8, cudaMemcpyHostToDevice, c->st));
@@ -779,7 +800,11 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     // passes over X at c5, Lanczos ~50), then a safety inflation: a Ritz value
     // approaches L from below, and overestimating L is safe.
     c->L = lanczos_lmax(c, pv) * (1.0 + 2e-3);
-    c->inv_L = c->L > 0 ? 1.0 / c->L : 1e300;
+    // L = 0 only for X = 0 (S = 0); any other non-positive or non-finite
+    // estimate would silently disable the tau <= 1/L floor of Alg. 1
+    if (!(c->L > 0) || !std::isfinite(c->L))
+      throw Fail{ACCORD_E_NUMERIC, "sigma_max(S) estimate is not positive (X = 0?); pass inv_L"};
+    c->inv_L = 1.0 / c->L;
   }
 
   // ---- operands ----
@@ -964,13 +989,25 @@ float ev_ms(accord_ctx* c, int a, int b) {
 
 double lam_eff(const accord_ctx* c) { return c->refit ? c->phi * c->lam : c->lam; }
 
+// Operands of a gradient pass other than the current iterate's (lambda_max:
+// A = the rank's rows of X^T, i.e. Omega = I, with an empty support).
+struct GradOverride {
+  int ybuf;                 // plan A map
+  const float *row_A, *row_B;
+  OmegaView om;
+  double lam_cand;
+  unsigned int* max_out;    // != NULL: max-reduce pass only (no candidates)
+  const void* yrows;        // f32/f64 rows for the refine
+  bool sym;
+};
+
 // Candidate set C with exact gradient values G on it and the current omega:
 // either the GEMM + fused epilogue + finalize (+ refine) of a plain iteration,
 // or, for the bias-correction refit (Eq. 3.8), the fixed support S_hat with G
 // from the SDDMM (entries off S_hat carry an infinite penalty and stay 0).
-void build_candidates(accord_ctx* c, accord_iter_stats& st) {
+void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* ov = nullptr) {
   cudaStream_t S = c->st;
-  if (c->refit) {
+  if (c->refit && !ov) {
     CK(cudaEventRecord(c->ev[1], S));
     CK(cudaEventRecord(c->ev[2], S));
     CK(cudaMemcpyAsync(c->c_ptr, c->refit_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, S));
@@ -1014,19 +1051,33 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
     // Omega = I on one rank: G = S is symmetric, half the tiles (ACCORD_GEMM_NOSYM: off)
     ep.sym = c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && c->world == 1 &&
              !c->sharded && c->r0 == 0 && c->pk == c->p && !std::getenv("ACCORD_GEMM_NOSYM");
+    ep.audit_acc = c->audit_acc;
+    ep.audit_ld = c->audit_ld;
+    OmegaView omv = omega_view(c);
+    int ybuf = c->cur;
+    if (ov) {
+      ybuf = ov->ybuf;
+      ep.row_A = ov->row_A;
+      ep.row_B = ov->row_B;
+      ep.lam_cand = ov->lam_cand;
+      ep.max_out = ov->max_out;
+      ep.sym = ov->sym;
+      ep.audit_acc = nullptr;
+      omv = ov->om;
+    }
     CK(cudaEventRecord(c->ev[1], S));
     const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
     auto gemm = [&](const void* xt, int bsel, int64_t v0, int64_t v1) {
       ep.col_base = v0;
       ep.col_end = v1;
       if (tc) {
-        const int l = launch_gemm_tc(c->plan, c->gemm, c->cur, bsel, c->sm_count, ep,
-                                     omega_view(c), pool_view(c), S);
+        const int l = launch_gemm_tc(c->plan, c->gemm, ybuf, bsel, c->sm_count, ep, omv,
+                                     pool_view(c), S);
         if (l < 0) throw Fail{ACCORD_E_CUDA, "tcgen05 GEMM launch failed"};
         c->launches += l;
       } else {
-        c->launches += launch_gemm_simt(c->dtype, c->Y[c->cur], xt, c->ldk, c->ldk, ep,
-                                        omega_view(c), pool_view(c), S);
+        c->launches += launch_gemm_simt(c->dtype, c->Y[c->cur], xt, c->ldk, c->ldk, ep, omv,
+                                        pool_view(c), S);
       }
       c->gemm_launches++;
     };
@@ -1047,6 +1098,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
       c->h_seg[1] = used;
     }
     st.ms_gemm += ev_ms(c, 1, 2);
+    if (ov && ov->max_out) return;   // max-reduce pass: no candidates
     // overflow: SIMT counts entries in chunk_fill[0]; tcgen05 counts chunks
     const int64_t need = c->gemm_warps == 0 ? (int64_t)c->h_seg[0]
                                             : (int64_t)c->h_seg[1] * c->chunk;
@@ -1090,14 +1142,15 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st) {
                          nullptr, nullptr};
       pit = &pitems;
     }
-    c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
-                                 c->om_val, c->c_w, S, pit);
+    if (!ov)
+      c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
+                                   c->om_val, c->c_w, S, pit);
   }
   CK(cudaEventRecord(c->ev[3], S));
   TR(c, "finalize");
   if (c->gemm == ACCORD_GEMM_BF16_FILTER) {
     // exact values of the filtered candidates: G_ik = <Y_i, X_k> / n (f64 accumulation)
-    refine_all(c);
+    refine_all(c, ov ? ov->yrows : nullptr);
   }
   CK(cudaEventRecord(c->ev[4], S));
   TR(c, "refine");
@@ -1270,6 +1323,86 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   TR_flush(c);
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
   if (s) *s = st;
+}
+
+// lambda_max = max_{i != k} |S_ik| (SPEC.md
+// lambda_grid), global (collective). BF16_FILTER: the gradient GEMM at
+// Omega = I (A = the rank's rows of X^T_hi) in max-reduce mode gives a
+// certified lower bound m on n lambda_max (max over entries of |acc| minus the
+// filter bound), then a candidate pass at threshold m / n (1 - 1e-6) holds the
+// maximiser, and the refine recomputes the candidates exactly (float64): the
+// result is the exact maximum of the f32 data's S. Other GEMM kinds: direct
+// float64 dot products on the CUDA cores. The iterate is not changed.
+double lambda_max_impl(accord_ctx* c) {
+  cudaStream_t S = c->st;
+  const int64_t xrow0 = c->sharded ? 0 : c->r0;   // X^T row of local row 0
+  const size_t T = c->tsz;
+  const char* xrows = (const char*)c->Xt + (size_t)xrow0 * c->ldk * T;
+  double* rmax = c->dalloc<double>(std::max<int64_t>(c->pk, 1));
+  double* dout = c->dalloc<double>(1);
+  struct Tmp {
+    accord_ctx* c;
+    std::vector<std::pair<void*, size_t>> v;
+    ~Tmp() { for (auto& q : v) c->dfree(q.first, q.second); }
+  } tmp{c, {{rmax, std::max<int64_t>(c->pk, 1) * 8}, {dout, 8}}};
+  const bool filt = c->gemm == ACCORD_GEMM_BF16_FILTER &&
+                    (c->sharded || c->r0 + c->pk_pad <= c->xrows_pad);
+  if (!filt) {
+    if (!c->sharded) {
+      c->launches += launch_gram_offdiag_max(c->dtype, c->pk, c->r0, c->n, c->ldk, xrows, c->Xt, 0,
+                                             c->p, 0, rmax, dout, S);
+    } else {
+      ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool first, bool last) {
+        c->launches += launch_gram_offdiag_max(c->dtype, c->pk, c->r0, c->n, c->ldk, xrows, slab,
+                                               v0, v1, first ? 0 : 1, rmax, last ? dout : nullptr,
+                                               S);
+      });
+    }
+    CK(cudaGetLastError());
+    return allreduce_max(c, dout);
+  }
+  // ---- tensor-core filter path ----
+  if (!c->plan_a_x) {
+    std::string e;
+    const __nv_bfloat16* xh = c->Xhi + (size_t)xrow0 * c->ldk;
+    if (!tc_plan_set_a(c->plan, 2, xh, c->pk_pad, &e)) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
+    c->plan_a_x = true;
+  }
+  float* rA = c->dalloc<float>(std::max<int64_t>(c->pk, 1));
+  float* rB = c->dalloc<float>(std::max<int64_t>(c->pk, 1));
+  int64_t* eptr = c->dalloc<int64_t>(c->pk + 1);   // empty support (diagonal is emitted anyway)
+  unsigned int* dmax = c->dalloc<unsigned int>(1);
+  tmp.v.push_back({rA, std::max<int64_t>(c->pk, 1) * 4});
+  tmp.v.push_back({rB, std::max<int64_t>(c->pk, 1) * 4});
+  tmp.v.push_back({eptr, (c->pk + 1) * 8});
+  tmp.v.push_back({dmax, 4});
+  CK(cudaMemsetAsync(eptr, 0, (c->pk + 1) * 8, S));
+  CK(cudaMemsetAsync(dmax, 0, 4, S));
+  c->launches += launch_row_ab(c->pk, c->ldk, (const float*)xrows, rA, rB, S);
+  GradOverride ov{2, rA, rB, OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax, xrows,
+                  c->world == 1 && !c->sharded && c->r0 == 0 && c->pk == c->p &&
+                      !std::getenv("ACCORD_GEMM_NOSYM")};
+  accord_iter_stats st{};
+  build_candidates(c, st, &ov);                      // pass 1: certified lower bound
+  unsigned int hm = 0;
+  CK(cudaMemcpyAsync(&hm, dmax, 4, cudaMemcpyDeviceToHost, S));
+  CK(cudaStreamSynchronize(S));
+  float lb = 0.f;
+  std::memcpy(&lb, &hm, 4);
+  double lbd = (double)lb;
+  {   // the global lower bound (every rank's maximiser must be kept)
+    double* d = c->red_d + 8;
+    CK(cudaMemcpyAsync(d, &lbd, 8, cudaMemcpyHostToDevice, S));
+    lbd = allreduce_max(c, d);
+  }
+  ov.max_out = nullptr;
+  ov.lam_cand = std::max(0.0, lbd / (double)c->n * (1.0 - 1e-6));
+  build_candidates(c, st, &ov);                      // pass 2: candidates + exact refine
+  c->items_of = nullptr;
+  c->launches += launch_cand_offdiag_max(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, rmax,
+                                         dout, S);
+  CK(cudaGetLastError());
+  return allreduce_max(c, dout);
 }
 
 // Gather every rank's row block of Omega into one global host CSR (collective).
@@ -1752,6 +1885,71 @@ accord_status accord_path(accord_ctx* c, const double* lambdas, int32_t k, int32
     recompute_y(c);
     refresh_objective(c);
     if (best) *best = bi;
+  });
+}
+
+accord_status accord_lambda_max(accord_ctx* c, double* lmax) {
+  if (!c || !lmax) return ACCORD_E_INVALID;
+  return guard(c, [&] {
+    const double v = lambda_max_impl(c);
+    if (!(v > 0) || !std::isfinite(v))
+      throw Fail{ACCORD_E_NUMERIC, "lambda_max is not positive (all-zero or uncorrelated data)"};
+    *lmax = v;
+  });
+}
+
+accord_status accord_lambda_grid(accord_ctx* c, int32_t k, double ratio, double* lambdas) {
+  if (!c || !lambdas || k < 1 || !(ratio > 0 && ratio < 1)) {
+    if (c) c->err = "need k >= 1 and 0 < ratio < 1";
+    return ACCORD_E_INVALID;
+  }
+  double lm = 0;
+  const accord_status s = accord_lambda_max(c, &lm);
+  if (s != ACCORD_OK) return s;
+  // k log-evenly spaced points from lambda_max down to ratio * lambda_max
+  for (int32_t j = 0; j < k; ++j)
+    lambdas[j] = k == 1 ? lm : lm * std::pow(ratio, (double)j / (double)(k - 1));
+  return ACCORD_OK;
+}
+
+accord_status accord_filter_audit(accord_ctx* c, float* acc, int64_t ld, float* y, int64_t ldy,
+                                  float* row_ab, float* col_sd, double* gamma, int64_t* c_ptr,
+                                  int32_t* c_col, int64_t capacity, int64_t* n_cand) {
+  if (!c || !acc || !n_cand) return ACCORD_E_INVALID;
+  return guard(c, [&] {
+    if (c->gemm != ACCORD_GEMM_BF16_FILTER)
+      throw Fail{ACCORD_E_UNSUPPORTED, "filter audit needs the BF16_FILTER GEMM"};
+    if (ld < c->p) throw Fail{ACCORD_E_INVALID, "ld < p"};
+    if (y && ldy < c->n) throw Fail{ACCORD_E_INVALID, "ldy < n"};
+    c->audit_acc = acc;
+    c->audit_ld = ld;
+    accord_iter_stats st{};
+    try {
+      build_candidates(c, st);
+    } catch (...) {
+      c->audit_acc = nullptr;
+      throw;
+    }
+    c->audit_acc = nullptr;
+    cudaStream_t S = c->st;
+    if (y)
+      CK(cudaMemcpy2DAsync(y, ldy * 4, c->Y[c->cur], c->ldk * 4, c->n * 4, c->pk,
+                           cudaMemcpyDeviceToDevice, S));
+    if (row_ab) {
+      CK(cudaMemcpyAsync(row_ab, c->row_A[c->cur], c->pk * 4, cudaMemcpyDeviceToHost, S));
+      CK(cudaMemcpyAsync(row_ab + c->pk, c->row_B[c->cur], c->pk * 4, cudaMemcpyDeviceToHost, S));
+    }
+    if (col_sd) CK(cudaMemcpyAsync(col_sd, c->col_sd, c->p * 8, cudaMemcpyDeviceToHost, S));
+    if (gamma) *gamma = (double)(float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
+    int64_t nc = 0;
+    CK(cudaMemcpyAsync(&nc, c->c_ptr + c->pk, 8, cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    *n_cand = nc;
+    if (!c_ptr) return;
+    if (capacity < nc) throw Fail{ACCORD_E_CAPACITY, "capacity too small"};
+    CK(cudaMemcpyAsync(c_ptr, c->c_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(c_col, c->c_col, nc * 4, cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
   });
 }
 

@@ -147,7 +147,11 @@ struct TileIt {
   __device__ bool unit_start() const { return start; }
 };
 
-template <int kMode, int kStagesT, bool kFast>
+// kDiag: 0 = the product epilogue; 1 = audit (also writes every raw fp32
+// accumulator to ep.audit_acc, for the filter certification test); 2 = max
+// reduction (no emission: a certified lower bound on n max_{i!=k} |G_ik|
+// into *ep.max_out, the lambda_max of a path)
+template <int kMode, int kStagesT, bool kFast, int kDiag = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
@@ -300,6 +304,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     bool row_ok = false;
     int32_t nxt = INT_MAX;
     float r1 = 0.f, Bn = 0.f;
+    float wmax = 0.f;                               // kDiag == 2
     for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
       const int n0 = (int)ep.col_base + it.n() * BN;   // global column of the tile
       if (it.unit_start()) {
@@ -377,6 +382,31 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           const uint32_t* v = h ? vb : va;
           const int c0 = n0 + ch2 * 64 + h * 32;
           const int64_t sp0 = sp;
+          if constexpr (kDiag == 1) {   // audit: the raw accumulator of every computed entry
+            if (row_ok) {
+              const bool mir = sched.sym && it.n() != it.m;
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int64_t k = c0 + c;
+                if (k < col_end) {
+                  ep.audit_acc[r * ep.audit_ld + k] = __uint_as_float(v[c]);
+                  if (mir) ep.audit_acc[k * ep.audit_ld + gi] = __uint_as_float(v[c]);
+                }
+              }
+            }
+          }
+          if constexpr (kDiag == 2) {
+            // max |acc| off the diagonal minus this row's tile bound n*delta
+            // (= thr - tfast): a lower bound on n |G_ik| of the maximiser
+            if (row_ok) {
+              float mm = 0.f;
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (c0 + c < col_end && c0 + c != gi) mm = fmaxf(mm, fabsf(__uint_as_float(v[c])));
+              wmax = fmaxf(wmax, mm - (thr - tfast));
+            }
+            continue;
+          }
           // common case first, one vote per 32 columns: no lane has an |acc|
           // above the tile's threshold (one FMNMX3 per two values), its
           // diagonal or a support entry of Omega in these columns
@@ -498,6 +528,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     }
     if (lane == 0 && chunk_id >= 0 && chunk_id < pool.nchunks)
       pool.chunk_fill[chunk_id] = (unsigned long long)fill;
+    if constexpr (kDiag == 2) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+      if (lane == 0 && wmax > 0.f) atomicMax(ep.max_out, __float_as_uint(wmax));
+    }
   }
   tc::tc_fence_before();
   tc::cluster_sync();
@@ -573,7 +608,9 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t kdim, int6
 struct TcGemmPlan {
   // B operand maps: [0] = X^T (all columns, or this rank's slab when X is
   // sharded), [1], [2] = the two ring buffers of the sharded mode (NEXT(3))
-  CUtensorMap a_hi[2], a_lo[2], b_hi[3], b_lo[3];
+  // A operand maps: [0], [1] = the two Y buffers, [2] = this rank's rows of
+  // X^T_hi (Omega = I operand of the lambda_max pass, tc_plan_set_a)
+  CUtensorMap a_hi[3], a_lo[3], b_hi[3], b_lo[3];
   int64_t pk_pad = 0, p_pad = 0, ldk = 0, kdim = 0;   // p_pad: padded column count (all p)
   float2* blk_sdmax = nullptr;   // [p_pad / 256] (BF16_FILTER)
 };
@@ -598,6 +635,8 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
             make_map(&p->b_lo[0], Xlo, xrows_pad, kdim, ldk, BNH, err);
   p->b_hi[1] = p->b_hi[2] = p->b_hi[0];
   p->b_lo[1] = p->b_lo[2] = p->b_lo[0];
+  p->a_hi[2] = p->a_hi[0];
+  p->a_lo[2] = p->a_lo[0];
   if (ok && cudaMalloc(&p->blk_sdmax, (p_pad / BN) * sizeof(float2)) != cudaSuccess) {
     *err = "alloc";
     ok = false;
@@ -617,9 +656,19 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                          (int)Cfg<1, 7>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<1, 6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg<1, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true, 1>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true, 2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
     attr_done(attr_seen);
   }
   return p;
+}
+
+bool tc_plan_set_a(TcGemmPlan* p, int idx, const __nv_bfloat16* hi, int64_t rows_pad,
+                   std::string* err) {
+  return make_map(&p->a_hi[idx], hi, rows_pad, p->kdim, p->ldk, BM, err) &&
+         make_map(&p->a_lo[idx], hi, rows_pad, p->kdim, p->ldk, BM, err);
 }
 
 bool tc_plan_set_b(TcGemmPlan* p, int idx, const __nv_bfloat16* hi, const __nv_bfloat16* lo,
@@ -683,6 +732,12 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0, 3, true><<<grid, kThreads, Cfg<0, 3>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_lo[bsel]));
+  else if (ep.audit_acc)
+    gemm_tc_kernel<1, 6, true, 1><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
+  else if (ep.max_out)
+    gemm_tc_kernel<1, 6, true, 2><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
   else if (var == 1)
     gemm_tc_kernel<1, 7, true><<<grid, kThreads, Cfg<1, 7>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_hi[bsel]));

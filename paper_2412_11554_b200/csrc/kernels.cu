@@ -738,6 +738,82 @@ __global__ void __launch_bounds__(1024) reduce_max_kernel(int64_t pk, const doub
   }
 }
 
+// ---------------------------------------------------------------------------
+// lambda_max = max_{i != k} |S_ik| (the top of a lambda path, SURVEY.md §8(f)
+// NEXT(2); SPEC.md lambda_grid)
+// ---------------------------------------------------------------------------
+// Filter row constants of A = the rank's rows of X^T (Omega = I): A_i =
+// ||x_i - bf16(x_i)||, B_i = ||x_i||, rounded up (warp per row).
+__global__ void xrow_ab_kernel(int64_t pk, int64_t ldk, const float* __restrict__ Xt,
+                               float* __restrict__ row_A, float* __restrict__ row_B) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  double xx = 0, ee = 0;
+  for (int64_t m = lane; m < ldk; m += 32) {
+    const float x = Xt[r * ldk + m];
+    const double e = (double)x - (double)__bfloat162float(filter_bf16(x));
+    xx += (double)x * x;
+    ee += e * e;
+  }
+  xx = warp_sum(xx);
+  ee = warp_sum(ee);
+  if (lane == 0) {
+    row_A[r] = __double2float_ru(sqrt(ee) * (1.0 + 1e-12));
+    row_B[r] = __double2float_ru(sqrt(xx) * (1.0 + 1e-12));
+  }
+}
+
+// Per-row max of |c_g| over the OFF-diagonal entries of C (warp per row).
+template <typename T>
+__global__ void cand_offdiag_max_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
+                                        const int32_t* __restrict__ c_col,
+                                        const T* __restrict__ c_g, double* __restrict__ row_max) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  double mx = 0.0;
+  for (int64_t e = c_ptr[r] + lane; e < c_ptr[r + 1]; e += 32)
+    if (c_col[e] != r0 + r) mx = fmax(mx, fabs((double)c_g[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) row_max[r] = mx;
+}
+
+// Direct evaluation (CUDA cores, float64 accumulation) for the SIMT / BF16X3
+// contexts: row_max[r] = max over columns k in [v0, v1), k != r0 + r, of
+// |<x_{r0+r}, x_k>| / n. Block per row, x_i staged in shared memory, warp per
+// column. Xi = the rank's row r of X^T; Xt row 0 = column v0.
+template <typename T>
+__global__ void __launch_bounds__(256) gram_offdiag_max_kernel(int64_t pk, int64_t r0, int64_t n,
+                                                               int64_t ldk, const T* __restrict__ Xi,
+                                                               const T* __restrict__ Xt, int64_t v0,
+                                                               int64_t v1, int accumulate,
+                                                               double* __restrict__ row_max) {
+  extern __shared__ __align__(16) uint8_t xs_raw[];
+  T* xs = reinterpret_cast<T*>(xs_raw);
+  __shared__ double wm[8];
+  const int64_t r = blockIdx.x;
+  for (int64_t m = threadIdx.x; m < ldk; m += blockDim.x) xs[m] = Xi[r * ldk + m];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double mx = 0.0;
+  for (int64_t k = v0 + wid; k < v1; k += nw) {
+    if (k == r0 + r) continue;
+    const T* xr = Xt + (k - v0) * ldk;
+    double s = 0.0;
+    for (int64_t m = lane; m < ldk; m += 32) s = fma((double)xs[m], (double)xr[m], s);
+    s = warp_sum(s);
+    mx = fmax(mx, fabs(s) / (double)n);
+  }
+  if (lane == 0) wm[wid] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) mx = fmax(mx, wm[w]);
+    row_max[r] = accumulate ? fmax(row_max[r], mx) : mx;
+  }
+}
+
 // per-column constants of the filter bound (warp per column of X = row of Xt)
 __global__ void col_norms_kernel(int64_t p, int64_t ldk, const float* __restrict__ Xt,
                                  float2* __restrict__ col_sd) {
@@ -1113,6 +1189,52 @@ int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const in
                                          (const float*)c_w, lam, row_max);
   reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
   return 2;
+}
+
+int launch_row_ab(int64_t pk, int64_t ldk, const float* Xt_rows, float* row_A, float* row_B,
+                  cudaStream_t st) {
+  if (pk == 0) return 0;
+  xrow_ab_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, ldk, Xt_rows, row_A, row_B);
+  return 1;
+}
+
+int launch_cand_offdiag_max(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr,
+                            const int32_t* c_col, const void* c_g, double* row_max, double* out,
+                            cudaStream_t st) {
+  if (pk == 0) return 0;
+  const unsigned g = (unsigned)((pk + 7) / 8);
+  if (dtype == ACCORD_F64)
+    cand_offdiag_max_kernel<double><<<g, 256, 0, st>>>(pk, r0, c_ptr, c_col, (const double*)c_g,
+                                                       row_max);
+  else
+    cand_offdiag_max_kernel<float><<<g, 256, 0, st>>>(pk, r0, c_ptr, c_col, (const float*)c_g,
+                                                      row_max);
+  reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
+  return 2;
+}
+
+int launch_gram_offdiag_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
+                            const void* Xi, const void* Xt, int64_t v0, int64_t v1, int accumulate,
+                            double* row_max, double* out, cudaStream_t st) {
+  if (pk == 0) return 0;
+  const size_t T = dtype == ACCORD_F64 ? 8 : 4;
+  const size_t smem = (size_t)ldk * T;
+  static unsigned long long attr_seen = 0;
+  if (attr_needed(attr_seen)) {
+    cudaFuncSetAttribute(gram_offdiag_max_kernel<float>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gram_offdiag_max_kernel<double>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_done(attr_seen);
+  }
+  if (dtype == ACCORD_F64)
+    gram_offdiag_max_kernel<double><<<(unsigned)pk, 256, smem, st>>>(
+        pk, r0, n, ldk, (const double*)Xi, (const double*)Xt, v0, v1, accumulate, row_max);
+  else
+    gram_offdiag_max_kernel<float><<<(unsigned)pk, 256, smem, st>>>(
+        pk, r0, n, ldk, (const float*)Xi, (const float*)Xt, v0, v1, accumulate, row_max);
+  if (out) reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
+  return out ? 2 : 1;
 }
 
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st) {

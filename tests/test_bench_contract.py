@@ -33,3 +33,22 @@ def test_bench_help_lists_the_driver_flags():
     assert r.returncode == 0
     for flag in ("--gpus", "--steps", "--warmup", "--impl", "--config"):
         assert flag in r.stdout
+
+
+def test_reference_arm_spawns_ranks_itself():
+    """--gpus 2 without torchrun: bench.py re-launches itself through
+    torch.distributed.run (gloo for the reference arm on CPU); rank 0 alone
+    prints one line with n_gpus = 2, and the oracle used every host core."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--config", "1", "--steps", "2", "--warmup", "1",
+                        "--ref-rows", "8"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert len(d["iterate"]["tau"]) == 2 and all(t > 0 for t in d["iterate"]["tau"])
+    assert d["cpu_baseline"]["cores"] == os.cpu_count()

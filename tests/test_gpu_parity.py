@@ -106,6 +106,28 @@ def test_objective_at_identity_and_export_invariants():
         assert np.all((vals != 0) | (cols == i))
 
 
+def test_lanczos_exactly_centered_and_zero_x():
+    """L from the device Lanczos on EXACTLY centered data (balanced +-1
+    columns: X^T 1 = 0 in exact arithmetic, so a constant start vector would
+    be mapped to 0) is sigma_max(S), and X = 0 is
+    reported instead of silently disabling the tau <= 1/L floor."""
+    _cuda()
+    rng = np.random.default_rng(5)
+    p, n = 300, 64
+    half = np.array([1.0] * (n // 2) + [-1.0] * (n // 2), dtype=np.float32)
+    Xt = np.stack([rng.permutation(half) for _ in range(p)])
+    assert np.all(Xt.sum(axis=1) == 0)
+    L = O.spectral_bound(Xt)
+    with A.AccordSolver(torch.from_numpy(Xt).cuda(), 0.1, inv_L=0.0) as s:
+        info = s.info()
+        assert abs(info["L"] / (1 + 2e-3) - L) <= 1e-9 * L
+        st = s.step(2)
+        assert all(x["tau"] >= min(0.5, 0.5 * info["inv_L"]) for x in st)
+    with pytest.raises(A.AccordError) as e:
+        A.AccordSolver(torch.zeros((50, 40), dtype=torch.float32).cuda(), 0.1, inv_L=0.0)
+    assert e.value.status == A.E_NUMERIC
+
+
 def test_warm_start_roundtrip():
     _cuda()
     pr = make_problem("t_ba_f64")

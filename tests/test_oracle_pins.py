@@ -198,6 +198,33 @@ def test_p8_kkt_and_p9_fixed_point():
     assert ((Om != 0).sum() - 25) > 0
 
 
+@pytest.mark.parametrize("case", GOLD["kkt_worked"])
+def test_p8_kkt_residual_worked_nonstationary(case):
+    """Eq. (3.3) at NON-stationary Omega, hand-worked: one case per branch
+    (diagonal, zero off-diagonal, nonzero off-diagonal) dominates, so dropping
+    a branch or flipping the sign of lam*sign(omega) changes the value."""
+    X = np.array(case["X_samples"], dtype=np.float64)     # n x p, samples-major
+    Xt = np.ascontiguousarray(X.T)
+    if "S_by_hand" in case:
+        np.testing.assert_array_equal(Xt @ Xt.T / X.shape[0], np.array(case["S_by_hand"]))
+    r = O.kkt_residual(np.array(case["Omega"]), Xt, case["lam"])
+    assert abs(r - case["expect"]) <= 1e-14, (case["branch"], r)
+
+
+def test_p16_candidate_set_worked_exact():
+    """C equals the hand-worked set, |G_ik| = lam exactly excluded; and C is
+    exactly the union over tau of supp prox(Omega - tau G) plus the diagonal
+    (an all-True or a superset C fails)."""
+    c = GOLD["candidate_set_worked"]
+    Om, G, lam = np.array(c["Omega"]), np.array(c["G"]), c["lam"]
+    C = O.candidate_set(Om, G, lam)
+    np.testing.assert_array_equal(C, np.array(c["expect"], dtype=bool))
+    U = np.eye(4, dtype=bool)
+    for tau in 10.0 ** np.arange(-300, 7, 3, dtype=np.float64):
+        U |= O.prox(Om - tau * G, tau, lam, np.arange(4)) != 0
+    np.testing.assert_array_equal(C, U)
+
+
 # ---------------------------------------------------------------- P10 --------
 def test_p10_lambda0_lowdim_closed_form():
     Xt = rand_problem(20, 200, 10)
@@ -315,6 +342,25 @@ def test_p15_row_replay_equals_full():
     assert np.abs(rr["Omega_rows"] - r["Omega"][rows]).max() < 1e-12
 
 
+def test_p15_row_replay_with_trials_and_all_rows_line_search():
+    """(a) charging the rejected trials does not change the replay; (b) the
+    row-restricted line search on ALL rows is Algorithm 1 itself (same tau
+    schedule, trial counts and iterate as fbs)."""
+    pr = make_problem("t_ba_f64")
+    c = pr.cfg
+    r = O.fbs(pr.Xt, c.lambdas[0], c.tau0, c.beta, None, T=8)
+    rows = np.array([0, 7, 299])
+    tt = [[c.tau0 * c.beta ** j for j in range(k)] for k in r["trials"]]
+    a = O.fbs_rows(pr.Xt, rows, c.lambdas[0], r["taus"])
+    b = O.fbs_rows(pr.Xt, rows, c.lambdas[0], r["taus"], trial_taus=tt)
+    assert np.array_equal(a["Omega_rows"], b["Omega_rows"])
+    assert max(r["trials"]) > 1                 # the case does backtrack
+    ls = O.fbs_rows_ls(pr.Xt, np.arange(c.p), c.lambdas[0], c.tau0, c.beta, r["inv_L"], T=8)
+    assert np.array_equal(ls["taus"], r["taus"])
+    assert np.array_equal(ls["trials"], r["trials"])
+    assert np.abs(ls["Omega_rows"] - r["Omega"]).max() < 1e-12
+
+
 # ---------------------------------------------------------------- P16 --------
 def test_p16_candidate_set_tau_independent():
     pr = make_problem("t_ba_f64")
@@ -331,6 +377,13 @@ def test_p16_candidate_set_tau_independent():
         new_sets.append((W != 0) & (Om == 0))
     for s in new_sets[1:]:
         assert np.array_equal(s, new_sets[0])
+    # exactness: C is the union over tau > 0 of the supports (diagonal always),
+    # with tau down to 1e-300 so that every nonzero omega_ik survives somewhere
+    U = np.eye(p, dtype=bool)
+    for tau in np.concatenate([10.0 ** np.arange(-300, -20, 20.0), [1e-8, 1e-4, 0.1, 0.5, 2.0]]):
+        U |= O.prox(Om - tau * G, tau, 0.1, np.arange(p)) != 0
+    assert np.array_equal(C, U)
+    assert 0 < C.sum() < C.size
 
 
 # ---------------------------------------------------------------- P18 --------

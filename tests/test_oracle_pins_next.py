@@ -93,3 +93,44 @@ def test_reparameterisation_and_partial_correlations():
     pc = GOLD["partial_corr"]
     assert abs(O.partial_correlations(np.array(pc["Omega"], float))[0, 1] - pc["rho12"]) < 1e-15
     assert np.all(O.partial_correlations(np.diag([1.0, 2.0, 3.0])) == 0)
+
+
+# ---------------------------------------------------------- lambda grid ------
+@pytest.mark.parametrize("case", GOLD["lambda_grid_worked"])
+def test_lambda_max_worked(case):
+    """lambda_max = max off-diagonal |S_ij| on worked cases (SPEC.md
+    lambda_grid example; by hand)."""
+    Xt = np.ascontiguousarray(np.array(case["X_samples"], dtype=np.float64).T)
+    assert O.lambda_max(Xt) == case["expect_lambda_max"]
+
+
+def test_lambda_max_brute_force_pairs():
+    """Against plain Python dot products over every pair i != k."""
+    Xt = rand_problem(9, 13, 77)
+    n = Xt.shape[1]
+    best = 0.0
+    for i in range(9):
+        for k in range(9):
+            if i != k:
+                best = max(best, abs(sum(float(Xt[i, m]) * float(Xt[k, m]) for m in range(n)) / n))
+    assert abs(O.lambda_max(Xt) - best) <= 1e-14 * best
+
+
+@pytest.mark.parametrize("case", GOLD["lambda_grid_spacing"])
+def test_lambda_grid_spacing_worked(case):
+    # a 2-variable X with S_01 = lambda_max: columns (a, a) scaled
+    a = np.sqrt(case["lambda_max"])
+    Xt = np.array([[a, -a], [a, -a]])
+    g = O.lambda_grid(Xt, case["k"], case["ratio"])
+    np.testing.assert_allclose(g, case["expect"], rtol=1e-14)
+
+
+def test_lambda_max_gives_empty_first_step():
+    """At lambda >= lambda_max no off-diagonal entry enters C from Omega = I
+    (|G_ik| = |S_ik| <= lambda, Eq. 3.5 / P16): the first FBS step is diagonal."""
+    Xt = rand_problem(12, 40, 78)
+    lm = O.lambda_max(Xt)
+    r = O.fbs(Xt, lm, 0.5, 0.5, None, T=1)
+    assert np.count_nonzero(r["Omega"] - np.diag(np.diag(r["Omega"]))) == 0
+    r2 = O.fbs(Xt, lm * 0.999, 0.5, 0.5, None, T=1)
+    assert np.count_nonzero(r2["Omega"] - np.diag(np.diag(r2["Omega"]))) > 0
