@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define ACCORD_ABI_VERSION 2
+#define ACCORD_ABI_VERSION 3
 
 typedef enum {
   ACCORD_OK = 0,
@@ -141,6 +141,16 @@ typedef struct {
                                (Alg. 2): NCCL send/recv on a split
                                communicator, or `sendrecv` with ACCORD_COMM_HOST. */
   accord_sendrecv_fn sendrecv;       /* ACCORD_COMM_HOST with x_sharded */
+  void* workspace;          /* NULL: the library cudaMallocs its device memory. Else a
+                               caller-owned device buffer on `device` (e.g. a torch
+                               tensor) of workspace_bytes bytes, at least
+                               accord_workspace_size(): every device buffer of the
+                               context is carved out of it and the library never calls
+                               cudaMalloc. A pool overflow grows inside the workspace;
+                               when it does not fit, the call returns ACCORD_E_CAPACITY
+                               (nothing committed; the message gives the bytes needed).
+                               The caller frees it after accord_destroy. */
+  size_t workspace_bytes;
 } accord_init_params;
 
 /* Per accepted outer iteration (one element per iteration of accord_step). */
@@ -179,12 +189,27 @@ typedef struct {
   int64_t gemm_launches;        /* cumulative count of gradient-GEMM launches */
   double f;                     /* current objective (global) */
   size_t device_bytes;          /* device memory held by the context */
+  size_t workspace_bytes;       /* caller workspace size (0: library-allocated memory) */
+  size_t workspace_high;        /* high-water mark of the workspace in use */
 } accord_info;
 
 typedef struct accord_ctx accord_ctx;
 
 /* Fill *prm with defaults (abi_version, device=-1, beta=0.5, tau0=0.5, world=1, ...). */
 void accord_default_params(accord_init_params* prm);
+
+/* Device bytes accord_create needs for *prm when the caller owns the memory
+ * (prm->workspace): X^T and its bf16 copy, Y x 2 and its bf16 copies, the
+ * per-row state, and the candidate pool / C / Omega arrays at the pool
+ * capacity (prm->cand_capacity, or the default ~512 candidates per row, the
+ * first iteration's demand at config 5) -- the inputs of Alg. 1
+ * laid out as DESIGN.md §6 states -- plus the transient
+ * staging of a host X or the Lanczos vectors of L. Pure: validates *prm (same
+ * errors as accord_create) and touches no device. An upper bound for the
+ * AUTO GEMM kind and balanced sharded slabs; later calls that allocate
+ * temporaries (export GATHER, transformed exports, path, refit, lambda_max)
+ * need free workspace beyond it. */
+accord_status accord_workspace_size(const accord_init_params* prm, size_t* bytes);
 
 /* Create a solver context: validates, copies X to the device (variable-major,
  * zero-padded to a multiple of 64 samples), builds GEMM operand copies,

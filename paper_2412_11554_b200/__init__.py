@@ -55,6 +55,7 @@ class InitParams(C.Structure):
         ("comm_user", C.c_void_p), ("stream", C.c_void_p),
         ("cand_capacity", C.c_int64),
         ("x_sharded", C.c_int32), ("sendrecv", SENDRECV_FN),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
     ]
 
 
@@ -86,6 +87,7 @@ class Info(C.Structure):
         ("iterations", C.c_int64), ("nnz_local", C.c_int64), ("cand_capacity", C.c_int64),
         ("kernel_launches", C.c_int64), ("gemm_launches", C.c_int64),
         ("f", C.c_double), ("device_bytes", C.c_size_t),
+        ("workspace_bytes", C.c_size_t), ("workspace_high", C.c_size_t),
     ]
 
     def as_dict(self):
@@ -104,7 +106,7 @@ class AccordLibraryMissing(RuntimeError):
 
 _LIB = None
 
-EXPORTED = ["accord_default_params", "accord_create", "accord_step", "accord_objective",
+EXPORTED = ["accord_default_params", "accord_workspace_size", "accord_create", "accord_step", "accord_objective",
             "accord_export_csr", "accord_set_omega_csr", "accord_row_stats",
             "accord_get_info", "accord_nccl_unique_id", "accord_destroy",
             "accord_status_string", "accord_last_error", "accord_abi_version",
@@ -126,6 +128,7 @@ def lib():
     L.accord_default_params.argtypes = [C.POINTER(InitParams)]
     L.accord_default_params.restype = None
     L.accord_create.argtypes = [C.POINTER(C.c_void_p), C.POINTER(InitParams)]
+    L.accord_workspace_size.argtypes = [C.POINTER(InitParams), C.POINTER(C.c_size_t)]
     L.accord_step.argtypes = [C.c_void_p, C.c_int32, C.POINTER(IterStats)]
     L.accord_objective.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.accord_export_csr.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -216,6 +219,82 @@ class CSR:
         return A
 
 
+def _build_params(X, lam, *, layout="variables", tau0=0.5, beta=0.5, inv_L=0.0,
+                  row_begin=0, row_end=None, rank=0, world=1, comm=COMM_NONE,
+                  nccl_id: bytes | None = None, allreduce=None, allgatherv=None,
+                  gemm=GEMM_AUTO, cand_capacity=0, stream=None, device=None,
+                  x_sharded=False, p_global=None, sendrecv=None):
+    """accord_init_params for X (argument marshalling only)."""
+    import torch
+    L = lib()
+    keep = []
+    if isinstance(X, np.ndarray):
+        X = torch.from_numpy(np.ascontiguousarray(X))
+    if X.dtype not in (torch.float32, torch.float64):
+        raise TypeError("X must be float32 or float64")
+    if X.dim() != 2 or not X.is_contiguous():
+        raise ValueError("X must be a contiguous 2-D tensor")
+    lay = LAYOUT_VARIABLES if layout.startswith("var") else LAYOUT_SAMPLES
+    p = X.shape[0] if lay == LAYOUT_VARIABLES else X.shape[1]
+    n = X.shape[1] if lay == LAYOUT_VARIABLES else X.shape[0]
+    if x_sharded:
+        # X holds this rank's variables [row_begin, row_end) only (NEXT(3))
+        if row_end is None or p_global is None:
+            raise ValueError("x_sharded needs row_begin, row_end and p_global")
+        if p != int(row_end) - int(row_begin):
+            raise ValueError("sharded X must hold exactly the rank's variables")
+        p = int(p_global)
+    prm = InitParams()
+    L.accord_default_params(C.byref(prm))
+    if device is None:
+        device = X.device.index if X.is_cuda else (torch.cuda.current_device()
+                                                   if torch.cuda.is_available() else 0)
+    prm.device = int(device)
+    prm.n, prm.p = n, p
+    prm.X = X.data_ptr()
+    prm.ldx = 0
+    prm.layout = lay
+    prm.dtype = F64 if X.dtype == torch.float64 else F32
+    prm.x_on_device = 1 if X.is_cuda else 0
+    prm.gemm = gemm
+    prm.lambda_ = float(lam)
+    prm.tau0, prm.beta, prm.inv_L = float(tau0), float(beta), float(inv_L)
+    prm.row_begin = int(row_begin)
+    prm.row_end = int(p if row_end is None else row_end)
+    prm.rank, prm.world, prm.comm = int(rank), int(world), int(comm)
+    if nccl_id is not None:
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        keep.append(idbuf)
+        prm.nccl_id = C.addressof(idbuf)
+    if allreduce is not None:
+        cb = ALLREDUCE_FN(allreduce)
+        keep.append(cb)
+        prm.allreduce = cb
+    if allgatherv is not None:
+        cb2 = ALLGATHERV_FN(allgatherv)
+        keep.append(cb2)
+        prm.allgatherv = cb2
+    if sendrecv is not None:
+        cb3 = SENDRECV_FN(sendrecv)
+        keep.append(cb3)
+        prm.sendrecv = cb3
+    prm.x_sharded = 1 if x_sharded else 0
+    if stream is None and torch.cuda.is_available():
+        stream = torch.cuda.current_stream(prm.device)
+    prm.stream = (stream.cuda_stream if hasattr(stream, "cuda_stream") else stream) or None
+    prm.cand_capacity = int(cand_capacity)
+    return prm, keep, dict(X=X, n=n, p=p)
+
+
+def workspace_size(X, lam, **kw) -> int:
+    """accord_workspace_size for the context AccordSolver(X, lam, **kw) would
+    create (pure: no device work)."""
+    prm, _keep, _meta = _build_params(X, lam, **kw)
+    b = C.c_size_t()
+    _check(lib().accord_workspace_size(C.byref(prm), C.byref(b)), None)
+    return int(b.value)
+
+
 class AccordSolver:
     """One rank's ACCORD-FBS solver context (accord_create .. accord_destroy).
 
@@ -224,78 +303,34 @@ class AccordSolver:
     x_sharded=True (with p_global and a communicator): X holds only this
     rank's variables [row_begin, row_end) and every pass over X runs as a ring
     of slab exchanges (Alg. 2; include/accord.h `x_sharded`).
+    workspace: None (the library allocates), "torch" (a torch uint8 tensor of
+    accord_workspace_size() bytes, owned by this object) or a CUDA tensor the
+    caller owns (every device buffer of the context is carved out of it).
     """
 
-    def __init__(self, X, lam, *, layout="variables", tau0=0.5, beta=0.5, inv_L=0.0,
-                 row_begin=0, row_end=None, rank=0, world=1, comm=COMM_NONE,
-                 nccl_id: bytes | None = None, allreduce=None, allgatherv=None,
-                 gemm=GEMM_AUTO, cand_capacity=0, stream=None, device=None,
-                 x_sharded=False, p_global=None, sendrecv=None):
+    def __init__(self, X, lam, *, workspace=None, **kw):
         import torch
         L = lib()
-        self._keep = []
-        if isinstance(X, np.ndarray):
-            X = torch.from_numpy(np.ascontiguousarray(X))
-        if X.dtype not in (torch.float32, torch.float64):
-            raise TypeError("X must be float32 or float64")
-        if X.dim() != 2 or not X.is_contiguous():
-            raise ValueError("X must be a contiguous 2-D tensor")
-        lay = LAYOUT_VARIABLES if layout.startswith("var") else LAYOUT_SAMPLES
-        p = X.shape[0] if lay == LAYOUT_VARIABLES else X.shape[1]
-        n = X.shape[1] if lay == LAYOUT_VARIABLES else X.shape[0]
-        if x_sharded:
-            # X holds this rank's variables [row_begin, row_end) only (NEXT(3))
-            if row_end is None or p_global is None:
-                raise ValueError("x_sharded needs row_begin, row_end and p_global")
-            if p != int(row_end) - int(row_begin):
-                raise ValueError("sharded X must hold exactly the rank's variables")
-            p = int(p_global)
-        prm = InitParams()
-        L.accord_default_params(C.byref(prm))
-        if device is None:
-            device = X.device.index if X.is_cuda else torch.cuda.current_device()
-        prm.device = int(device)
-        prm.n, prm.p = n, p
-        prm.X = X.data_ptr()
-        prm.ldx = 0
-        prm.layout = lay
-        prm.dtype = F64 if X.dtype == torch.float64 else F32
-        prm.x_on_device = 1 if X.is_cuda else 0
-        prm.gemm = gemm
-        prm.lambda_ = float(lam)
-        prm.tau0, prm.beta, prm.inv_L = float(tau0), float(beta), float(inv_L)
-        prm.row_begin = int(row_begin)
-        prm.row_end = int(p if row_end is None else row_end)
-        prm.rank, prm.world, prm.comm = int(rank), int(world), int(comm)
-        if nccl_id is not None:
-            idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-            self._keep.append(idbuf)
-            prm.nccl_id = C.addressof(idbuf)
-        if allreduce is not None:
-            cb = ALLREDUCE_FN(allreduce)
-            self._keep.append(cb)
-            prm.allreduce = cb
-        if allgatherv is not None:
-            cb2 = ALLGATHERV_FN(allgatherv)
-            self._keep.append(cb2)
-            prm.allgatherv = cb2
-        if sendrecv is not None:
-            cb3 = SENDRECV_FN(sendrecv)
-            self._keep.append(cb3)
-            prm.sendrecv = cb3
-        prm.x_sharded = 1 if x_sharded else 0
-        if stream is None:
-            stream = torch.cuda.current_stream(prm.device)
-        prm.stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
-        prm.cand_capacity = int(cand_capacity)
-        self._X = X                    # keep alive through create
+        prm, self._keep, meta = _build_params(X, lam, **kw)
+        self._ws = None
+        if workspace is not None:
+            if isinstance(workspace, str):
+                need = workspace_size(X, lam, **kw)
+                workspace = torch.empty(need, dtype=torch.uint8,
+                                        device=torch.device("cuda", prm.device))
+            if not workspace.is_cuda:
+                raise ValueError("workspace must be a CUDA tensor")
+            self._ws = workspace
+            prm.workspace = workspace.data_ptr()
+            prm.workspace_bytes = workspace.numel() * workspace.element_size()
+        self._X = meta["X"]            # keep alive through create
         self.ctx = C.c_void_p()
         _check(L.accord_create(C.byref(self.ctx), C.byref(prm)), None)
         self._X = None
-        self.n, self.p = n, p
+        self.n, self.p = meta["n"], meta["p"]
         self.dtype = np.float64 if prm.dtype == F64 else np.float32
         self.row_begin, self.row_end = prm.row_begin, prm.row_end
-        self.world = world
+        self.world = prm.world
 
     # -- calls -------------------------------------------------------------
     def step(self, iters=1):

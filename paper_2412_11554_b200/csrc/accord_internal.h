@@ -310,7 +310,8 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            const __nv_bfloat16* Yhi1, const __nv_bfloat16* Ylo1,
                            int64_t pk_pad, const __nv_bfloat16* Xhi,
                            const __nv_bfloat16* Xlo, int64_t xrows_pad, int64_t p_pad,
-                           int64_t kdim, int64_t ldk, std::string* err);
+                           int64_t kdim, int64_t ldk, float2* blk_sdmax /* [p_pad/256], zeroed */,
+                           std::string* err);
 void tc_plan_destroy(TcGemmPlan*);
 // per-256-column maxima of the filter's column constants (after launch_col_norms)
 int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st);

@@ -13,11 +13,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -57,6 +60,8 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)();
   ncclResult_t (*CommDestroy)(ncclComm_t);
   const char* (*GetErrorString)(ncclResult_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);   // watchdog (may be NULL)
+  ncclResult_t (*CommAbort)(ncclComm_t);
 };
 
 NcclApi* nccl_api() {
@@ -71,6 +76,7 @@ NcclApi* nccl_api() {
     SYM(GetUniqueId); SYM(CommInitRank); SYM(AllReduce); SYM(AllGather); SYM(Broadcast);
     SYM(GroupStart); SYM(GroupEnd); SYM(CommDestroy); SYM(GetErrorString);
     SYM(Send); SYM(Recv); SYM(CommSplit);   // ring of the sharded mode (checked at use)
+    SYM(CommGetAsyncError); SYM(CommAbort);
 #undef SYM
     ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather &&
          api.Broadcast && api.GroupStart && api.GroupEnd && api.CommDestroy &&
@@ -85,6 +91,63 @@ NcclApi* nccl_api() {
     if (r_ != ncclSuccess)                                                        \
       throw Fail{ACCORD_E_NCCL, std::string(#call) + ": " + nccl_api()->GetErrorString(r_)}; \
   } while (0)
+
+// Caller-owned workspace (accord_init_params.workspace): every device buffer
+// of the context is carved out of it, first fit with 256-B alignment, freed
+// blocks coalesced. The library then never calls cudaMalloc; a request that
+// does not fit is ACCORD_E_CAPACITY with the size asked for.
+struct Arena {
+  char* base = nullptr;
+  size_t size = 0, in_use = 0, high = 0;
+  std::map<size_t, size_t> free_, used_;   // offset -> length
+  void init(void* b, size_t s) {
+    const uintptr_t a = ((uintptr_t)b + 255) & ~(uintptr_t)255;
+    base = (char*)a;
+    size = s > (a - (uintptr_t)b) ? (s - (a - (uintptr_t)b)) & ~(size_t)255 : 0;
+    if (size) free_[0] = size;
+  }
+  void* alloc(size_t b) {
+    b = (std::max<size_t>(b, 1) + 255) & ~(size_t)255;
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second < b) continue;
+      const size_t off = it->first, len = it->second;
+      free_.erase(it);
+      if (len > b) free_[off + b] = len - b;
+      used_[off] = b;
+      in_use += b;
+      high = std::max(high, in_use);
+      return base + off;
+    }
+    return nullptr;
+  }
+  bool release(void* p) {
+    if (!base || (char*)p < base || (char*)p >= base + size) return false;
+    auto it = used_.find((size_t)((char*)p - base));
+    if (it == used_.end()) return false;
+    size_t off = it->first, len = it->second;
+    used_.erase(it);
+    in_use -= len;
+    auto nx = free_.lower_bound(off);
+    if (nx != free_.end() && off + len == nx->first) {
+      len += nx->second;
+      nx = free_.erase(nx);
+    }
+    if (nx != free_.begin()) {
+      auto pv = std::prev(nx);
+      if (pv->first + pv->second == off) {
+        pv->second += len;
+        return true;
+      }
+    }
+    free_[off] = len;
+    return true;
+  }
+  size_t largest_free() const {
+    size_t m = 0;
+    for (auto& f : free_) m = std::max(m, f.second);
+    return m;
+  }
+};
 
 }  // namespace
 
@@ -193,34 +256,102 @@ struct accord_ctx {
   double f = 0, parts[3] = {0, 0, 0};
   std::vector<void*> allocs;
   size_t bytes = 0;
+  Arena arena;                             // caller-owned workspace (empty: cudaMalloc)
   std::string err;
 
-  template <typename T>
-  T* dalloc(size_t count) {
-    void* ptr = nullptr;
-    const size_t b = std::max<size_t>(count, 1) * sizeof(T);
-    CK(cudaMalloc(&ptr, b));
-    allocs.push_back(ptr);
-    bytes += b;
-    return (T*)ptr;
-  }
   void* dalloc_bytes(size_t b) {
     void* ptr = nullptr;
-    CK(cudaMalloc(&ptr, std::max<size_t>(b, 1)));
+    b = std::max<size_t>(b, 1);
+    if (arena.base) {
+      ptr = arena.alloc(b);
+      if (!ptr) {
+        char m[200];
+        std::snprintf(m, sizeof m,
+                      "workspace exhausted: %zu more bytes needed (%zu of %zu in use, largest "
+                      "free block %zu); recreate with a larger workspace",
+                      b, arena.in_use, arena.size, arena.largest_free());
+        throw Fail{ACCORD_E_CAPACITY, m};
+      }
+    } else {
+      CK(cudaMalloc(&ptr, b));
+    }
     allocs.push_back(ptr);
     bytes += b;
     return ptr;
+  }
+  template <typename T>
+  T* dalloc(size_t count) {
+    return (T*)dalloc_bytes(std::max<size_t>(count, 1) * sizeof(T));
   }
   void dfree(void* ptr, size_t b) {
     if (!ptr) return;
     auto it = std::find(allocs.begin(), allocs.end(), ptr);
     if (it != allocs.end()) allocs.erase(it);
-    cudaFree(ptr);
+    if (!arena.release(ptr)) cudaFree(ptr);
     bytes -= std::min(bytes, b);
   }
 };
 
 namespace {
+
+// Host wait for the stream. With NCCL this is a watchdog: poll the stream and
+// the communicators' asynchronous error state, and give up after
+// ACCORD_NCCL_TIMEOUT_S seconds (default 1800) -- a dead or diverged rank
+// otherwise hangs every survivor in cudaStreamSynchronize forever. On either
+// failure the communicators are aborted (they cannot be reused) and the call
+// returns ACCORD_E_NCCL.
+double nccl_timeout_s() {
+  static const double t = [] {
+    const char* e = std::getenv("ACCORD_NCCL_TIMEOUT_S");
+    const double v = e ? std::atof(e) : 0.0;
+    return v > 0 ? v : 1800.0;
+  }();
+  return t;
+}
+
+void nccl_abort(accord_ctx* c) {
+  NcclApi* api = nccl_api();
+  if (!api || !api->CommAbort) return;
+  if (c->nccl_ring) api->CommAbort(c->nccl_ring);
+  if (c->nccl) api->CommAbort(c->nccl);
+  c->nccl_ring = nullptr;
+  c->nccl = nullptr;
+}
+
+void csync(accord_ctx* c, cudaStream_t s) {
+  if (c->comm != ACCORD_COMM_NCCL || !c->nccl) {
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  NcclApi* api = nccl_api();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) CK(q);
+    if (api->CommGetAsyncError && (spin & 63) == 0) {
+      for (ncclComm_t cm : {c->nccl, c->nccl_ring}) {
+        if (!cm) continue;
+        ncclResult_t r = ncclSuccess;
+        api->CommGetAsyncError(cm, &r);
+        if (r != ncclSuccess && r != ncclInProgress) {
+          const std::string m = std::string("NCCL asynchronous error: ") + api->GetErrorString(r);
+          nccl_abort(c);
+          throw Fail{ACCORD_E_NCCL, m};
+        }
+      }
+      const double el =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > nccl_timeout_s()) {
+        nccl_abort(c);
+        throw Fail{ACCORD_E_NCCL, "NCCL watchdog: stream not done after " +
+                                      std::to_string((int)el) +
+                                      " s (a peer rank died or diverged); communicators aborted"};
+      }
+    }
+    if (spin > 2000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
 
 void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
   // d_buf (device) -> h_buf (host), summed over ranks. Synchronizes the stream.
@@ -228,7 +359,7 @@ void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
     NK(nccl_api()->AllReduce(d_buf, d_buf, count, ncclDouble, ncclSum, c->nccl, c->st));
   }
   CK(cudaMemcpyAsync(h_buf, d_buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
   if (c->world > 1 && c->comm == ACCORD_COMM_HOST) {
     if (c->ar(c->cu, h_buf, count) != 0) throw Fail{ACCORD_E_COMM, "host allreduce failed"};
   }
@@ -240,7 +371,7 @@ double allreduce_max(accord_ctx* c, double* d_val) {
   if (c->comm == ACCORD_COMM_NCCL)
     NK(nccl_api()->AllReduce(d_val, d_val, 1, ncclDouble, ncclMax, c->nccl, c->st));
   CK(cudaMemcpyAsync(&h, d_val, 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
   if (c->world > 1 && c->comm == ACCORD_COMM_HOST) {
     std::vector<double> v(c->world, 0.0);
     v[c->rank] = h;
@@ -260,10 +391,10 @@ void dev_allreduce(accord_ctx* c, double* d, int count) {
   }
   std::vector<double> h(count);
   CK(cudaMemcpyAsync(h.data(), d, count * 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
   if (c->ar(c->cu, h.data(), count) != 0) throw Fail{ACCORD_E_COMM, "host allreduce failed"};
   CK(cudaMemcpyAsync(d, h.data(), count * 8, cudaMemcpyHostToDevice, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
 }
 
 OmegaView omega_view(accord_ctx* c) { return OmegaView{c->om_ptr, c->om_col, c->om_val}; }
@@ -302,7 +433,7 @@ void ring_exchange(accord_ctx* c, int s, const void* slab, int j) {
     CK(cudaEventRecord(c->ev_recv[s & 1], c->cs));
   } else {
     CK(cudaMemcpyAsync(c->h_send, slab, sb, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    csync(c, c->st);
     if (c->sr(c->cu, c->h_send, (int64_t)sb, left, c->h_recv, (int64_t)rb, right) != 0)
       throw Fail{ACCORD_E_COMM, "host sendrecv failed"};
     CK(cudaMemcpyAsync(target, c->h_recv, rb, cudaMemcpyHostToDevice, c->st));
@@ -344,7 +475,7 @@ void build_items(accord_ctx* c, const int64_t* ptr) {
   int64_t h[2] = {0, 0};
   CK(cudaMemcpyAsync(&h[0], c->itm_ptr + c->pk, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(&h[1], c->slot_ptr + c->pk, 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
   c->n_items = h[0];
   c->n_slots = h[1];
   if (c->tma_spmm && c->n_slots > c->part_slots) {
@@ -424,48 +555,98 @@ void refine_all(accord_ctx* c, const void* yrows = nullptr) {
 }
 
 // (Re)allocate the entry-indexed arrays for capacity `cap`, preserving Omega.
+// Candidate-indexed arrays (C, sort keys, pool) at capacity `cap`; on an
+// allocation failure the ones allocated are released and the error rethrown.
+void alloc_entry_arrays(accord_ctx* c, int64_t cap) {
+  const size_t T = c->tsz;
+  const bool vals = c->gemm != ACCORD_GEMM_BF16_FILTER;   // the filter emits positions only
+  int64_t ch = cap, nch = 1;
+  if (c->gemm_warps != 0) {
+    // the tcgen05 epilogue warps take private chunks of 2048..8192 entries
+    // (>= one emission batch: 32 rows x 32 columns, twice that when the
+    // symmetric first GEMM mirrors its survivors); SIMT: one chunk
+    ch = 8192;
+    while (ch > 2048 && cap / ch < 4 * (int64_t)c->gemm_warps) ch >>= 1;
+    nch = std::max<int64_t>(1, cap / ch);
+  }
+  struct A {
+    void** dst;
+    size_t bytes;
+  } list[] = {{(void**)&c->c_col, (size_t)cap * 4},      {(void**)&c->c_g, (size_t)cap * T},
+              {(void**)&c->c_w, (size_t)cap * T},        {(void**)&c->c_wn, (size_t)cap * T},
+              {(void**)&c->c_wn2, (size_t)cap * T},      {(void**)&c->keys, (size_t)cap * 8},
+              {(void**)&c->keys_tmp, (size_t)cap * 8},   {(void**)&c->pool_row, (size_t)cap * 4},
+              {(void**)&c->pool_col, (size_t)cap * 4},
+              {(void**)&c->pool_g, vals ? (size_t)cap * T : 0},
+              {(void**)&c->pool_w, vals ? (size_t)cap * T : 0},
+              {(void**)&c->chunk_fill, (size_t)nch * 8}};
+  size_t k = 0;
+  try {
+    for (; k < sizeof(list) / sizeof(list[0]); ++k)
+      *list[k].dst = list[k].bytes ? c->dalloc_bytes(list[k].bytes) : nullptr;
+  } catch (...) {
+    for (size_t j = 0; j < k; ++j) {
+      c->dfree(*list[j].dst, list[j].bytes);
+      *list[j].dst = nullptr;
+    }
+    throw;
+  }
+  c->chunk = ch;
+  c->nchunks = nch;
+}
+
+void free_entry_arrays(accord_ctx* c, int64_t cap) {
+  const size_t T = c->tsz;
+  c->dfree(c->c_col, cap * 4);     c->c_col = nullptr;
+  c->dfree(c->c_g, cap * T);       c->c_g = nullptr;
+  c->dfree(c->c_w, cap * T);       c->c_w = nullptr;
+  c->dfree(c->c_wn, cap * T);      c->c_wn = nullptr;
+  c->dfree(c->c_wn2, cap * T);     c->c_wn2 = nullptr;
+  c->dfree(c->keys, cap * 8);      c->keys = nullptr;
+  c->dfree(c->keys_tmp, cap * 8);  c->keys_tmp = nullptr;
+  c->dfree(c->pool_row, cap * 4);  c->pool_row = nullptr;
+  c->dfree(c->pool_col, cap * 4);  c->pool_col = nullptr;
+  c->dfree(c->pool_g, cap * T);    c->pool_g = nullptr;
+  c->dfree(c->pool_w, cap * T);    c->pool_w = nullptr;
+  c->dfree(c->chunk_fill, c->nchunks * 8);
+  c->chunk_fill = nullptr;
+}
+
+// (Re)allocate the entry-indexed arrays for capacity `cap`, preserving Omega.
+// Transactional: if the new arrays do not fit (a caller workspace that is too
+// small), the context keeps a valid state at the old capacity and the error
+// (ACCORD_E_CAPACITY / NOMEM) propagates; nothing of the iterate is lost.
 void grow(accord_ctx* c, int64_t cap, int64_t keep_nnz) {
   const size_t T = c->tsz;
+  const int64_t oc = c->cap;
+  // Omega first, copied (the old arrays stay until the new ones exist)
   int32_t* om_col = c->dalloc<int32_t>(cap);
-  void* om_val = c->dalloc_bytes(cap * T);
+  void* om_val = nullptr;
+  try {
+    om_val = c->dalloc_bytes(cap * T);
+  } catch (...) {
+    c->dfree(om_col, cap * 4);
+    throw;
+  }
   if (c->om_col && keep_nnz > 0) {
     CK(cudaMemcpyAsync(om_col, c->om_col, keep_nnz * 4, cudaMemcpyDeviceToDevice, c->st));
     CK(cudaMemcpyAsync(om_val, c->om_val, keep_nnz * T, cudaMemcpyDeviceToDevice, c->st));
-    CK(cudaStreamSynchronize(c->st));
   }
-  const int64_t oc = c->cap;
+  csync(c, c->st);
   c->dfree(c->om_col, oc * 4);
   c->dfree(c->om_val, oc * T);
   c->om_col = om_col;
   c->om_val = om_val;
-  c->dfree(c->c_col, oc * 4);   c->c_col = c->dalloc<int32_t>(cap);
-  c->dfree(c->c_g, oc * T);     c->c_g = c->dalloc_bytes(cap * T);
-  c->dfree(c->c_w, oc * T);     c->c_w = c->dalloc_bytes(cap * T);
-  c->dfree(c->c_wn, oc * T);    c->c_wn = c->dalloc_bytes(cap * T);
-  c->dfree(c->c_wn2, oc * T);   c->c_wn2 = c->dalloc_bytes(cap * T);
-  c->dfree(c->keys, oc * 8);    c->keys = c->dalloc<uint64_t>(cap);
-  c->dfree(c->keys_tmp, oc * 8); c->keys_tmp = c->dalloc<uint64_t>(cap);
-  c->dfree(c->pool_row, oc * 4); c->pool_row = c->dalloc<int32_t>(cap);
-  c->dfree(c->pool_col, oc * 4); c->pool_col = c->dalloc<int32_t>(cap);
-  // the BF16 filter's epilogue emits positions only (values: refine + lookup)
-  const bool vals = c->gemm != ACCORD_GEMM_BF16_FILTER;
-  c->dfree(c->pool_g, oc * T);  c->pool_g = vals ? c->dalloc_bytes(cap * T) : nullptr;
-  c->dfree(c->pool_w, oc * T);  c->pool_w = vals ? c->dalloc_bytes(cap * T) : nullptr;
-  c->cap = cap;
-  // chunking: the SIMT GEMM uses one chunk; the tcgen05 epilogue warps take
-  // private chunks of 2048..8192 entries (>= one emission batch: 32 rows x 32
-  // columns, twice that when the symmetric first GEMM mirrors its survivors)
-  c->dfree(c->chunk_fill, c->nchunks * 8);
-  if (c->gemm_warps == 0) {
-    c->chunk = cap;
-    c->nchunks = 1;
-  } else {
-    int64_t ch = 8192;
-    while (ch > 2048 && cap / ch < 4 * (int64_t)c->gemm_warps) ch >>= 1;
-    c->chunk = ch;
-    c->nchunks = std::max<int64_t>(1, cap / ch);
+  // C / keys / pool: contents are rebuilt by the next GEMM
+  if (oc > 0) free_entry_arrays(c, oc);
+  try {
+    alloc_entry_arrays(c, cap);
+  } catch (...) {
+    if (oc > 0) alloc_entry_arrays(c, oc);   // the blocks just freed: fits again
+    c->cap = oc;                              // (Omega's arrays are larger: fine)
+    throw;
   }
-  c->chunk_fill = c->dalloc<unsigned long long>(c->nchunks);
+  c->cap = cap;
 }
 
 // Objective and nnz of the current Omega (collective). Y[cur] must be current
@@ -480,7 +661,7 @@ void refresh_objective(accord_ctx* c) {
   double loc[8];
   CK(cudaMemcpyAsync(&bad, c->bad_diag, 4, cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(loc, c->red_d, sizeof(loc), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
   c->nnz_local = (int64_t)loc[5];
   loc[7] = bad ? 1.0 : 0.0;   // make the domain check collective
   CK(cudaMemcpyAsync(c->red_d, loc, sizeof(loc), cudaMemcpyHostToDevice, c->st));
@@ -536,6 +717,93 @@ void validate(const accord_init_params* prm) {
     bad("tensor-core GEMM kinds need dtype F32");
 }
 
+// Default candidate-pool capacity (entries): the first iteration (G = S) has
+// the most candidates (config 5: ~380 per row), so size for ~512 per row.
+int64_t default_capacity(int64_t pk, int64_t p) {
+  const int64_t dense = pk * p;
+  int64_t cap = std::min<int64_t>(dense, std::max<int64_t>(pk * 512, 1 << 20));
+  return std::max<int64_t>(cap, std::min<int64_t>(dense, pk * 16));
+}
+
+// Device bytes accord_create takes for `prm` (mirrors create_impl buffer by
+// buffer, each rounded to the 256-B arena granule), for the workspace query.
+// Pure host arithmetic: no CUDA call. Upper bound: AUTO is resolved as on an
+// sm_100 device (tensor-core operand copies), the sharded ring buffers assume
+// no rank's slab exceeds max(p_k, ceil(p / world)) rows, and the per-iteration
+// scratch of hub rows (work items split at kItemEntries) is reserved for
+// 64 + p_k / 64 split slots.
+struct Footprint {
+  size_t total = 0, transient = 0;
+  int64_t cap = 0;
+};
+Footprint footprint(const accord_init_params* prm) {
+  auto R = [](size_t b) { return (std::max<size_t>(b, 1) + 255) & ~(size_t)255; };
+  Footprint f;
+  const int64_t n = prm->n, p = prm->p, pk = prm->row_end - prm->row_begin;
+  const int64_t ldk = round_up(n, kKPad), p_pad = round_up(p, kRowPad),
+                pk_pad = round_up(pk, kRowPad);
+  const size_t T = prm->dtype == ACCORD_F64 ? 8 : 4;
+  int gemm = prm->gemm;
+  if (gemm == ACCORD_GEMM_AUTO)
+    gemm = prm->dtype == ACCORD_F32 ? (ldk <= 4096 ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_BF16X3)
+                                    : ACCORD_GEMM_SIMT;
+  const bool x3 = gemm == ACCORD_GEMM_BF16X3, filt = gemm == ACCORD_GEMM_BF16_FILTER,
+             tc = x3 || filt;
+  const bool sharded = prm->x_sharded && prm->world > 1;
+  const int64_t pv = sharded ? pk : p;
+  const int64_t xrows_pad = sharded ? pk_pad : p_pad;
+  size_t a = 0;
+  a += R(16 * 8);                                      // red_d
+  a += R((size_t)xrows_pad * ldk * T);                 // Xt
+  a += R(8);                                           // bad index
+  // transient: host staging of X, or the Lanczos vectors (freed before Y)
+  size_t tr = 0;
+  if (!prm->x_on_device) {
+    tr = R((size_t)n * pv * T);
+  }
+  if (!(prm->inv_L > 0)) {
+    const int64_t nsplit = std::min<int64_t>(256, std::max<int64_t>(1, pv / 256));
+    tr = std::max(tr, 2 * R(ldk * 8) + R(std::max<int64_t>(pv, 1) * 8) + R(nsplit * ldk * 8));
+  }
+  a += 2 * R((size_t)pk_pad * ldk * T);                // Y (x2)
+  if (tc) {
+    a += R((size_t)xrows_pad * ldk * 2) * (x3 ? 2 : 1); // X^T bf16 (hi, lo)
+    a += 2 * R((size_t)pk_pad * ldk * 2) * (x3 ? 2 : 1); // Y bf16 (x2)
+    a += 4 * R(pk * 4);                                // row_A, row_B (x2)
+    if (filt) a += R(p * 8);                           // col_sd
+    a += R((p_pad / kRowPad) * 8);                     // tile maxima of col_sd
+  }
+  if (sharded) {
+    const int64_t rr = std::max(pk_pad, round_up((p + prm->world - 1) / prm->world, kRowPad));
+    a += 2 * R((size_t)rr * ldk * T);                  // ring buffers
+    if (tc) a += 2 * R((size_t)rr * ldk * 2) * (x3 ? 2 : 1);
+    a += 2 * R((size_t)pk_pad * ldk * 8);              // yacc, dacc
+  }
+  a += 2 * R((pk + 1) * 8) + 2 * R(pk * 4) + R((pk + 1) * 4) + R(4);   // om/c ptr, counts
+  a += 9 * R(pk * 8) + 2 * R(pk * 4) + 4 * R(pk * 8) + R(4);          // per-row sums
+  a += R(scan_tmp_bytes(pk + 1));
+  a += 2 * R(pk * 4) + 2 * R((pk + 1) * 8) + R(pk * 4);               // work-item maps
+  const int64_t cap = std::min<int64_t>(prm->cand_capacity > 0 ? std::max(prm->cand_capacity, pk)
+                                                               : default_capacity(pk, p),
+                                        (int64_t)UINT32_MAX);
+  f.cap = cap;
+  size_t pool = R(cap * 4) + R(cap * T)                // Omega col, val
+                + R(cap * 4) + 4 * R(cap * T)          // C col, g, w, w+, w+'
+                + 2 * R(cap * 8)                       // sort keys
+                + 2 * R(cap * 4)                       // pool positions
+                + (filt ? 0 : 2 * R(cap * T))          // pool values (BF16X3, SIMT)
+                + R((cap / 2048 + 1) * 8);             // chunk fill counts
+  a += pool;
+  // work items of C: <= p_k + cap / L items; split-row slots reserved
+  const int64_t items = pk + cap / kItemEntries + 1024;
+  a += 3 * R(items * 8) + 2 * R(items * 4);
+  const bool tma = !sharded && spmm_tma_supported(prm->dtype, ldk) && pk >= 65536;
+  if (tma || std::getenv("ACCORD_SPMM_TMA")) a += 3 * R((size_t)(64 + pk / 64) * ldk * 8);
+  f.transient = tr;
+  f.total = a + tr;
+  return f;
+}
+
 // All ranks' per-column filter constants into every rank's col_sd[p]
 // (sharded mode; each rank computed its slab's at col_sd + r0).
 void gather_col_sd(accord_ctx* c) {
@@ -547,14 +815,14 @@ void gather_col_sd(accord_ctx* c) {
       NK(api->Broadcast(c->col_sd + c->vb[q], c->col_sd + c->vb[q],
                         (size_t)slab_rows(c, q) * sizeof(float2), ncclChar, q, c->nccl, c->st));
     NK(api->GroupEnd());
-    CK(cudaStreamSynchronize(c->st));
+    csync(c, c->st);
     return;
   }
   if (!c->agv) throw Fail{ACCORD_E_INVALID, "x_sharded with host comm needs allgatherv"};
   std::vector<float2> mine(c->pk), all(c->p);
   CK(cudaMemcpyAsync(mine.data(), c->col_sd + c->r0, c->pk * sizeof(float2),
                      cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
   std::vector<int64_t> counts(P, 0);
   const int64_t bytes = c->pk * (int64_t)sizeof(float2);
   if (c->agv(c->cu, mine.data(), bytes, nullptr, counts.data()) != 0 ||
@@ -562,7 +830,7 @@ void gather_col_sd(accord_ctx* c) {
     throw Fail{ACCORD_E_COMM, "allgatherv failed"};
   CK(cudaMemcpyAsync(c->col_sd, all.data(), c->p * sizeof(float2), cudaMemcpyHostToDevice,
                      c->st));
-  CK(cudaStreamSynchronize(c->st));
+  csync(c, c->st);
 }
 
 // Largest eigenvalue of the symmetric tridiagonal matrix (alpha, beta) by
@@ -626,7 +894,7 @@ double lanczos_lmax(accord_ctx* c, int64_t pv) {
     c->launches += launch_gram_apply(c->dtype, c->Xt, pv, c->n, N, u, t, part, nsplit, w, c->st);
     if (c->sharded) dev_allreduce(c, w, (int)N);
     CK(cudaMemcpyAsync(wv.data(), w, N * 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    csync(c, c->st);
     const double* q = &Q[(size_t)j * N];
     double al = 0.0;
     for (int64_t i = 0; i < N; ++i) al += wv[i] * q[i];
@@ -658,6 +926,10 @@ double lanczos_lmax(accord_ctx* c, int64_t pv) {
 
 void create_impl(accord_ctx* c, const accord_init_params* prm) {
   validate(prm);
+  if (prm->workspace) {
+    if (prm->workspace_bytes == 0) throw Fail{ACCORD_E_INVALID, "workspace_bytes is 0"};
+    c->arena.init(prm->workspace, prm->workspace_bytes);
+  }
   if (prm->device >= 0) CK(cudaSetDevice(prm->device));
   CK(cudaGetDevice(&c->device));
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
@@ -765,7 +1037,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   const void* Xsrc = prm->X;
   void* staging = nullptr;
   if (!prm->x_on_device) {
-    CK(cudaMalloc(&staging, (size_t)rows_src * cols_src * T));
+    staging = c->dalloc_bytes((size_t)rows_src * cols_src * T);
     if (ldx == cols_src)   // dense: one linear copy (a 2-D copy of 4 KB rows is ~8x slower)
       CK(cudaMemcpyAsync(staging, prm->X, (size_t)rows_src * cols_src * T,
                          cudaMemcpyHostToDevice, c->st));
@@ -780,8 +1052,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
                                 c->n, pv, c->Xt, c->ldk, c->xrows_pad, badidx, c->st);
   unsigned long long hb = 0;
   CK(cudaMemcpyAsync(&hb, badidx, 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  if (staging) cudaFree(staging);
+  csync(c, c->st);
+  if (staging) c->dfree(staging, (size_t)rows_src * cols_src * T);
   if (hb != ~0ull) {
     char m[160];
     std::snprintf(m, sizeof m, "non-finite X at (row %lld, col %lld) of the given layout",
@@ -837,9 +1109,11 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
       if (c->sharded) gather_col_sd(c);
     }
     std::string e;
+    float2* bsd = c->dalloc<float2>(c->p_pad / kRowPad);
+    CK(cudaMemsetAsync(bsd, 0, (c->p_pad / kRowPad) * sizeof(float2), c->st));
     c->plan = tc_plan_create(c->Yhi[0], x3 ? c->Ylo[0] : c->Yhi[0], c->Yhi[1],
                              x3 ? c->Ylo[1] : c->Yhi[1], c->pk_pad, c->Xhi,
-                             x3 ? c->Xlo : c->Xhi, c->xrows_pad, c->p_pad, c->n, c->ldk, &e);
+                             x3 ? c->Xlo : c->Xhi, c->xrows_pad, c->p_pad, c->n, c->ldk, bsd, &e);
     if (!c->plan) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
     if (filt) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
   }
@@ -919,14 +1193,17 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   int64_t cap = prm->cand_capacity;
   if (cap <= 0) {
     // The first iteration (G = S) has the most candidates (config 5: ~365 per
-    // row); size for it so that it is not recomputed, within 40% of the free
-    // device memory (~52 B per entry across pool, C, keys and Omega arrays).
-    const int64_t dense = c->pk * c->p;
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    const int64_t mem_cap = (int64_t)(0.4 * (double)fr / 52.0);
-    cap = std::min<int64_t>(dense, std::max<int64_t>(c->pk * 512, 1 << 20));
-    cap = std::max<int64_t>(std::min(cap, mem_cap), std::min<int64_t>(dense, c->pk * 16));
+    // row); size for it so that it is not recomputed (~52 B per entry across
+    // pool, C, keys and Omega arrays): within 40% of the free device memory,
+    // or exactly the default the workspace query assumed.
+    cap = default_capacity(c->pk, c->p);
+    if (!c->arena.base) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const int64_t mem_cap = (int64_t)(0.4 * (double)fr / 52.0);
+      cap = std::max<int64_t>(std::min(cap, mem_cap),
+                              std::min<int64_t>(c->pk * c->p, c->pk * 16));
+    }
   }
   cap = std::max<int64_t>(cap, c->pk);
   grow(c, std::min<int64_t>(cap, (int64_t)UINT32_MAX), 0);
@@ -1094,7 +1371,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       unsigned int used = 0;
       CK(cudaMemcpyAsync(&used, c->chunk_next, 4, cudaMemcpyDeviceToHost, S));
       CK(cudaMemcpyAsync(c->h_seg, c->chunk_fill, 8, cudaMemcpyDeviceToHost, S));
-      CK(cudaStreamSynchronize(S));
+      csync(c, S);
       c->h_seg[1] = used;
     }
     st.ms_gemm += ev_ms(c, 1, 2);
@@ -1386,7 +1663,7 @@ double lambda_max_impl(accord_ctx* c) {
   build_candidates(c, st, &ov);                      // pass 1: certified lower bound
   unsigned int hm = 0;
   CK(cudaMemcpyAsync(&hm, dmax, 4, cudaMemcpyDeviceToHost, S));
-  CK(cudaStreamSynchronize(S));
+  csync(c, S);
   float lb = 0.f;
   std::memcpy(&lb, &hm, 4);
   double lbd = (double)lb;
@@ -1439,7 +1716,7 @@ void gather_host(accord_ctx* c, bool fetch, int64_t* total_out, std::vector<int6
     CK(cudaMemcpyAsync(lp.data(), c->om_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(lc.data(), c->om_col, c->nnz_local * 4, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(lv.data(), c->om_val, c->nnz_local * T, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    csync(c, c->st);
     std::vector<int64_t>& gp = *gp_out;
     std::vector<int32_t>& gc = *gc_out;
     std::vector<char>& gv = *gv_out;
@@ -1451,9 +1728,9 @@ void gather_host(accord_ctx* c, bool fetch, int64_t* total_out, std::vector<int6
       int64_t* dptr = nullptr;
       int32_t* dcol = nullptr;
       char* dval = nullptr;
-      CK(cudaMalloc(&dptr, (rows_total + c->world) * 8));
-      CK(cudaMalloc(&dcol, std::max<int64_t>(total, 1) * 4));
-      CK(cudaMalloc(&dval, std::max<int64_t>(total, 1) * T));
+      dptr = c->dalloc<int64_t>(rows_total + c->world);
+      dcol = c->dalloc<int32_t>(std::max<int64_t>(total, 1));
+      dval = c->dalloc<char>(std::max<int64_t>(total, 1) * T);
       int64_t ro = 0, eo = 0;
       NK(api->GroupStart());
       for (int q = 0; q < c->world; ++q) {
@@ -1475,10 +1752,10 @@ void gather_host(accord_ctx* c, bool fetch, int64_t* total_out, std::vector<int6
       CK(cudaMemcpyAsync(hp.data(), dptr, hp.size() * 8, cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(gc.data(), dcol, total * 4, cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(gv.data(), dval, total * T, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      cudaFree(dptr);
-      cudaFree(dcol);
-      cudaFree(dval);
+      csync(c, c->st);
+      c->dfree(dptr, (rows_total + c->world) * 8);
+      c->dfree(dcol, std::max<int64_t>(total, 1) * 4);
+      c->dfree(dval, std::max<int64_t>(total, 1) * T);
       ro = 0;
       eo = 0;
       for (int q = 0; q < c->world; ++q) {
@@ -1542,6 +1819,25 @@ void accord_default_params(accord_init_params* prm) {
   prm->comm = ACCORD_COMM_NONE;
 }
 
+accord_status accord_workspace_size(const accord_init_params* prm, size_t* bytes) {
+  g_create_err.clear();
+  if (!bytes) {
+    g_create_err = "bytes is NULL";
+    return ACCORD_E_INVALID;
+  }
+  try {
+    validate(prm);
+    *bytes = footprint(prm).total + 4096;   // + the arena's alignment slack
+    return ACCORD_OK;
+  } catch (const Fail& f) {
+    g_create_err = f.msg;
+    return f.s;
+  } catch (...) {
+    g_create_err = "internal error";
+    return ACCORD_E_INVALID;
+  }
+}
+
 accord_status accord_create(accord_ctx** out, const accord_init_params* prm) {
   g_create_err.clear();
   if (!out) {
@@ -1593,7 +1889,7 @@ accord_status accord_export_csr(accord_ctx* c, int32_t scope, int64_t* row_ptr, 
       CK(cudaMemcpyAsync(row_ptr, c->om_ptr, (c->pk + 1) * 8, k, c->st));
       CK(cudaMemcpyAsync(col, c->om_col, c->nnz_local * 4, k, c->st));
       CK(cudaMemcpyAsync(val, c->om_val, c->nnz_local * T, k, c->st));
-      CK(cudaStreamSynchronize(c->st));
+      csync(c, c->st);
       return;
     }
     if (scope != ACCORD_SCOPE_GATHER) throw Fail{ACCORD_E_INVALID, "bad scope"};
@@ -1628,15 +1924,18 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
     const size_t T = c->tsz;
     cudaStream_t S = c->st;
     // temporaries of this call only
-    std::vector<void*> tmp;
+    std::vector<std::pair<void*, size_t>> tmp;
     struct Free {
-      std::vector<void*>& v;
-      ~Free() { for (void* q : v) cudaFree(q); }
-    } fr{tmp};
+      accord_ctx* c;
+      std::vector<std::pair<void*, size_t>>& v;
+      ~Free() {
+        if (c->st) cudaStreamSynchronize(c->st);
+        for (auto& q : v) c->dfree(q.first, q.second);
+      }
+    } fr{c, tmp};
     auto talloc = [&](size_t b) {
-      void* q = nullptr;
-      CK(cudaMalloc(&q, std::max<size_t>(b, 1)));
-      tmp.push_back(q);
+      void* q = c->dalloc_bytes(b);
+      tmp.push_back({q, b});
       return q;
     };
     // The input CSR: this rank's block (THETA of the local rows, or P = 1) or the
@@ -1658,7 +1957,7 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
       CK(cudaMemcpyAsync(dp, gp.data(), gp.size() * 8, cudaMemcpyHostToDevice, S));
       CK(cudaMemcpyAsync(dc, gc.data(), gc.size() * 4, cudaMemcpyHostToDevice, S));
       CK(cudaMemcpyAsync(dv, gv.data(), gv.size(), cudaMemcpyHostToDevice, S));
-      CK(cudaStreamSynchronize(S));   // the host vectors go out of scope
+      csync(c, S);   // the host vectors go out of scope
       iptr = dp;
       icol = dc;
       ival = dv;
@@ -1681,7 +1980,7 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
     CK(cudaMemcpyAsync(h_ab + 1, iptr + b, 8, cudaMemcpyDeviceToHost, S));
     int32_t hbad = 0;
     CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, S));
-    CK(cudaStreamSynchronize(S));
+    csync(c, S);
     if (hbad) throw Fail{ACCORD_E_DOMAIN, "Omega has a missing or nonpositive diagonal entry"};
     int64_t nnz = 0;
     if (kind == ACCORD_EXPORT_THETA) {
@@ -1692,11 +1991,11 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
       optr = (int64_t*)talloc((rows + 1) * 8);
       std::vector<int64_t> hp(rows + 1);
       CK(cudaMemcpyAsync(hp.data(), iptr + a, (rows + 1) * 8, cudaMemcpyDeviceToHost, S));
-      CK(cudaStreamSynchronize(S));
+      csync(c, S);
       for (auto& x : hp) x -= h_ab[0];
       CK(cudaMemcpyAsync(optr, hp.data(), (rows + 1) * 8, cudaMemcpyHostToDevice, S));
       ocol = const_cast<int32_t*>(icol) + h_ab[0];
-      CK(cudaStreamSynchronize(S));
+      csync(c, S);
     } else {
       int32_t* own = (int32_t*)talloc(rows * 4);
       int32_t* cnt = (int32_t*)talloc(rows * 4);
@@ -1711,7 +2010,7 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
       void* stmp = talloc(scan_tmp_bytes(rows + 1));
       c->launches += launch_scan_i32(cnt, optr, rows, stmp, scan_tmp_bytes(rows + 1), S);
       CK(cudaMemcpyAsync(&nnz, optr + rows, 8, cudaMemcpyDeviceToHost, S));
-      CK(cudaStreamSynchronize(S));
+      csync(c, S);
       uint64_t* keys = (uint64_t*)talloc(nnz * 8);
       uint64_t* ktmp = (uint64_t*)talloc(nnz * 8);
       c->launches += launch_pcorr_fill(c->dtype, irows, a, b, iptr, icol, ival, own, optr, ext,
@@ -1725,7 +2024,7 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
     CK(cudaGetLastError());
     *nnz_out = nnz;
     if (!row_ptr) {
-      CK(cudaStreamSynchronize(S));
+      csync(c, S);
       return;
     }
     if (capacity < nnz) throw Fail{ACCORD_E_CAPACITY, "capacity too small"};
@@ -1733,7 +2032,7 @@ accord_status accord_export_transformed(accord_ctx* c, int32_t kind, int32_t sco
     CK(cudaMemcpyAsync(row_ptr, optr, (rows + 1) * 8, k, S));
     CK(cudaMemcpyAsync(col, ocol, nnz * 4, k, S));
     CK(cudaMemcpyAsync(val, oval, nnz * T, k, S));
-    CK(cudaStreamSynchronize(S));
+    csync(c, S);
   });
 }
 
@@ -1876,7 +2175,7 @@ accord_status accord_path(accord_ctx* c, const double* lambdas, int32_t k, int32
     CK(cudaMemcpyAsync(c->om_ptr, bptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, c->st));
     CK(cudaMemcpyAsync(c->om_col, bcol, bnnz * 4, cudaMemcpyDeviceToDevice, c->st));
     CK(cudaMemcpyAsync(c->om_val, bval, bnnz * T, cudaMemcpyDeviceToDevice, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    csync(c, c->st);
     c->dfree(bptr, (c->pk + 1) * 8);
     c->dfree(bcol, bcap * 4);
     c->dfree(bval, bcap * T);
@@ -1943,13 +2242,13 @@ accord_status accord_filter_audit(accord_ctx* c, float* acc, int64_t ld, float* 
     if (gamma) *gamma = (double)(float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
     int64_t nc = 0;
     CK(cudaMemcpyAsync(&nc, c->c_ptr + c->pk, 8, cudaMemcpyDeviceToHost, S));
-    CK(cudaStreamSynchronize(S));
+    csync(c, S);
     *n_cand = nc;
     if (!c_ptr) return;
     if (capacity < nc) throw Fail{ACCORD_E_CAPACITY, "capacity too small"};
     CK(cudaMemcpyAsync(c_ptr, c->c_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToHost, S));
     CK(cudaMemcpyAsync(c_col, c->c_col, nc * 4, cudaMemcpyDeviceToHost, S));
-    CK(cudaStreamSynchronize(S));
+    csync(c, S);
   });
 }
 
@@ -1960,7 +2259,7 @@ accord_status accord_row_stats(accord_ctx* c, const int64_t* rows, int64_t count
     std::vector<double> a(c->pk), b(c->pk);
     CK(cudaMemcpyAsync(a.data(), c->row_D2, c->pk * 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(b.data(), c->row_dd, c->pk * 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    csync(c, c->st);
     for (int64_t q = 0; q < count; ++q) {
       if (rows[q] < 0 || rows[q] >= c->pk) throw Fail{ACCORD_E_INVALID, "row out of range"};
       if (d2) d2[q] = a[rows[q]];
@@ -1994,6 +2293,8 @@ accord_status accord_get_info(accord_ctx* c, accord_info* info) {
   info->gemm_launches = c->gemm_launches;
   info->f = c->f;
   info->device_bytes = c->bytes;
+  info->workspace_bytes = c->arena.size;
+  info->workspace_high = c->arena.high;
   return ACCORD_OK;
 }
 

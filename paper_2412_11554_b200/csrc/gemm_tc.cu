@@ -612,7 +612,7 @@ struct TcGemmPlan {
   // X^T_hi (Omega = I operand of the lambda_max pass, tc_plan_set_a)
   CUtensorMap a_hi[3], a_lo[3], b_hi[3], b_lo[3];
   int64_t pk_pad = 0, p_pad = 0, ldk = 0, kdim = 0;   // p_pad: padded column count (all p)
-  float2* blk_sdmax = nullptr;   // [p_pad / 256] (BF16_FILTER)
+  float2* blk_sdmax = nullptr;   // [p_pad / 256] (BF16_FILTER; caller-owned, zeroed)
 };
 
 bool tc_supported(int cc_major, int cc_minor) { return cc_major == 10 && cc_minor == 0; }
@@ -620,7 +620,8 @@ bool tc_supported(int cc_major, int cc_minor) { return cc_major == 10 && cc_mino
 TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            const __nv_bfloat16* Yhi1, const __nv_bfloat16* Ylo1, int64_t pk_pad,
                            const __nv_bfloat16* Xhi, const __nv_bfloat16* Xlo, int64_t xrows_pad,
-                           int64_t p_pad, int64_t kdim, int64_t ldk, std::string* err) {
+                           int64_t p_pad, int64_t kdim, int64_t ldk, float2* blk_sdmax,
+                           std::string* err) {
   auto* p = new TcGemmPlan();
   if (std::getenv("ACCORD_GEMM_KFULL")) kdim = ldk;   // A-B diagnostic: no K-tail trim
   p->pk_pad = pk_pad;
@@ -637,15 +638,11 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
   p->b_lo[1] = p->b_lo[2] = p->b_lo[0];
   p->a_hi[2] = p->a_hi[0];
   p->a_lo[2] = p->a_lo[0];
-  if (ok && cudaMalloc(&p->blk_sdmax, (p_pad / BN) * sizeof(float2)) != cudaSuccess) {
-    *err = "alloc";
-    ok = false;
-  }
+  p->blk_sdmax = blk_sdmax;   // owned by the caller
   if (!ok) {
     delete p;
     return nullptr;
   }
-  cudaMemset(p->blk_sdmax, 0, (p_pad / BN) * sizeof(float2));
   static unsigned long long attr_seen = 0;
   if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(gemm_tc_kernel<0, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -685,7 +682,6 @@ int tc_plan_set_col_norms(TcGemmPlan* p, const float2* col_sd, int64_t pcols, cu
 
 void tc_plan_destroy(TcGemmPlan* p) {
   if (!p) return;
-  if (p->blk_sdmax) cudaFree(p->blk_sdmax);
   delete p;
 }
 

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in decl if not hasattr(L, n)]
     assert not missing, missing
     assert set(decl) == set(A.EXPORTED)
-    assert A.lib().accord_abi_version() == 2
+    assert A.lib().accord_abi_version() == 3
 
 
 def test_status_strings_and_create_error_without_gpu():
@@ -62,6 +62,8 @@ int main(void) {
   P(accord_init_params, lambda) P(accord_init_params, row_begin) P(accord_init_params, nccl_id)
   P(accord_init_params, stream) P(accord_init_params, cand_capacity)
   P(accord_init_params, x_sharded) P(accord_init_params, sendrecv)
+  P(accord_init_params, workspace) P(accord_init_params, workspace_bytes)
+  P(accord_info, workspace_bytes) P(accord_info, workspace_high)
   P(accord_iter_stats, nnz) P(accord_iter_stats, trials) P(accord_iter_stats, ms_total)
   P(accord_info, f) P(accord_info, device_bytes) P(accord_info, kernel_launches)
   return 0;
@@ -125,3 +127,45 @@ def test_header_cites_the_paper_for_every_entry_point():
         i = h.index(name + "(")
         block = h[max(0, i - 1500):i]
         assert "/*" in block, name
+
+
+def _prm(n, p, dtype=A.F32, gemm=A.GEMM_AUTO, x_on_device=0, cap=0, inv_L=0.0, rows=None):
+    L = A.lib()
+    prm = A.InitParams()
+    L.accord_default_params(C.byref(prm))
+    prm.n, prm.p, prm.X = n, p, 1          # X is not read by the size query
+    prm.dtype, prm.gemm, prm.x_on_device = dtype, gemm, x_on_device
+    prm.lambda_, prm.inv_L, prm.cand_capacity = 0.1, inv_L, cap
+    prm.row_begin, prm.row_end = (0, p) if rows is None else rows
+    return prm
+
+
+def _size(prm):
+    b = C.c_size_t()
+    st = A.lib().accord_workspace_size(C.byref(prm), C.byref(b))
+    return st, b.value
+
+
+def test_workspace_size_query_is_pure_and_accounts_the_layout():
+    """accord_workspace_size without a GPU: config 5 needs
+    X^T (4 GB f32) + its bf16 copy (2 GB) + Y x 2 (8 GB) + their bf16 copies
+    (4 GB) + the pool at ~512 candidates per row (52 B per entry, 26.6 GB)
+    + the host-X staging (4 GB); monotone in the pool capacity; bad
+    parameters are rejected like accord_create."""
+    st, b = _size(_prm(1000, 1000000))
+    assert st == 0
+    p, ldk = 1000000, 1024
+    parts = p * ldk * 4 + p * ldk * 2 + 2 * p * ldk * 4 + 2 * p * ldk * 2 + 512 * p * 52 \
+        + 1000 * p * 4
+    assert parts <= b <= parts * 1.05, (b, parts)
+    st2, b2 = _size(_prm(1000, 1000000, x_on_device=1))
+    assert st2 == 0 and b2 < b                       # no host staging
+    st3, b3 = _size(_prm(1000, 1000000, cap=2 * 512 * 1000000))
+    assert st3 == 0 and b3 > b + 512 * p * 50
+    st4, b4 = _size(_prm(50, 100, dtype=A.F64, gemm=A.GEMM_SIMT))
+    assert st4 == 0 and 0 < b4 < 16 << 20
+    st5, _ = _size(_prm(0, 100))
+    assert st5 == 1 and b"n >= 1" in A.lib().accord_last_error(None)
+    # a rank's block needs less than the whole problem
+    st6, b6 = _size(_prm(1000, 1000000, rows=(0, 125000)))
+    assert st6 == 0 and b6 < b / 2
