@@ -250,14 +250,15 @@ int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const in
                cudaStream_t st);
 
 // lambda_max (NEXT(2)): filter row constants of A = rows of X^T (Omega = I);
-// max |c_g| over the off-diagonal entries of C -> *out; direct max over
+// max over the off-diagonal entries of C of |<x_i, x_k>| / n in float64 -> *out; direct max over
 // columns [v0, v1) of |<x_i, x_k>| / n (CUDA cores; out may be NULL: ring steps
 // accumulate into row_max with accumulate = 1, then launch once more or reduce).
 int launch_row_ab(int64_t pk, int64_t ldk, const float* Xt_rows, float* row_A, float* row_B,
                   cudaStream_t st);
-int launch_cand_offdiag_max(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr,
-                            const int32_t* c_col, const void* c_g, double* row_max, double* out,
-                            cudaStream_t st);
+int launch_cand_dot_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
+                        const int64_t* c_ptr, const int32_t* c_col, const void* Xi, const void* Xt,
+                        int64_t v0, int64_t v1, int accumulate, double* row_max, double* out,
+                        cudaStream_t st);
 int launch_gram_offdiag_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
                             const void* Xi, const void* Xt, int64_t v0, int64_t v1, int accumulate,
                             double* row_max, double* out, cudaStream_t st);

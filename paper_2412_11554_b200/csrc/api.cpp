@@ -1274,7 +1274,6 @@ struct GradOverride {
   OmegaView om;
   double lam_cand;
   unsigned int* max_out;    // != NULL: max-reduce pass only (no candidates)
-  const void* yrows;        // f32/f64 rows for the refine
   bool sym;
 };
 
@@ -1425,9 +1424,9 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
   }
   CK(cudaEventRecord(c->ev[3], S));
   TR(c, "finalize");
-  if (c->gemm == ACCORD_GEMM_BF16_FILTER) {
+  if (c->gemm == ACCORD_GEMM_BF16_FILTER && !ov) {
     // exact values of the filtered candidates: G_ik = <Y_i, X_k> / n (f64 accumulation)
-    refine_all(c, ov ? ov->yrows : nullptr);
+    refine_all(c);
   }
   CK(cudaEventRecord(c->ev[4], S));
   TR(c, "refine");
@@ -1656,7 +1655,7 @@ double lambda_max_impl(accord_ctx* c) {
   CK(cudaMemsetAsync(eptr, 0, (c->pk + 1) * 8, S));
   CK(cudaMemsetAsync(dmax, 0, 4, S));
   c->launches += launch_row_ab(c->pk, c->ldk, (const float*)xrows, rA, rB, S);
-  GradOverride ov{2, rA, rB, OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax, xrows,
+  GradOverride ov{2, rA, rB, OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax,
                   c->world == 1 && !c->sharded && c->r0 == 0 && c->pk == c->p &&
                       !std::getenv("ACCORD_GEMM_NOSYM")};
   accord_iter_stats st{};
@@ -1674,10 +1673,19 @@ double lambda_max_impl(accord_ctx* c) {
   }
   ov.max_out = nullptr;
   ov.lam_cand = std::max(0.0, lbd / (double)c->n * (1.0 - 1e-6));
-  build_candidates(c, st, &ov);                      // pass 2: candidates + exact refine
+  build_candidates(c, st, &ov);                      // pass 2: the candidates near the max
   c->items_of = nullptr;
-  c->launches += launch_cand_offdiag_max(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_g, rmax,
-                                         dout, S);
+  // their values exactly (float64 dots of the f32 data)
+  if (!c->sharded) {
+    c->launches += launch_cand_dot_max(c->dtype, c->pk, c->r0, c->n, c->ldk, c->c_ptr, c->c_col,
+                                       xrows, c->Xt, 0, c->p, 0, rmax, dout, S);
+  } else {
+    ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool first, bool last) {
+      c->launches += launch_cand_dot_max(c->dtype, c->pk, c->r0, c->n, c->ldk, c->c_ptr, c->c_col,
+                                         xrows, slab, v0, v1, first ? 0 : 1, rmax,
+                                         last ? dout : nullptr, S);
+    });
+  }
   CK(cudaGetLastError());
   return allreduce_max(c, dout);
 }

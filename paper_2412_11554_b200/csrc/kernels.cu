@@ -764,19 +764,31 @@ __global__ void xrow_ab_kernel(int64_t pk, int64_t ldk, const float* __restrict_
   }
 }
 
-// Per-row max of |c_g| over the OFF-diagonal entries of C (warp per row).
+// Per-row max over the OFF-diagonal entries (i,k) of C, columns [v0, v1), of
+// |<x_i, x_k>| / n recomputed in float64 (warp per row, warp per entry).
+// Xi = the rank's row r of X^T; Xt row 0 = column v0.
 template <typename T>
-__global__ void cand_offdiag_max_kernel(int64_t pk, int64_t r0, const int64_t* __restrict__ c_ptr,
-                                        const int32_t* __restrict__ c_col,
-                                        const T* __restrict__ c_g, double* __restrict__ row_max) {
+__global__ void cand_dot_max_kernel(int64_t pk, int64_t r0, int64_t n, int64_t ldk,
+                                    const int64_t* __restrict__ c_ptr,
+                                    const int32_t* __restrict__ c_col, const T* __restrict__ Xi,
+                                    const T* __restrict__ Xt, int64_t v0, int64_t v1,
+                                    int accumulate, double* __restrict__ row_max) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= pk) return;
-  double mx = 0.0;
-  for (int64_t e = c_ptr[r] + lane; e < c_ptr[r + 1]; e += 32)
-    if (c_col[e] != r0 + r) mx = fmax(mx, fabs((double)c_g[e]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int64_t beg = lower_bound_col(c_col, c_ptr[r], c_ptr[r + 1], v0);
+  const int64_t end = lower_bound_col(c_col, beg, c_ptr[r + 1], v1);
+  double mx = accumulate ? row_max[r] : 0.0;
+  for (int64_t e = beg; e < end; ++e) {
+    const int64_t k = c_col[e];
+    if (k == r0 + r) continue;
+    const T* xa = Xi + r * ldk;
+    const T* xb = Xt + (k - v0) * ldk;
+    double s = 0.0;
+    for (int64_t m = lane; m < ldk; m += 32) s = fma((double)xa[m], (double)xb[m], s);
+    s = warp_sum(s);
+    mx = fmax(mx, fabs(s) / (double)n);
+  }
   if (lane == 0) row_max[r] = mx;
 }
 
@@ -1198,19 +1210,21 @@ int launch_row_ab(int64_t pk, int64_t ldk, const float* Xt_rows, float* row_A, f
   return 1;
 }
 
-int launch_cand_offdiag_max(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr,
-                            const int32_t* c_col, const void* c_g, double* row_max, double* out,
-                            cudaStream_t st) {
+int launch_cand_dot_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
+                        const int64_t* c_ptr, const int32_t* c_col, const void* Xi, const void* Xt,
+                        int64_t v0, int64_t v1, int accumulate, double* row_max, double* out,
+                        cudaStream_t st) {
   if (pk == 0) return 0;
   const unsigned g = (unsigned)((pk + 7) / 8);
   if (dtype == ACCORD_F64)
-    cand_offdiag_max_kernel<double><<<g, 256, 0, st>>>(pk, r0, c_ptr, c_col, (const double*)c_g,
-                                                       row_max);
+    cand_dot_max_kernel<double><<<g, 256, 0, st>>>(pk, r0, n, ldk, c_ptr, c_col,
+                                                   (const double*)Xi, (const double*)Xt, v0, v1,
+                                                   accumulate, row_max);
   else
-    cand_offdiag_max_kernel<float><<<g, 256, 0, st>>>(pk, r0, c_ptr, c_col, (const float*)c_g,
-                                                      row_max);
-  reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
-  return 2;
+    cand_dot_max_kernel<float><<<g, 256, 0, st>>>(pk, r0, n, ldk, c_ptr, c_col, (const float*)Xi,
+                                                  (const float*)Xt, v0, v1, accumulate, row_max);
+  if (out) reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
+  return out ? 2 : 1;
 }
 
 int launch_gram_offdiag_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
