@@ -214,6 +214,7 @@ struct accord_ctx {
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
+  int refine_kind = 2;                     // 0 block per item, 1 flat warps, 2 TMA ring (ACCORD_REFINE)
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
@@ -541,11 +542,21 @@ void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void*
 void refine_all(accord_ctx* c, const void* yrows = nullptr) {
   const void* Y = yrows ? yrows : c->Y[c->cur];
   if (!c->sharded) {
-    // hub rows (up to ~1.6e5 candidates) split over several blocks
+    // hub rows (up to ~1.6e5 candidates) split over several work items
     if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
-    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
-                                 c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
-                                 kItemEntries, c->item_row);
+    if (c->dtype == ACCORD_F32 && c->refine_kind == 2) {
+      c->launches += launch_refine_tma(c->pk, c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
+                                       (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
+                                       c->item_row, c->n_items, kItemEntries, c->sm_count, c->st);
+    } else if (c->dtype == ACCORD_F32 && c->refine_kind == 1) {
+      c->launches += launch_refine_flat(c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
+                                        (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
+                                        c->item_row, c->n_items, kItemEntries, c->sm_count, c->st);
+    } else {
+      c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
+                                   c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
+                                   kItemEntries, c->item_row);
+    }
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
@@ -1172,6 +1183,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   {
     const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
     c->pair_ls = !(e && e[0] == '0');
+    const char* r = std::getenv("ACCORD_REFINE");     // A-B switch: block | flat | tma
+    if (r) c->refine_kind = r[0] == 'b' ? 0 : r[0] == 'f' ? 1 : 2;
   }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
@@ -2320,7 +2333,9 @@ void accord_destroy(accord_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   else cudaDeviceSynchronize();
   if (c->plan) tc_plan_destroy(c->plan);
-  for (void* ptr : c->allocs) cudaFree(ptr);
+  // (buffers carved out of a caller workspace belong to the caller's allocation)
+  if (!c->arena.base)
+    for (void* ptr : c->allocs) cudaFree(ptr);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->tr_pool) cudaEventDestroy(e);

@@ -614,11 +614,14 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
                                                      const T* __restrict__ Xt,
                                                      T* __restrict__ c_g, int64_t v0,
                                                      int64_t v1, const int64_t* __restrict__ itm_ptr,
-                                                     int64_t L, const int32_t* __restrict__ item_row) {
+                                                     int64_t L, const int32_t* __restrict__ item_row,
+                                                     int y_global) {
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   extern __shared__ __align__(16) uint8_t ys_raw[];
-  T* ys = reinterpret_cast<T*>(ys_raw);
+  // Y_i staged in shared memory, or read in place (through L1) when a row
+  // does not fit (n beyond ~25,000 float64 / ~50,000 float32 samples)
+  const T* ys = reinterpret_cast<const T*>(ys_raw);
   int64_t r = blockIdx.x;
   int64_t beg, end;
   if (itm_ptr) {   // work item = chunk of <= L candidates of one row (hub rows split)
@@ -635,9 +638,14 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   beg = lower_bound_col(c_col, beg, end, v0);
   end = lower_bound_col(c_col, beg, end, v1);
   if (beg == end) return;
-  for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V)
-    *reinterpret_cast<VT*>(ys + m) = *reinterpret_cast<const VT*>(Y + r * ldk + m);
-  __syncthreads();
+  if (y_global) {
+    ys = Y + r * ldk;
+  } else {
+    T* yw = reinterpret_cast<T*>(ys_raw);
+    for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V)
+      *reinterpret_cast<VT*>(yw + m) = *reinterpret_cast<const VT*>(Y + r * ldk + m);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double inv_n = 1.0 / (double)n;
   constexpr int kStep = 32 * V;           // elements per lane-pass over the row
@@ -1153,7 +1161,9 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                   int64_t n_items, int64_t L, const int32_t* item_row) {
   const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
-  const size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
+  size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
+  const int y_global = smem > 200 * 1024 ? 1 : 0;
+  if (y_global) smem = 0;
   static unsigned long long attr_seen = 0;
   if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(refine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1165,11 +1175,13 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
   if (dtype == ACCORD_F64)
     refine_kernel<double><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                    (const double*)Y, (const double*)Xt,
-                                                   (double*)c_g, v0, v1, itm_ptr, L, item_row);
+                                                   (double*)c_g, v0, v1, itm_ptr, L, item_row,
+                                                   y_global);
   else
     refine_kernel<float><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                   (const float*)Y, (const float*)Xt,
-                                                  (float*)c_g, v0, v1, itm_ptr, L, item_row);
+                                                  (float*)c_g, v0, v1, itm_ptr, L, item_row,
+                                                  y_global);
   return 1;
 }
 

@@ -44,7 +44,7 @@ def test_config2_runs_inside_a_torch_workspace(host_x):
     csr, st, info = _run(X, lam, 100, inv_L, workspace=ws)
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
-    assert abs(free0 - free1) < (64 << 20), (free0 - free1)
+    assert free0 - free1 < (64 << 20), (free0 - free1)      # nothing taken from the device
     assert info["workspace_bytes"] <= need and 0 < info["workspace_high"] <= need
     assert [x["tau"] for x in st] == [x["tau"] for x in st_ref]
     assert np.array_equal(csr.row_ptr, ref.row_ptr) and np.array_equal(csr.col, ref.col)
