@@ -214,7 +214,7 @@ struct accord_ctx {
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
-  int refine_kind = 2;                     // 0 block per item, 1 flat warps, 2 TMA ring (ACCORD_REFINE)
+  int refine_kind = 3;                     // 0 block/f64, 1 flat, 2 TMA ring, 3 block/float-float (ACCORD_REFINE)
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
@@ -555,13 +555,14 @@ void refine_all(accord_ctx* c, const void* yrows = nullptr) {
     } else {
       c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
                                    c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
-                                   kItemEntries, c->item_row);
+                                   kItemEntries, c->item_row, c->refine_kind == 3);
     }
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
     c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, slab,
-                                 c->c_g, c->st, v0, v1);
+                                 c->c_g, c->st, v0, v1, nullptr, 0, 0, nullptr,
+                                 c->refine_kind == 3);
   });
 }
 
@@ -756,8 +757,7 @@ Footprint footprint(const accord_init_params* prm) {
   const size_t T = prm->dtype == ACCORD_F64 ? 8 : 4;
   int gemm = prm->gemm;
   if (gemm == ACCORD_GEMM_AUTO)
-    gemm = prm->dtype == ACCORD_F32 ? (ldk <= 4096 ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_BF16X3)
-                                    : ACCORD_GEMM_SIMT;
+    gemm = prm->dtype == ACCORD_F32 ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_SIMT;
   const bool x3 = gemm == ACCORD_GEMM_BF16X3, filt = gemm == ACCORD_GEMM_BF16_FILTER,
              tc = x3 || filt;
   const bool sharded = prm->x_sharded && prm->world > 1;
@@ -969,11 +969,10 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   c->agv = prm->allgatherv;
   c->cu = prm->comm_user;
   const bool tc_ok = tc_supported(c->cc_major, c->cc_minor);
-  constexpr int64_t kMaxFilterK = 4096;   // refine kernel stages a Y row in smem
+  // F32 on sm_100: the certified bf16 filter for any n (the refine streams
+  // X^T rows in 4 KB chunks; the filter bound's gamma grows with n)
   if (prm->gemm == ACCORD_GEMM_AUTO)
-    c->gemm = (c->dtype == ACCORD_F32 && tc_ok)
-                  ? (c->ldk <= kMaxFilterK ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_BF16X3)
-                  : ACCORD_GEMM_SIMT;
+    c->gemm = (c->dtype == ACCORD_F32 && tc_ok) ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_SIMT;
   else
     c->gemm = prm->gemm;
   const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
@@ -981,8 +980,6 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   if (tc && prm->x_sharded && prm->world > 1 && prm->row_begin % kRowPad != 0)
     throw Fail{ACCORD_E_INVALID,
                "x_sharded with a tensor-core GEMM: row_begin must be a multiple of 256"};
-  if (c->gemm == ACCORD_GEMM_BF16_FILTER && c->ldk > kMaxFilterK)
-    throw Fail{ACCORD_E_UNSUPPORTED, "BF16_FILTER supports n <= 4096"};
 
   for (auto& e : c->ev) CK(cudaEventCreate(&e));
   {
@@ -1183,8 +1180,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   {
     const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
     c->pair_ls = !(e && e[0] == '0');
-    const char* r = std::getenv("ACCORD_REFINE");     // A-B switch: block | flat | tma
-    if (r) c->refine_kind = r[0] == 'b' ? 0 : r[0] == 'f' ? 1 : 2;
+    const char* r = std::getenv("ACCORD_REFINE");     // A-B switch: block | flat | tma | ff
+    if (r) c->refine_kind = r[0] == 'b' ? 0 : r[0] == 'f' && r[1] == 'l' ? 1 : r[0] == 't' ? 2 : 3;
   }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
@@ -1197,6 +1194,14 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
                 std::getenv("ACCORD_SPMM_PLAIN") == nullptr;   // env: A-B diagnostic
   if (std::getenv("ACCORD_SPMM_TMA"))   // env: force (tests of the TMA path at small sizes)
     c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk);
+  if (c->world > 1 && !c->sharded && spmm_tma_supported(c->dtype, c->ldk)) {
+    // the paired line-search pass exists for the TMA SpMM only, and every
+    // rank must run the same passes (each ends in an allreduce of 8 or 16
+    // sums): one SpMM kind for all ranks, TMA if any rank's block is large
+    const double flag = c->tma_spmm ? 1.0 : 0.0;
+    CK(cudaMemcpyAsync(c->red_d + 8, &flag, 8, cudaMemcpyHostToDevice, c->st));
+    c->tma_spmm = allreduce_max(c, c->red_d + 8) > 0.5;
+  }
   c->itm_n = c->dalloc<int32_t>(c->pk);
   c->itm_s = c->dalloc<int32_t>(c->pk);
   c->itm_ptr = c->dalloc<int64_t>(c->pk + 1);

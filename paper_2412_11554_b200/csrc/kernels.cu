@@ -605,8 +605,28 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
 // Exact candidate values (BF16_FILTER refine, and the gradient on a fixed
 // support for the bias-correction refit): c_g[e] = (1/n) <Y_i, Xt_k> with
 // float64 accumulation; warp per candidate, Y_i staged in shared memory.
+//
+// kFF (float data): the dot product in float-float arithmetic on the FP32
+// pipes instead of float64: each product x y is split exactly into p + e
+// (p = rn(x y), e = fma(x, y, -p)) and summed with Knuth's TwoSum into a
+// (hi, lo) pair. The float64 path converts both operands of every product
+// (F2F.F64.F32 on the XU pipe, 16 per clock per SM): ncu showed the XU pipe
+// 56 % busy at 4.4 TB/s, the ceiling the gather could not pass. Float-float
+// keeps ~2^-46 of the sum of |products| (the f32 result is the correctly
+// rounded value of the exact dot except in ties below that), far inside the
+// f32 value c_g stores.
 // ---------------------------------------------------------------------------
-template <typename T>
+__device__ __forceinline__ void ff_madd(float& hi, float& lo, float x, float y) {
+  const float p = __fmul_rn(x, y);
+  const float e = __fmaf_rn(x, y, -p);              // x y = p + e exactly
+  const float t = __fadd_rn(hi, p);                 // TwoSum(hi, p) = t + err exactly
+  const float z = __fsub_rn(t, hi);
+  const float err = __fadd_rn(__fsub_rn(hi, __fsub_rn(t, z)), __fsub_rn(p, z));
+  lo = __fadd_rn(lo, __fadd_rn(err, e));
+  hi = t;
+}
+
+template <typename T, bool kFF = false>
 __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
                                                      const int64_t* __restrict__ c_ptr,
                                                      const int32_t* __restrict__ c_col,
@@ -651,6 +671,35 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   constexpr int kStep = 32 * V;           // elements per lane-pass over the row
   for (int64_t e = beg + wid; e < end; e += nw) {
     const T* xr = Xt + (int64_t)(c_col[e] - v0) * ldk;
+    if constexpr (kFF) {
+      // two (hi, lo) accumulators: shorter dependent chains
+      float h0 = 0.f, l0 = 0.f, h1 = 0.f, l1 = 0.f;
+      int64_t m = lane * V;
+      for (; m + 7 * kStep < ldk; m += 8 * kStep) {
+        VT x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const VT*>(xr + m + u * kStep));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const VT yv = *reinterpret_cast<const VT*>(ys + m + u * kStep);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (v & 1) ff_madd(h1, l1, (float)vget(yv, v), (float)vget(x[u], v));
+            else ff_madd(h0, l0, (float)vget(yv, v), (float)vget(x[u], v));
+          }
+        }
+      }
+      for (; m < ldk; m += kStep) {
+        const VT x = __ldg(reinterpret_cast<const VT*>(xr + m));
+        const VT yv = *reinterpret_cast<const VT*>(ys + m);
+#pragma unroll
+        for (int v = 0; v < V; ++v) ff_madd(h0, l0, (float)vget(yv, v), (float)vget(x, v));
+      }
+      double s = ((double)h0 + (double)h1) + ((double)l0 + (double)l1);
+      s = warp_sum(s);
+      if (lane == 0) c_g[e] = (T)(s * inv_n);
+      continue;
+    }
     double s = 0.0;
     int64_t m = lane * V;
     for (; m + 7 * kStep < ldk; m += 8 * kStep) {   // 8 loads in flight per lane
@@ -1158,7 +1207,7 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
                   cudaStream_t st, int64_t v0, int64_t v1, const int64_t* itm_ptr,
-                  int64_t n_items, int64_t L, const int32_t* item_row) {
+                  int64_t n_items, int64_t L, const int32_t* item_row, bool ff) {
   const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
   size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
@@ -1170,6 +1219,8 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                          200 * 1024);
     cudaFuncSetAttribute(refine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
+    cudaFuncSetAttribute(refine_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr_done(attr_seen);
   }
   if (dtype == ACCORD_F64)
@@ -1177,6 +1228,11 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                                                    (const double*)Y, (const double*)Xt,
                                                    (double*)c_g, v0, v1, itm_ptr, L, item_row,
                                                    y_global);
+  else if (ff)
+    refine_kernel<float, true><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                        (const float*)Y, (const float*)Xt,
+                                                        (float*)c_g, v0, v1, itm_ptr, L, item_row,
+                                                        y_global);
   else
     refine_kernel<float><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                   (const float*)Y, (const float*)Xt,

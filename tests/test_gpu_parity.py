@@ -128,6 +128,24 @@ def test_lanczos_exactly_centered_and_zero_x():
     assert e.value.status == A.E_NUMERIC
 
 
+@pytest.mark.parametrize("refine", ["tma", "flat", "block"])
+def test_filter_path_beyond_4096_samples(refine, monkeypatch):
+    """n = 5000 (ldk = 5056: the refine streams each X^T row in five chunks,
+    the last partial): AUTO is the certified bf16 filter for any n (round 1
+    fell back to BF16X3 above n = 4096); parity with the oracle, each refine
+    variant."""
+    _cuda()
+    monkeypatch.setenv("ACCORD_REFINE", refine)
+    from accord_inputs import Config
+    cfg = Config(name="t_bign_p600_n5000_f32", p=600, n=5000, dtype="f32", structure="ba",
+                 block=300, lambdas=(0.05,), T=8, graph_seed=61, sample_seed=62)
+    pr = make_problem(cfg)
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    csr, stats, info = run_gpu(pr.Xt, 0.05, cfg.T, inv_L, A.GEMM_AUTO)
+    assert info["gemm"] == A.GEMM_BF16_FILTER and info["ldk"] == 5056
+    compare_full(pr.Xt, 0.05, cfg.T, inv_L, csr.to_dense(cfg.p), stats, "f32")
+
+
 def test_warm_start_roundtrip():
     _cuda()
     pr = make_problem("t_ba_f64")

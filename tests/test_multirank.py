@@ -166,6 +166,33 @@ def test_p_invariance_one_gpu(gemm):
 
 
 @pytest.mark.gpu
+def test_mixed_block_sizes_agree_on_the_spmm_kind():
+    """p = 131,000, P = 2: rank 0's block (65,536 rows) qualifies for the TMA
+    SpMM with paired line-search passes, rank 1's (65,464) alone would not.
+    The ranks must run the same passes (each ends in an allreduce of 8 or 16
+    sums), so create agrees on one kind; the run equals P = 1 (decisions, f,
+    gathered Omega)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import Config, make_problem
+    cfg = Config(name="t_mixed_p131000_n256_f32", p=131000, n=256, dtype="f32", structure="ba",
+                 block=1000, lambdas=(0.35,), T=4, graph_seed=71, sample_seed=72)
+    pr = make_problem(cfg)
+    b = A.partition_rows(cfg.p, 2)
+    assert b[0][1] - b[0][0] >= 65536 > b[1][1] - b[1][0]
+    ref, _ = run_ranks(pr.Xt, 0.35, cfg.T, 0.0, 1, A.GEMM_BF16_FILTER)
+    out, bounds = run_ranks(pr.Xt, 0.35, cfg.T, 0.0, 2, A.GEMM_BF16_FILTER)
+    for r in range(2):
+        st, g, loc, f = out[r]
+        assert [x["tau"] for x in st] == [x["tau"] for x in ref[0][0]]
+        assert [x["trials"] for x in st] == [x["trials"] for x in ref[0][0]]
+        assert abs(f - ref[0][3]) <= 1e-9 * abs(f)
+        assert np.array_equal(g.row_ptr, ref[0][1].row_ptr) and np.array_equal(g.col, ref[0][1].col)
+        assert np.abs(g.val - ref[0][1].val).max() <= 1e-6 * np.abs(ref[0][1].val).max()
+
+
+@pytest.mark.gpu
 def test_transformed_exports_p_invariant_one_gpu():
     """NEXT(4) with P = 2 row blocks (ThreadComm): PCORR needs the transpose
     across ranks (gathered), THETA is rank-local; both must equal P = 1."""

@@ -1,7 +1,7 @@
 """Summarise an ncu --set full capture of the gradient GEMM: key counters to
 profiles/<round>/ncu_<tag>_raw.csv and the per-launch DRAM traffic that
 bench.py reports as roofline.traffic to profiles/gemm_traffic.json.
-Usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep <tag> [workload] [world]"""
+Usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep <tag> [workload] [world] [round]"""
 import csv
 import io
 import json
@@ -13,6 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, tag = sys.argv[1], sys.argv[2]
 workload = sys.argv[3] if len(sys.argv) > 3 else "c5_ba1000x1000_p1000000_n1000_f32"
 world = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+rnd = sys.argv[5] if len(sys.argv) > 5 else "r02"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -21,7 +22,7 @@ keys = ("dram__bytes", "gpu__time_duration.sum", "pipe_tensor", "lts__t_sector_h
         "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__throughput.avg", "sm__cycles_elapsed.avg.per_second",
         "launch__", "sm__throughput.avg", "ltcfabric.sum", "Kernel Name")
 keep = [i for i, h in enumerate(hdr) if any(k in h for k in keys)]
-out = os.path.join(ROOT, "profiles", "r01", f"ncu_{tag}_raw.csv")
+out = os.path.join(ROOT, "profiles", rnd, f"ncu_{tag}_raw.csv")
 with open(out, "w", newline="") as f:
     w = csv.writer(f)
     for row in (hdr, units, r):
@@ -38,7 +39,7 @@ traffic = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
 json.dump({"workload": workload, "world": world, "kernel": "gemm_tc_kernel (BF16 filter)",
            "dram_bytes_per_launch": traffic,
            "source": f"ncu --set full --clock-control none, one steady-state launch "
-                     f"(profiles/r01/ncu_{tag}_raw.csv)"},
+                     f"(profiles/{rnd}/ncu_{tag}_raw.csv)"},
           open(os.path.join(ROOT, "profiles", "gemm_traffic.json"), "w"), indent=1)
 for i in keep:
     print(hdr[i], units[i], r[i])
