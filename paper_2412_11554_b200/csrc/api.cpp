@@ -937,6 +937,17 @@ double lanczos_lmax(accord_ctx* c, int64_t pv) {
 
 void create_impl(accord_ctx* c, const accord_init_params* prm) {
   validate(prm);
+  // ACCORD_TRACE=1: host wall time of the create phases (stderr)
+  const bool ctrace = std::getenv("ACCORD_TRACE") && std::getenv("ACCORD_TRACE")[0] == '1';
+  auto tprev = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!ctrace) return;
+    cudaStreamSynchronize((cudaStream_t)prm->stream);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[accord create] %s %.1f ms\n", name,
+                 std::chrono::duration<double, std::milli>(t - tprev).count());
+    tprev = t;
+  };
   if (prm->workspace) {
     if (prm->workspace_bytes == 0) throw Fail{ACCORD_E_INVALID, "workspace_bytes is 0"};
     c->arena.init(prm->workspace, prm->workspace_bytes);
@@ -1036,6 +1047,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   const int64_t pv = c->sharded ? c->pk : c->p;   // variables held in Xt
   c->xrows_pad = c->sharded ? c->pk_pad : c->p_pad;
 
+  phase("init+comm");
   // ---- X -> Xt (variable-major, padded), finiteness check ----
   const size_t T = c->tsz;
   c->Xt = c->dalloc_bytes((size_t)c->xrows_pad * c->ldk * T);
@@ -1069,6 +1081,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     throw Fail{ACCORD_E_INVALID, m};
   }
 
+  phase("X^T (alloc, copy, transpose, check)");
   // ---- L ----
   if (prm->inv_L > 0) {
     c->inv_L = prm->inv_L;
@@ -1087,6 +1100,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     c->inv_L = 1.0 / c->L;
   }
 
+  phase("L (Lanczos)");
   // ---- operands ----
   const bool x3 = c->gemm == ACCORD_GEMM_BF16X3, filt = c->gemm == ACCORD_GEMM_BF16_FILTER;
   for (int b = 0; b < 2; ++b) {
@@ -1126,6 +1140,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     if (filt) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
   }
 
+  phase("operands (Y, bf16 copies, column norms, tensor maps)");
   // ---- ring buffers of the sharded mode ----
   if (c->sharded) {
     for (int q = 0; q < c->world; ++q)
@@ -1224,13 +1239,16 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     }
   }
   cap = std::max<int64_t>(cap, c->pk);
+  phase("per-row state");
   grow(c, std::min<int64_t>(cap, (int64_t)UINT32_MAX), 0);
+  phase("candidate pool");
 
   // ---- Omega^{(0)} = I, Y^{(0)} = rows of X^T, f^{(0)} ----
   c->launches += launch_identity(c->dtype, c->pk, c->r0, c->om_ptr, c->om_col, c->om_val, c->st);
   recompute_y(c);
   c->omega_identity = true;
   refresh_objective(c);
+  phase("Omega = I, Y, f");
 }
 
 template <typename F>

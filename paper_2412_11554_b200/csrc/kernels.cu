@@ -7,6 +7,7 @@
 #include "accord_internal.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cfloat>
 #include <climits>
 #include <vector>
@@ -1213,6 +1214,12 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
   size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
   const int y_global = smem > 200 * 1024 ? 1 : 0;
   if (y_global) smem = 0;
+  // threads per block (one warp per candidate of the item): ACCORD_REFINE_THREADS (A-B)
+  static const int thr = [] {
+    const char* e = std::getenv("ACCORD_REFINE_THREADS");
+    const int t = e ? std::atoi(e) : 256;
+    return (t == 64 || t == 128 || t == 256) ? t : 256;
+  }();
   static unsigned long long attr_seen = 0;
   if (attr_needed(attr_seen)) {
     cudaFuncSetAttribute(refine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1224,17 +1231,17 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
     attr_done(attr_seen);
   }
   if (dtype == ACCORD_F64)
-    refine_kernel<double><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+    refine_kernel<double><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                    (const double*)Y, (const double*)Xt,
                                                    (double*)c_g, v0, v1, itm_ptr, L, item_row,
                                                    y_global);
   else if (ff)
-    refine_kernel<float, true><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+    refine_kernel<float, true><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                         (const float*)Y, (const float*)Xt,
                                                         (float*)c_g, v0, v1, itm_ptr, L, item_row,
                                                         y_global);
   else
-    refine_kernel<float><<<grid, 256, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+    refine_kernel<float><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                   (const float*)Y, (const float*)Xt,
                                                   (float*)c_g, v0, v1, itm_ptr, L, item_row,
                                                   y_global);

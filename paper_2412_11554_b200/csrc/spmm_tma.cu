@@ -58,9 +58,13 @@ __device__ __forceinline__ double wsum(double v) {
 // kPair: also D' = (W' - Wold) X^T for a second trial step (weights wn2),
 // of which only the row norms ||D'_i||^2 are kept (row_D2b): one gather pass
 // serves two line-search trials.
-template <bool kPair>
-__global__ void __launch_bounds__(kPair ? 32 + kSpmmPairMaxConsumers : 32 + kSpmmTmaMaxConsumers,
-                                  kPair ? 3 : 2)
+// kCols: output columns per consumer thread (8: two float4 per staged row;
+// 4: one float4, twice the consumer warps per block and a third of the
+// accumulator registers -- more warps in flight per SM)
+template <bool kPair, int kCols>
+__global__ void __launch_bounds__(kCols == 4 ? 32 + kSpmmTmaMaxConsumers
+                                  : (kPair ? 32 + kSpmmPairMaxConsumers : 32 + kSpmmTmaMaxConsumers),
+                                  kCols == 4 ? (kPair ? 2 : 3) : (kPair ? 3 : 2))
 spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__ ptr,
                 const int32_t* __restrict__ col, const float* __restrict__ wn,
                 const float* __restrict__ wo, const float* __restrict__ Xt, float* __restrict__ Yout,
@@ -196,11 +200,11 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
 
   // ================================ consumers ===============================
   const int t = threadIdx.x - 32;
-  const int64_t c0 = (int64_t)t * 8;
+  const int64_t c0 = (int64_t)t * kCols;
   const bool active = c0 < ldk;
-  double ay[8], ad[8], ae[8];   // Y+, D, and D' (kPair)
+  double ay[kCols], ad[kCols], ae[kCols];   // Y+, D, and D' (kPair)
 #pragma unroll
-  for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
+  for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
   int stage = 0;
   uint32_t phase = 0;
   double* sh_red = red;                                   // [16] per-warp partials x 5
@@ -208,7 +212,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
   auto accumulate = [&](double w, double d, double d2, float4 x0, float4 x1) {
     const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
+    for (int v = 0; v < kCols; ++v) {
       ay[v] = fma(w, (double)xv[v], ay[v]);
       ad[v] = fma(d, (double)xv[v], ad[v]);
       if constexpr (kPair) ae[v] = fma(d2, (double)xv[v], ae[v]);
@@ -228,7 +232,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     if ((f0 & kFlagData) && active) {
       const float* xs = data + (size_t)stage * ldk + c0;
       a0 = *reinterpret_cast<const float4*>(xs);
-      b0 = *reinterpret_cast<const float4*>(xs + 4);
+      if constexpr (kCols == 8) b0 = *reinterpret_cast<const float4*>(xs + 4);
     }
     const int s1 = stage + 1 == stages ? 0 : stage + 1;
     const uint32_t ph1 = stage + 1 == stages ? phase ^ 1 : phase;
@@ -245,7 +249,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       if ((f1 & kFlagData) && active) {
         const float* xs = data + (size_t)s1 * ldk + c0;
         a1 = *reinterpret_cast<const float4*>(xs);
-        b1 = *reinterpret_cast<const float4*>(xs + 4);
+        if constexpr (kCols == 8) b1 = *reinterpret_cast<const float4*>(xs + 4);
       }
     }
     const bool last = (f0 & kFlagLast) || (f1 & kFlagLast);
@@ -275,11 +279,11 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         double* py = items.part_y + (slot0 + m.chunk) * ldk + c0;
         double* pd = items.part_d + (slot0 + m.chunk) * ldk + c0;
 #pragma unroll
-        for (int v = 0; v < 8; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
+        for (int v = 0; v < kCols; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
         if constexpr (kPair) {
           double* pe = items.part_d2 + (slot0 + m.chunk) * ldk + c0;
 #pragma unroll
-          for (int v = 0; v < 8; ++v) pe[v] = ae[v];
+          for (int v = 0; v < kCols; ++v) pe[v] = ae[v];
         }
       }
       __threadfence();
@@ -291,19 +295,19 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         __threadfence();
         if (active) {
 #pragma unroll
-          for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
+          for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
           for (int k = 0; k < m.nch; ++k) {   // chunk order: deterministic sum
             const double* py = items.part_y + (slot0 + k) * ldk + c0;
             const double* pd = items.part_d + (slot0 + k) * ldk + c0;
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
+            for (int v = 0; v < kCols; ++v) {
               ay[v] += __ldcg(py + v);
               ad[v] += __ldcg(pd + v);
             }
             if constexpr (kPair) {
               const double* pe = items.part_d2 + (slot0 + k) * ldk + c0;
 #pragma unroll
-              for (int v = 0; v < 8; ++v) ae[v] += __ldcg(pe + v);
+              for (int v = 0; v < kCols; ++v) ae[v] += __ldcg(pe + v);
             }
           }
         }
@@ -313,9 +317,9 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     if (finish) {
       double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0, e2 = 0.0;
       if (active) {
-        float yt[8];
+        float yt[kCols];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
+        for (int v = 0; v < kCols; ++v) {
           d2 += ad[v] * ad[v];
           y2 += ay[v] * ay[v];
           if constexpr (kPair) e2 += ae[v] * ae[v];
@@ -323,11 +327,12 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         }
         float* yo = Yout + r * ldk + c0;
         *reinterpret_cast<float4*>(yo) = make_float4(yt[0], yt[1], yt[2], yt[3]);
-        *reinterpret_cast<float4*>(yo + 4) = make_float4(yt[4], yt[5], yt[6], yt[7]);
+        if constexpr (kCols == 8)
+          *reinterpret_cast<float4*>(yo + 4) = make_float4(yt[4], yt[5], yt[6], yt[7]);
         if (Yhi) {
-          uint32_t hp[4], lp[4];
+          uint32_t hp[kCols / 2], lp[kCols / 2];
 #pragma unroll
-          for (int v = 0; v < 8; v += 2) {
+          for (int v = 0; v < kCols; v += 2) {
             const __nv_bfloat162 h2 = filter_bf16x2(yt[v], yt[v + 1]);
             const float2 hf = __bfloat1622float2(h2);
             const __nv_bfloat162 l2 = __floats2bfloat162_rn(yt[v] - hf.x, yt[v + 1] - hf.y);
@@ -337,9 +342,14 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
             a2 += e0 * e0 + e1 * e1;
             b2 += (double)yt[v] * (double)yt[v] + (double)yt[v + 1] * (double)yt[v + 1];
           }
-          *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-          if (Ylo)
-            *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+          if constexpr (kCols == 8) {
+            *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+            if (Ylo)
+              *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+          } else {
+            *reinterpret_cast<uint2*>(Yhi + r * ldk + c0) = make_uint2(hp[0], hp[1]);
+            if (Ylo) *reinterpret_cast<uint2*>(Ylo + r * ldk + c0) = make_uint2(lp[0], lp[1]);
+          }
         }
       }
       d2 = wsum(d2);
@@ -377,7 +387,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       named_sync(1, nct);
     }
 #pragma unroll
-    for (int v = 0; v < 8; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
+    for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
   }
 }
 
@@ -699,13 +709,21 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
   const size_t smem = spmm_tma_smem(ldk, &stages);
   static unsigned long long attr_seen = 0;
   if (attr_needed(attr_seen)) {
-    cudaFuncSetAttribute(spmm_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spmm_tma_kernel<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          100 * 1024);
-    cudaFuncSetAttribute(spmm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spmm_tma_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         100 * 1024);
+    cudaFuncSetAttribute(spmm_tma_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         100 * 1024);
+    cudaFuncSetAttribute(spmm_tma_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          100 * 1024);
     attr_done(attr_seen);
   }
-  const int consumers = (int)round_up(ldk / 8, 32);
+  // 4 columns per consumer thread when the row fits 256 consumers (ldk <= 1024),
+  // else 8 (ACCORD_SPMM_COLS: A-B)
+  int cols = ldk <= 4 * kSpmmTmaMaxConsumers ? 4 : 8;
+  if (const char* e = std::getenv("ACCORD_SPMM_COLS")) cols = std::atoi(e) == 8 ? 8 : cols;
+  const int consumers = (int)round_up(ldk / cols, 32);
   // persistent: exactly the resident blocks (items are dealt round-robin)
   auto launch = [&](auto kern) {
     int per_sm = 0;
@@ -717,8 +735,13 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
         pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2,
         wn2, row_D2b, items);
   };
-  if (wn2) launch(spmm_tma_kernel<true>);
-  else launch(spmm_tma_kernel<false>);
+  if (cols == 4) {
+    if (wn2) launch(spmm_tma_kernel<true, 4>);
+    else launch(spmm_tma_kernel<false, 4>);
+  } else {
+    if (wn2) launch(spmm_tma_kernel<true, 8>);
+    else launch(spmm_tma_kernel<false, 8>);
+  }
   return 1;
 }
 

@@ -191,14 +191,16 @@ def test_parity_dense_candidate_rows(p, n, lam, T):
     compare_full(pr.Xt, lam, T, inv_L, csr.to_dense(p), stats, "f32")
 
 
+@pytest.mark.parametrize("cols", ["4", "8"])
 @pytest.mark.parametrize("p,n,lam,T", [(4000, 60, 0.05, 3), (1100, 333, 0.1, 8)])
-def test_tma_spmm_matches_block_per_row_spmm(p, n, lam, T, monkeypatch):
+def test_tma_spmm_matches_block_per_row_spmm(p, n, lam, T, cols, monkeypatch):
     """The TMA-staged SpMM (producer warp + cp.async.bulk ring, hub rows split
     into work items with a deterministic last-block sum) and the block-per-row
     SpMM compute the same Y+ and D (both float64-accumulated): identical tau
     schedule, objective and Omega to rounding, on a case whose candidate rows
     exceed one work item (2048 entries)."""
     _cuda()
+    monkeypatch.setenv("ACCORD_SPMM_COLS", cols)    # columns per consumer thread
     rng = np.random.default_rng(5 + p)
     Xt = rng.standard_normal((p, n)).astype(np.float32)
     Xt -= Xt.mean(axis=1, keepdims=True)
