@@ -214,7 +214,7 @@ struct accord_ctx {
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
-  int refine_kind = 3;                     // 0 block/f64, 1 flat, 2 TMA ring, 3 block/float-float (ACCORD_REFINE)
+  int refine_kind = 0;                     // 0 block/f64, 1 flat, 2 TMA ring, 3 block/float-float (ACCORD_REFINE)
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
