@@ -241,6 +241,7 @@ struct accord_ctx {
   float* audit_acc = nullptr;              // accord_filter_audit (diagnostic)
   int64_t audit_ld = 0;
   bool plan_a_x = false;                   // plan A map 2 = X^T_hi rows (lambda_max)
+  int lanczos_steps = 0;                   // diagnostic (ACCORD_TRACE)
 
   // bias-correction refit (Eq. 3.8): fixed support S_hat, penalty phi * lambda
   bool refit = false;
@@ -922,6 +923,7 @@ double lanczos_lmax(accord_ctx* c, int64_t pv) {
     bt = std::sqrt(bt);
     b[j] = bt;
     theta = tridiag_lmax(a, b, j + 1);
+    c->lanczos_steps = j + 1;
     if (j >= 8 && std::fabs(theta - prev) <= 1e-12 * std::fabs(theta)) break;
     prev = theta;
     if (!(bt > 1e-13 * std::max(std::fabs(theta), 1e-300))) break;   // invariant subspace
@@ -1100,6 +1102,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     c->inv_L = 1.0 / c->L;
   }
 
+  if (ctrace) std::fprintf(stderr, "[accord create] Lanczos steps %d\n", c->lanczos_steps);
   phase("L (Lanczos)");
   // ---- operands ----
   const bool x3 = c->gemm == ACCORD_GEMM_BF16X3, filt = c->gemm == ACCORD_GEMM_BF16_FILTER;

@@ -1065,6 +1065,79 @@ __global__ void pi_xtu_kernel(const T* __restrict__ Xt, int64_t p, int64_t ldk, 
 
 
 
+// One pass over X^T for the Lanczos operator w = X (X^T u) / n (ldk <= 1024,
+// float X): a warp takes whole rows x_j, t_j = <x_j, u> / n by a warp
+// reduction, then w += t_j x_j, with u and the warp's share of w held in
+// registers (lane = columns 4 lane + 128 q + v); the next row of the warp is
+// loaded while the current one is used. Each block sums its warps in fixed
+// order into part[block] (the caller sums the blocks in order):
+// deterministic, and X is read once instead of twice.
+__global__ void __launch_bounds__(256, 1) gram_fused_kernel(const float* __restrict__ Xt,
+                                                            int64_t p, int64_t ldk, int64_t n,
+                                                            int64_t rows_per,
+                                                            const double* __restrict__ u,
+                                                            double* __restrict__ part) {
+  __shared__ double sw[1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nq = (int)(ldk / 128);          // float4 chunks per lane (<= 8)
+  double uv[32], wv[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t m = (int64_t)q * 128 + lane * 4 + v;
+      uv[q * 4 + v] = (q < nq) ? u[m] : 0.0;
+      wv[q * 4 + v] = 0.0;
+    }
+  const int64_t j0 = (int64_t)blockIdx.x * rows_per, j1 = min(p, j0 + rows_per);
+  const double inv_n = 1.0 / (double)n;
+  auto load = [&](int64_t j, float4* x) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      x[q] = (q < nq && j < j1) ? __ldg(reinterpret_cast<const float4*>(Xt + j * ldk + q * 128 +
+                                                                       lane * 4))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float4 xa[8], xb[8];
+  int64_t j = j0 + warp;
+  load(j, xa);
+  for (; j < j1; j += 8) {
+    load(j + 8, xb);                        // next row of this warp in flight
+    double d = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      d = fma(uv[q * 4 + 0], (double)xa[q].x, d);
+      d = fma(uv[q * 4 + 1], (double)xa[q].y, d);
+      d = fma(uv[q * 4 + 2], (double)xa[q].z, d);
+      d = fma(uv[q * 4 + 3], (double)xa[q].w, d);
+    }
+    const double t = warp_sum(d) * inv_n;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      wv[q * 4 + 0] = fma(t, (double)xa[q].x, wv[q * 4 + 0]);
+      wv[q * 4 + 1] = fma(t, (double)xa[q].y, wv[q * 4 + 1]);
+      wv[q * 4 + 2] = fma(t, (double)xa[q].z, wv[q * 4 + 2]);
+      wv[q * 4 + 3] = fma(t, (double)xa[q].w, wv[q * 4 + 3]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) xa[q] = xb[q];
+  }
+  // block sum of the warps' w, fixed order
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int m = q * 128 + lane * 4 + v;
+          if (q < nq) sw[m] = (w == 0 ? 0.0 : sw[m]) + wv[q * 4 + v];
+        }
+    }
+    __syncthreads();
+  }
+  for (int64_t m = threadIdx.x; m < ldk; m += blockDim.x) part[blockIdx.x * ldk + m] = sw[m];
+}
+
 inline int grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -1214,11 +1287,12 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
   size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
   const int y_global = smem > 200 * 1024 ? 1 : 0;
   if (y_global) smem = 0;
-  // threads per block (one warp per candidate of the item): ACCORD_REFINE_THREADS (A-B)
+  // threads per block (warps share the item's candidates): ACCORD_REFINE_THREADS (A-B);
+  // a c5 item has ~13 candidates, so 4 warps keep each warp busier than 8
   static const int thr = [] {
     const char* e = std::getenv("ACCORD_REFINE_THREADS");
-    const int t = e ? std::atoi(e) : 256;
-    return (t == 64 || t == 128 || t == 256) ? t : 256;
+    const int t = e ? std::atoi(e) : 128;   // c5: 128 -> 14.2 ms, 256 -> 16.6-17.1 ms
+    return (t == 64 || t == 128 || t == 256) ? t : 128;
   }();
   static unsigned long long attr_seen = 0;
   if (attr_needed(attr_seen)) {
@@ -1388,6 +1462,19 @@ int launch_gram_apply(int dtype, const void* Xt, int64_t p, int64_t n, int64_t l
   if (p <= 0) {
     cudaMemsetAsync(w, 0, ldk * sizeof(double), st);
     return 0;
+  }
+  if (dtype == ACCORD_F32 && ldk <= 1024 && ldk % 128 == 0 && !std::getenv("ACCORD_GRAM_2PASS")) {
+    // single pass: one block of contiguous rows per SM (255 registers per
+    // thread: one resident block), part holds nb x ldk (nb <= nsplit)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(nsplit, sms));
+    const int64_t rows_per = (p + nb - 1) / nb;
+    gram_fused_kernel<<<(unsigned)nb, 256, 0, st>>>((const float*)Xt, p, ldk, n, rows_per, u,
+                                                    part);
+    pi_sum_parts<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(part, nb, ldk, w);
+    return 2;
   }
   const unsigned g3 = (unsigned)((p + 7) / 8);
   if (dtype == ACCORD_F64)

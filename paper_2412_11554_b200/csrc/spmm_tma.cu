@@ -719,10 +719,12 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                          100 * 1024);
     attr_done(attr_seen);
   }
-  // 4 columns per consumer thread when the row fits 256 consumers (ldk <= 1024),
-  // else 8 (ACCORD_SPMM_COLS: A-B)
-  int cols = ldk <= 4 * kSpmmTmaMaxConsumers ? 4 : 8;
-  if (const char* e = std::getenv("ACCORD_SPMM_COLS")) cols = std::atoi(e) == 8 ? 8 : cols;
+  // 8 columns per consumer thread; 4 (twice the consumer warps, a third of the
+  // accumulator registers) measured slower at c5: 50.3 vs 39.8 ms per step
+  // (ACCORD_SPMM_COLS=4: A-B, ldk <= 1024)
+  int cols = 8;
+  if (const char* e = std::getenv("ACCORD_SPMM_COLS"))
+    cols = (std::atoi(e) == 4 && ldk <= 4 * kSpmmTmaMaxConsumers) ? 4 : 8;
   const int consumers = (int)round_up(ldk / cols, 32);
   // persistent: exactly the resident blocks (items are dealt round-robin)
   auto launch = [&](auto kern) {
