@@ -191,6 +191,8 @@ typedef struct {
   size_t device_bytes;          /* device memory held by the context */
   size_t workspace_bytes;       /* caller workspace size (0: library-allocated memory) */
   size_t workspace_high;        /* high-water mark of the workspace in use */
+  int64_t mirrored_sent;        /* candidate positions this rank sent to their row's owner in the
+                                   symmetric first GEMM across ranks (cumulative, diagnostic) */
 } accord_info;
 
 typedef struct accord_ctx accord_ctx;

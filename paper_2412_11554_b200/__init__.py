@@ -88,6 +88,7 @@ class Info(C.Structure):
         ("kernel_launches", C.c_int64), ("gemm_launches", C.c_int64),
         ("f", C.c_double), ("device_bytes", C.c_size_t),
         ("workspace_bytes", C.c_size_t), ("workspace_high", C.c_size_t),
+        ("mirrored_sent", C.c_int64),
     ]
 
     def as_dict(self):

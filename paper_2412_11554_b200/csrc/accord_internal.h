@@ -98,10 +98,18 @@ struct EpiParams {            // candidate rule of the fused epilogue (SURVEY P1
   const float2* col_sd;       // (||x_k|| + ||x_k - bf16(x_k)||, ||x_k - bf16(x_k)||)
   float gamma;                // accumulation-error factor
   int exact_cols;             // 1: re-test tile-test survivors with their own column's bound
-  // 1: Omega is exactly I on one rank (the first iteration of a solve), so
-  // G = X^T X / n is symmetric: only tiles with N-block >= M-block run, and an
-  // off-diagonal tile emits every survivor (i,k) also as (k,i) (BF16_FILTER)
+  // Omega is exactly I (the first iteration of a solve), so G = X^T X / n is
+  // symmetric and each off-diagonal tile pair runs once, its survivors (i,k)
+  // emitted also as (k,i) (BF16_FILTER): 1 = one rank, tiles with N-block >=
+  // M-block; 2 = several ranks (row blocks on 256-row tiles), the cyclic half
+  // of gemm_tc.cu's Sched; mirrored entries of another rank's rows go to the
+  // mirror buffer (global row, column) and are sent to their owner
   int sym;
+  int mt0, nt;                // sym 2: global row tile of local M-block 0, column tiles
+  int32_t* mir_row;           // [mir_cap] global row of a mirrored entry (sym 2)
+  int32_t* mir_col;
+  unsigned long long* mir_cnt;   // entries written (may exceed mir_cap: overflow)
+  int64_t mir_cap;
   // diagnostics / NEXT(2) (nullptr in the product path): audit_acc != NULL
   // writes every raw fp32 accumulator (row-major, audit_ld floats per local
   // row) besides the normal emission; max_out != NULL emits nothing and
@@ -273,6 +281,16 @@ int launch_cand_dot_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ld
 int launch_gram_offdiag_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
                             const void* Xi, const void* Xt, int64_t v0, int64_t v1, int accumulate,
                             double* row_max, double* out, cudaStream_t st);
+
+// Symmetric first GEMM across ranks: bucket the mirrored (global row, col)
+// entries by owner rank (rb: the ranks' global row boundaries, P <= 64), and
+// append received ones (global rows of this rank) to the pool from `start`.
+int launch_mirror_count(int64_t n, const int32_t* row, const int64_t* rb, int P,
+                        unsigned long long* cnt, cudaStream_t st);
+int launch_mirror_scatter(int64_t n, const int32_t* row, const int32_t* col, const int64_t* rb,
+                          int P, unsigned long long* cursor, int32_t* out, cudaStream_t st);
+int launch_mirror_append(int64_t n, const int32_t* in, int64_t r0, int32_t* prow, int32_t* pcol,
+                         int64_t start, int32_t* row_cnt, cudaStream_t st);
 
 // Per-column constants of the filter bound from Xt (f32).
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st);

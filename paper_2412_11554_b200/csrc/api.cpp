@@ -242,6 +242,14 @@ struct accord_ctx {
   int64_t audit_ld = 0;
   bool plan_a_x = false;                   // plan A map 2 = X^T_hi rows (lambda_max)
   int lanczos_steps = 0;                   // diagnostic (ACCORD_TRACE)
+  // symmetric first GEMM across ranks (EpiParams::sym = 2)
+  bool sym2_ok = false;                    // every rank's block starts on a 256-row tile
+  std::vector<int64_t> rb;                 // all ranks' global row boundaries [world + 1]
+  int64_t* rb_dev = nullptr;
+  int32_t *mir_row = nullptr, *mir_col = nullptr, *mir_send = nullptr, *mir_recv = nullptr;
+  unsigned long long* mir_cnt = nullptr;   // [1 + 2 world]: written, per-owner counts, cursors
+  int64_t mir_cap = 0, mir_recv_cap = 0, mir_recv_n = 0;
+  int64_t mirrored_sent = 0;               // cumulative (diagnostic, accord_info)
 
   // bias-correction refit (Eq. 3.8): fixed support S_hat, penalty phi * lambda
   bool refit = false;
@@ -1046,6 +1054,35 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     }
     c->sr = prm->sendrecv;
   }
+  if (c->world > 1 && !c->sharded) {
+    // every rank's row block (the owner of a mirrored entry of the symmetric
+    // first GEMM); the cyclic tile schedule needs blocks on 256-row tiles
+    const int P = c->world;
+    std::vector<double> mine(2 * P, 0.0), tot(2 * P, 0.0);
+    mine[2 * c->rank] = (double)c->r0;
+    mine[2 * c->rank + 1] = (double)c->r1;
+    for (int q = 0; q < 2 * P; q += 8) {
+      const int cnt = std::min(8, 2 * P - q);
+      CK(cudaMemcpyAsync(c->red_d, mine.data() + q, cnt * 8, cudaMemcpyHostToDevice, c->st));
+      allreduce(c, c->red_d, c->h_red, cnt);
+      std::memcpy(tot.data() + q, c->h_red, cnt * 8);
+    }
+    c->rb.assign(P + 1, 0);
+    bool ok = P <= 64;
+    for (int q = 0; q < P; ++q) {
+      c->rb[q] = (int64_t)tot[2 * q];
+      if (q > 0 && (int64_t)tot[2 * q] != (int64_t)tot[2 * q - 1]) ok = false;
+      if (c->rb[q] % kRowPad != 0) ok = false;
+    }
+    c->rb[P] = (int64_t)tot[2 * P - 1];
+    if (c->rb[0] != 0 || c->rb[P] != c->p) ok = false;
+    c->sym2_ok = ok;
+    if (ok) {
+      c->rb_dev = c->dalloc<int64_t>(P + 1);
+      CK(cudaMemcpyAsync(c->rb_dev, c->rb.data(), (P + 1) * 8, cudaMemcpyHostToDevice, c->st));
+      c->mir_cnt = c->dalloc<unsigned long long>(1 + 2 * P);
+    }
+  }
   const int64_t pv = c->sharded ? c->pk : c->p;   // variables held in Xt
   c->xrows_pad = c->sharded ? c->pk_pad : c->p_pad;
 
@@ -1305,6 +1342,122 @@ float ev_ms(accord_ctx* c, int a, int b) {
 
 double lam_eff(const accord_ctx* c) { return c->refit ? c->phi * c->lam : c->lam; }
 
+// ---- symmetric first GEMM across ranks: the mirrored entries' exchange ----
+void grow_mirror(accord_ctx* c, int64_t need) {
+  const int64_t cap = need + need / 4 + (1 << 20);
+  c->dfree(c->mir_row, c->mir_cap * 4);
+  c->dfree(c->mir_col, c->mir_cap * 4);
+  c->dfree(c->mir_send, c->mir_cap * 8);
+  c->mir_row = c->dalloc<int32_t>(cap);
+  c->mir_col = c->dalloc<int32_t>(cap);
+  c->mir_send = c->dalloc<int32_t>(2 * cap);
+  c->mir_cap = cap;
+}
+
+// Send every mirrored entry (global row k, column i) to the rank owning row
+// k and receive this rank's into mir_recv (mir_recv_n entries). Collective.
+void mirror_exchange(accord_ctx* c, int64_t n_out) {
+  const int P = c->world;
+  cudaStream_t S = c->st;
+  unsigned long long* dcnt = c->mir_cnt + 1;
+  unsigned long long* dcur = c->mir_cnt + 1 + P;
+  CK(cudaMemsetAsync(dcnt, 0, P * 8, S));
+  c->launches += launch_mirror_count(n_out, c->mir_row, c->rb_dev, P, dcnt, S);
+  std::vector<unsigned long long> cnt(P), off(P, 0);
+  CK(cudaMemcpyAsync(cnt.data(), dcnt, P * 8, cudaMemcpyDeviceToHost, S));
+  csync(c, S);
+  for (int q = 1; q < P; ++q) off[q] = off[q - 1] + cnt[q - 1];
+  CK(cudaMemcpyAsync(dcur, off.data(), P * 8, cudaMemcpyHostToDevice, S));
+  c->launches += launch_mirror_scatter(n_out, c->mir_row, c->mir_col, c->rb_dev, P, dcur,
+                                       c->mir_send, S);
+  // counts[src][dst] on every rank
+  std::vector<double> m(P * P, 0.0);
+  for (int q = 0; q < P; ++q) m[c->rank * P + q] = (double)cnt[q];
+  for (int q = 0; q < P * P; q += 16) {
+    const int k = std::min(16, P * P - q);
+    CK(cudaMemcpyAsync(c->red_d, m.data() + q, k * 8, cudaMemcpyHostToDevice, S));
+    allreduce(c, c->red_d, c->h_red, k);
+    std::memcpy(m.data() + q, c->h_red, k * 8);
+  }
+  std::vector<int64_t> rc(P), roff(P, 0);
+  int64_t R = 0;
+  for (int q = 0; q < P; ++q) {
+    rc[q] = (int64_t)m[q * P + c->rank];
+    roff[q] = R;
+    R += rc[q];
+  }
+  if (R > c->mir_recv_cap) {
+    c->dfree(c->mir_recv, c->mir_recv_cap * 8);
+    c->mir_recv_cap = R + R / 4 + 1024;
+    c->mir_recv = c->dalloc<int32_t>(2 * c->mir_recv_cap);
+  }
+  c->mir_recv_n = R;
+  for (int q = 0; q < P; ++q) c->mirrored_sent += (int64_t)cnt[q];
+  if (c->comm == ACCORD_COMM_NCCL) {
+    NcclApi* api = nccl_api();
+    if (!api->Send || !api->Recv) throw Fail{ACCORD_E_NCCL, "NCCL without send/recv"};
+    NK(api->GroupStart());
+    for (int q = 0; q < P; ++q) {
+      if (q == c->rank) continue;
+      if (cnt[q])
+        NK(api->Send(c->mir_send + 2 * off[q], cnt[q] * 8, ncclChar, q, c->nccl, S));
+      if (rc[q])
+        NK(api->Recv(c->mir_recv + 2 * roff[q], (size_t)rc[q] * 8, ncclChar, q, c->nccl, S));
+    }
+    NK(api->GroupEnd());
+    csync(c, S);
+    return;
+  }
+  // host transport (tests): every rank gathers [counts | pairs] of all ranks
+  if (!c->agv) throw Fail{ACCORD_E_INVALID, "multi-rank host comm needs allgatherv"};
+  std::vector<char> mineb(P * 8 + n_out * 8);
+  for (int q = 0; q < P; ++q) {
+    const int64_t v = (int64_t)cnt[q];
+    std::memcpy(mineb.data() + q * 8, &v, 8);
+  }
+  if (n_out)
+    CK(cudaMemcpyAsync(mineb.data() + P * 8, c->mir_send, n_out * 8, cudaMemcpyDeviceToHost, S));
+  csync(c, S);
+  std::vector<int64_t> counts(P, 0);
+  if (c->agv(c->cu, mineb.data(), (int64_t)mineb.size(), nullptr, counts.data()) != 0)
+    throw Fail{ACCORD_E_COMM, "allgatherv (sizes) failed"};
+  int64_t all = 0;
+  for (auto x : counts) all += x;
+  std::vector<char> buf(all);
+  if (c->agv(c->cu, mineb.data(), (int64_t)mineb.size(), buf.data(), counts.data()) != 0)
+    throw Fail{ACCORD_E_COMM, "allgatherv failed"};
+  std::vector<int32_t> recv(2 * std::max<int64_t>(R, 1));
+  const char* rd = buf.data();
+  for (int q = 0; q < P; ++q) {
+    std::vector<int64_t> cq(P);
+    std::memcpy(cq.data(), rd, P * 8);
+    int64_t o = 0;
+    for (int d = 0; d < c->rank; ++d) o += cq[d];
+    if (q != c->rank && cq[c->rank])
+      std::memcpy(recv.data() + 2 * roff[q], rd + P * 8 + o * 8, cq[c->rank] * 8);
+    rd += counts[q];
+  }
+  if (R) CK(cudaMemcpyAsync(c->mir_recv, recv.data(), R * 8, cudaMemcpyHostToDevice, S));
+  csync(c, S);
+}
+
+// Append the received mirrored entries to the pool as chunks [used, used+needc).
+void mirror_append(accord_ctx* c, int64_t used, int64_t needc) {
+  cudaStream_t S = c->st;
+  const int64_t R = c->mir_recv_n;
+  c->launches += launch_mirror_append(R, c->mir_recv, c->r0, c->pool_row, c->pool_col,
+                                      used * c->chunk, c->row_cnt, S);
+  if (needc > 0) {
+    std::vector<unsigned long long> fill(needc, (unsigned long long)c->chunk);
+    fill.back() = (unsigned long long)(R - (needc - 1) * c->chunk);
+    CK(cudaMemcpyAsync(c->chunk_fill + used, fill.data(), needc * 8, cudaMemcpyHostToDevice, S));
+    const unsigned int nx = (unsigned int)(used + needc);
+    CK(cudaMemcpyAsync(c->chunk_next, &nx, 4, cudaMemcpyHostToDevice, S));
+    csync(c, S);   // the host vectors go out of scope
+  }
+  c->h_seg[1] = used + needc;
+}
+
 // Operands of a gradient pass other than the current iterate's (lambda_max:
 // A = the rank's rows of X^T, i.e. Omega = I, with an empty support).
 struct GradOverride {
@@ -1340,6 +1493,12 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     return;
   }
   // ---------------- a2 + a3: gradient GEMM with the fused epilogue --------
+  // several ranks at Omega = I: the cyclic half of the symmetric GEMM, with
+  // the mirrored entries of other ranks' rows exchanged after it
+  const bool sym2 = !ov && c->sym2_ok && c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER &&
+                    !std::getenv("ACCORD_GEMM_NOSYM");
+  bool exchanged = false;
+  if (sym2 && !c->mir_row) grow_mirror(c, std::max<int64_t>(c->pk * 64, 1 << 20));
   for (;;) {
     CK(cudaMemsetAsync(c->row_cnt, 0, c->pk * 4, S));
     CK(cudaMemsetAsync(c->chunk_fill, 0, c->nchunks * 8, S));
@@ -1366,6 +1525,16 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     // Omega = I on one rank: G = S is symmetric, half the tiles (ACCORD_GEMM_NOSYM: off)
     ep.sym = c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && c->world == 1 &&
              !c->sharded && c->r0 == 0 && c->pk == c->p && !std::getenv("ACCORD_GEMM_NOSYM");
+    if (sym2) {
+      ep.sym = 2;
+      ep.mt0 = (int)(c->r0 / kRowPad);
+      ep.nt = (int)(c->p_pad / kRowPad);
+      ep.mir_row = c->mir_row;
+      ep.mir_col = c->mir_col;
+      ep.mir_cnt = c->mir_cnt;
+      ep.mir_cap = c->mir_cap;
+      CK(cudaMemsetAsync(c->mir_cnt, 0, 8, S));
+    }
     ep.audit_acc = c->audit_acc;
     ep.audit_ld = c->audit_ld;
     OmegaView omv = omega_view(c);
@@ -1405,10 +1574,12 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], S));
     TR(c, "gemm");
+    unsigned long long h_mir = 0;
     {
       unsigned int used = 0;
       CK(cudaMemcpyAsync(&used, c->chunk_next, 4, cudaMemcpyDeviceToHost, S));
       CK(cudaMemcpyAsync(c->h_seg, c->chunk_fill, 8, cudaMemcpyDeviceToHost, S));
+      if (sym2) CK(cudaMemcpyAsync(&h_mir, c->mir_cnt, 8, cudaMemcpyDeviceToHost, S));
       csync(c, S);
       c->h_seg[1] = used;
     }
@@ -1425,7 +1596,26 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       allreduce(c, c->red_d, c->h_red, 1);
       ovf_any = c->h_red[0] > 0;
     }
-    if (!ovf_any) break;
+    if (sym2 && (int64_t)h_mir > c->mir_cap) {   // mirror buffer overflow: grow, redo locally
+      grow_mirror(c, (int64_t)h_mir);
+      if (!ovf) continue;
+    }
+    if (!ovf_any) {
+      if (!sym2) break;
+      if (!exchanged) {   // collective, once (a local redo regenerates the same entries)
+        mirror_exchange(c, (int64_t)h_mir);
+        exchanged = true;
+      }
+      const int64_t used = (int64_t)c->h_seg[1];
+      const int64_t needc = (c->mir_recv_n + c->chunk - 1) / c->chunk;
+      if (used + needc <= c->nchunks) {
+        mirror_append(c, used, needc);
+        break;
+      }
+      const int64_t want = (used + needc) * c->chunk;   // room for the received entries
+      grow(c, want + want / 4 + (1 << 20), c->nnz_local);
+      continue;
+    }
     if (!ovf) continue;
     const int64_t want = need + need / 4 + (1 << 20);
     if (want >= (int64_t)UINT32_MAX)
@@ -2342,6 +2532,7 @@ accord_status accord_get_info(accord_ctx* c, accord_info* info) {
   info->device_bytes = c->bytes;
   info->workspace_bytes = c->arena.size;
   info->workspace_high = c->arena.high;
+  info->mirrored_sent = c->mirrored_sent;
   return ACCORD_OK;
 }
 

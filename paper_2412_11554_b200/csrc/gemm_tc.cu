@@ -87,15 +87,27 @@ struct Sched {
   int num_m, num_n, GN, U;
   int full_groups, rem, spu, spu_last;
   long long units_full, units;
-  bool sym;   // upper triangle only (N-block >= M-block), see EpiParams::sym
-  __device__ Sched(int nm, int nn, int gn, int u, bool sy)
-      : num_m(nm), num_n(nn), GN(gn), U(u), sym(sy) {
+  // symmetric G (EpiParams::sym): 1 = upper triangle only (one rank), 2 = the
+  // cyclic half across ranks: tile (I, J) of global row tile I = mt0 + m runs
+  // iff d = (J - I) mod nt is 0 or <= (nt-1)/2 (d = nt/2: iff I < J), so each
+  // unordered pair of tiles runs once and every row tile runs ~half its tiles
+  int sym, mt0, nt;
+  __device__ Sched(int nm, int nn, int gn, int u, int sy, int m0, int ntg)
+      : num_m(nm), num_n(nn), GN(gn), U(u), sym(sy), mt0(m0), nt(ntg) {
     full_groups = num_n / GN;
     rem = num_n - full_groups * GN;
     spu = (GN + U - 1) / U;
     spu_last = (rem + U - 1) / U;
     units_full = (long long)full_groups * num_m * spu;
     units = units_full + (long long)num_m * spu_last;
+  }
+  __device__ bool valid(int m, int n) const {
+    if (sym != 2) return sym == 0 || n >= m;
+    const int I = mt0 + m;
+    if (n == I) return true;
+    const int d = ((n - I) % nt + nt) % nt;
+    if (d <= (nt - 1) / 2) return true;
+    return (nt % 2 == 0) && d == nt / 2 && I < n;
   }
   // unit -> (M-block, first N-block, count)
   __device__ void unit(long long u, int& m, int& n0, int& cnt) const {
@@ -134,14 +146,25 @@ struct TileIt {
       if (!ok) return;
       S.unit(u, m, n0, cnt);
       if (!S.sym) return;
-      if (n0 + cnt - 1 < m) { u += stride; continue; }   // whole unit below the diagonal
-      if (n0 < m) ni = m - n0;
+      if (S.sym == 1) {
+        if (n0 + cnt - 1 < m) { u += stride; continue; }   // whole unit below the diagonal
+        if (n0 < m) ni = m - n0;
+        return;
+      }
+      while (ni < cnt && !S.valid(m, n0 + ni)) ++ni;
+      if (ni == cnt) { u += stride; continue; }
       return;
     }
   }
   __device__ void next() {
     start = false;
-    if (++ni == cnt) { u += stride; load(); }
+    ++ni;
+    if (S.sym == 2)
+      while (ni < cnt && !S.valid(m, n0 + ni)) {   // a gap: the row walk restarts after it
+        ++ni;
+        start = true;
+      }
+    if (ni == cnt) { u += stride; load(); }
   }
   __device__ int n() const { return n0 + ni; }
   __device__ bool unit_start() const { return start; }
@@ -176,7 +199,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const Sched sched(num_m, num_n, group_n, unit_n, kMode == 1 && ep.sym != 0);
+  const Sched sched(num_m, num_n, group_n, unit_n, kMode == 1 ? ep.sym : 0, ep.mt0, ep.nt);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&mA_hi);
@@ -384,13 +407,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           const int64_t sp0 = sp;
           if constexpr (kDiag == 1) {   // audit: the raw accumulator of every computed entry
             if (row_ok) {
-              const bool mir = sched.sym && it.n() != it.m;
+              const bool mir = sched.sym && it.n() != sched.mt0 + it.m;
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
                 const int64_t k = c0 + c;
                 if (k < col_end) {
                   ep.audit_acc[r * ep.audit_ld + k] = __uint_as_float(v[c]);
-                  if (mir) ep.audit_acc[k * ep.audit_ld + gi] = __uint_as_float(v[c]);
+                  if (mir && k >= ep.r0 && k < ep.r0 + ep.pk)
+                    ep.audit_acc[(k - ep.r0) * ep.audit_ld + gi] = __uint_as_float(v[c]);
                 }
               }
             }
@@ -457,9 +481,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           }
           if (__ballot_sync(0xffffffffu, mask != 0u) == 0u) continue;
           // sym, off-diagonal tile: each survivor (i,k) is also (k,i) (G = G^T;
-          // the bound on |acc_ik - G_ik| is one on |acc_ik - G_ki|)
-          const bool mirror = kMode == 1 && sched.sym && it.n() != it.m;
-          const int cnt = __popc(mask) << (mirror ? 1 : 0);
+          // the bound on |acc_ik - G_ik| is one on |acc_ik - G_ki|). Row k is
+          // this rank's (into the pool) or another rank's (into the mirror
+          // buffer, sent after the GEMM); a 32-column chunk never straddles a
+          // rank boundary (multiples of 256)
+          const bool mirror = kMode == 1 && sched.sym && it.n() != sched.mt0 + it.m;
+          const bool mir_local = mirror && (int64_t)c0 >= ep.r0 && (int64_t)c0 < ep.r0 + ep.pk;
+          const bool mir_remote = mirror && !mir_local;
+          const int cnt = __popc(mask) << (mir_local ? 1 : 0);
           const int total = __reduce_add_sync(0xffffffffu, cnt);
           int incl = cnt;
 #pragma unroll
@@ -479,6 +508,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           int64_t pos = chunk_id * pool.chunk + fill + (incl - cnt);
           fill += total;
           row_count += cnt;
+          int64_t rpos = 0;
+          if (mir_remote) {   // warp-aggregated reservation in the mirror buffer
+            const int rc = __popc(mask);
+            int rincl = rc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, rincl, o);
+              if (lane >= o) rincl += y;
+            }
+            const int rtot = __shfl_sync(0xffffffffu, rincl, 31);
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(ep.mir_cnt, (unsigned long long)rtot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            rpos = (int64_t)base + rincl - rc;
+          }
           if constexpr (kMode == 1) {
             // candidate positions only: the exact values come from the refine
             // SDDMM and omega_ik from a lookup in Omega's CSR after the sort
@@ -492,16 +536,23 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                 pool.col[pos] = c0 + c;
               }
               ++pos;
-              if (mirror) {
+              if (mir_local) {
+                const int32_t kr = (int32_t)(c0 + c - ep.r0);
                 if (writable) {
-                  pool.row[pos] = c0 + c;
-                  pool.col[pos] = (int32_t)r;
+                  pool.row[pos] = kr;
+                  pool.col[pos] = (int32_t)gi;
                 }
                 ++pos;
-                atomicAdd(&pool.row_cnt[c0 + c], 1);
+                atomicAdd(&pool.row_cnt[kr], 1);
+              } else if (mir_remote) {
+                if (rpos < ep.mir_cap) {
+                  ep.mir_row[rpos] = c0 + c;
+                  ep.mir_col[rpos] = (int32_t)gi;
+                }
+                ++rpos;
               }
             }
-            if (mirror) row_count -= cnt >> 1;   // row r gained only the direct half
+            if (mir_local) row_count -= cnt >> 1;   // row r gained only the direct half
           } else if (cnt) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) {

@@ -884,6 +884,57 @@ __global__ void __launch_bounds__(256) gram_offdiag_max_kernel(int64_t pk, int64
   }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric first GEMM across ranks (EpiParams::sym = 2): the mirrored
+// entries (k, i) of rows k another rank owns are bucketed by owner, sent, and
+// the received ones appended to the candidate pool as extra chunks.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int owner_of(int64_t k, const int64_t* __restrict__ rb, int P) {
+  int q = 0;
+  while (q + 1 < P && k >= rb[q + 1]) ++q;
+  return q;
+}
+
+__global__ void mirror_count_kernel(int64_t n, const int32_t* __restrict__ row,
+                                    const int64_t* __restrict__ rb, int P,
+                                    unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned int sc[64];
+  for (int q = threadIdx.x; q < P; q += blockDim.x) sc[q] = 0;
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&sc[owner_of(row[e], rb, P)], 1u);
+  __syncthreads();
+  for (int q = threadIdx.x; q < P; q += blockDim.x)
+    if (sc[q]) atomicAdd(&cnt[q], (unsigned long long)sc[q]);
+}
+
+__global__ void mirror_scatter_kernel(int64_t n, const int32_t* __restrict__ row,
+                                      const int32_t* __restrict__ col,
+                                      const int64_t* __restrict__ rb, int P,
+                                      unsigned long long* __restrict__ cursor,
+                                      int32_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = row[e];
+    const unsigned long long pos = atomicAdd(&cursor[owner_of(k, rb, P)], 1ull);
+    out[2 * pos] = k;
+    out[2 * pos + 1] = col[e];
+  }
+}
+
+__global__ void mirror_append_kernel(int64_t n, const int32_t* __restrict__ in, int64_t r0,
+                                     int32_t* __restrict__ prow, int32_t* __restrict__ pcol,
+                                     int64_t start, int32_t* __restrict__ row_cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(in[2 * e] - r0);
+    prow[start + e] = r;
+    pcol[start + e] = in[2 * e + 1];
+    atomicAdd(&row_cnt[r], 1);
+  }
+}
+
 // per-column constants of the filter bound (warp per column of X = row of Xt)
 __global__ void col_norms_kernel(int64_t p, int64_t ldk, const float* __restrict__ Xt,
                                  float2* __restrict__ col_sd) {
@@ -1398,6 +1449,27 @@ int launch_gram_offdiag_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_
         pk, r0, n, ldk, (const float*)Xi, (const float*)Xt, v0, v1, accumulate, row_max);
   if (out) reduce_max_kernel<<<1, 1024, 0, st>>>(pk, row_max, out);
   return out ? 2 : 1;
+}
+
+int launch_mirror_count(int64_t n, const int32_t* row, const int64_t* rb, int P,
+                        unsigned long long* cnt, cudaStream_t st) {
+  if (n == 0) return 0;
+  mirror_count_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, row, rb, P, cnt);
+  return 1;
+}
+
+int launch_mirror_scatter(int64_t n, const int32_t* row, const int32_t* col, const int64_t* rb,
+                          int P, unsigned long long* cursor, int32_t* out, cudaStream_t st) {
+  if (n == 0) return 0;
+  mirror_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, row, col, rb, P, cursor, out);
+  return 1;
+}
+
+int launch_mirror_append(int64_t n, const int32_t* in, int64_t r0, int32_t* prow, int32_t* pcol,
+                         int64_t start, int32_t* row_cnt, cudaStream_t st) {
+  if (n == 0) return 0;
+  mirror_append_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, in, r0, prow, pcol, start, row_cnt);
+  return 1;
 }
 
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st) {

@@ -63,7 +63,7 @@ int main(void) {
   P(accord_init_params, stream) P(accord_init_params, cand_capacity)
   P(accord_init_params, x_sharded) P(accord_init_params, sendrecv)
   P(accord_init_params, workspace) P(accord_init_params, workspace_bytes)
-  P(accord_info, workspace_bytes) P(accord_info, workspace_high)
+  P(accord_info, workspace_bytes) P(accord_info, workspace_high) P(accord_info, mirrored_sent)
   P(accord_iter_stats, nnz) P(accord_iter_stats, trials) P(accord_iter_stats, ms_total)
   P(accord_info, f) P(accord_info, device_bytes) P(accord_info, kernel_launches)
   return 0;

@@ -103,7 +103,7 @@ def test_thread_comm_three_ranks():
 
 
 # ----------------------------------------------------------------- GPU -----
-def run_ranks(Xt, lam, T, inv_L, P, gemm, align=256):
+def run_ranks(Xt, lam, T, inv_L, P, gemm, align=256, infos=None):
     import torch
     comm = ThreadComm(P)
     bounds = A.partition_rows(Xt.shape[0], P, align=align)
@@ -123,6 +123,8 @@ def run_ranks(Xt, lam, T, inv_L, P, gemm, align=256):
             g = s.export_csr(A.SCOPE_GATHER)
             loc = s.export_csr(A.SCOPE_LOCAL)
             f = s.objective()[0]
+            if infos is not None:
+                infos[r] = s.info()
             s.close()
             out[r] = (st, g, loc, f)
         except Exception as e:      # surface in the main thread
@@ -190,6 +192,44 @@ def test_mixed_block_sizes_agree_on_the_spmm_kind():
         assert abs(f - ref[0][3]) <= 1e-9 * abs(f)
         assert np.array_equal(g.row_ptr, ref[0][1].row_ptr) and np.array_equal(g.col, ref[0][1].col)
         assert np.abs(g.val - ref[0][1].val).max() <= 1e-6 * np.abs(ref[0][1].val).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_symmetric_first_gemm_across_ranks(P, monkeypatch):
+    """At Omega = I several ranks run the cyclic half of the symmetric GEMM
+    (each unordered pair of 256-tiles once, ~half of every rank's tiles) and
+    send the mirrored candidate positions of other ranks' rows to their owner
+    (host transport here; NCCL send/recv in production). The run equals the
+    P = 1 run and the P-rank run without the symmetric schedule."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import make_problem
+    from oracle import accord_oracle as O
+    pr = make_problem("t_mid_f32")          # p = 3000: 12 tiles, blocks on tile boundaries
+    c = pr.cfg
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    ref, _ = run_ranks(pr.Xt, c.lambdas[0], 6, inv_L, 1, A.GEMM_BF16_FILTER)
+    infos = [None] * P
+    out, bounds = run_ranks(pr.Xt, c.lambdas[0], 6, inv_L, P, A.GEMM_BF16_FILTER, infos=infos)
+    assert all(b % 256 == 0 for b, _ in bounds)
+    assert sum(i["mirrored_sent"] for i in infos) > 0          # the exchange ran
+    monkeypatch.setenv("ACCORD_GEMM_NOSYM", "1")
+    full, _ = run_ranks(pr.Xt, c.lambdas[0], 6, inv_L, P, A.GEMM_BF16_FILTER)
+    W1 = ref[0][1].to_dense(c.p)
+    for r in range(P):
+        for run in (out, full):
+            st, g, loc, f = run[r]
+            assert [x["tau"] for x in st] == [x["tau"] for x in ref[0][0]]
+            assert abs(f - ref[0][3]) <= 1e-9 * abs(f)
+            Wg = g.to_dense(c.p)
+            assert np.array_equal(Wg != 0, W1 != 0)
+            assert np.abs(Wg - W1).max() <= 1e-6 * np.abs(W1).max()
+    # the schedule is the symmetric one: iteration 1's |C| equals the P = 1 run's
+    # (the same certified rule from the mirrored side) within the filter slack
+    n1 = ref[0][0][0]["n_cand"]
+    assert abs(out[0][0][0]["n_cand"] - n1) <= 0.05 * n1
 
 
 @pytest.mark.gpu
