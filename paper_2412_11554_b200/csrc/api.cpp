@@ -1495,8 +1495,10 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
   // ---------------- a2 + a3: gradient GEMM with the fused epilogue --------
   // several ranks at Omega = I: the cyclic half of the symmetric GEMM, with
   // the mirrored entries of other ranks' rows exchanged after it
-  const bool sym2 = !ov && c->sym2_ok && c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER &&
-                    !std::getenv("ACCORD_GEMM_NOSYM");
+  // (not under the filter audit: another rank's mirrored accumulators would
+  // be missing from this rank's dump)
+  const bool sym2 = !ov && !c->audit_acc && c->sym2_ok && c->omega_identity &&
+                    c->gemm == ACCORD_GEMM_BF16_FILTER && !std::getenv("ACCORD_GEMM_NOSYM");
   bool exchanged = false;
   if (sym2 && !c->mir_row) grow_mirror(c, std::max<int64_t>(c->pk * 64, 1 << 20));
   for (;;) {

@@ -487,7 +487,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           // rank boundary (multiples of 256)
           const bool mirror = kMode == 1 && sched.sym && it.n() != sched.mt0 + it.m;
           const bool mir_local = mirror && (int64_t)c0 >= ep.r0 && (int64_t)c0 < ep.r0 + ep.pk;
+#ifdef ACCORD_NO_SYM2   // A-B diagnostic build: the single-rank epilogue only
+          const bool mir_remote = false;
+#else
           const bool mir_remote = mirror && !mir_local;
+#endif
           const int cnt = __popc(mask) << (mir_local ? 1 : 0);
           const int total = __reduce_add_sync(0xffffffffu, cnt);
           int incl = cnt;

@@ -207,8 +207,11 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
   for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
   int stage = 0;
   uint32_t phase = 0;
-  double* sh_red = red;                                   // [16] per-warp partials x 5
-  volatile int* sh_flag = reinterpret_cast<volatile int*>(red + 80);
+  // per-warp partials of a finished row, x 5 quantities, double-buffered by
+  // row parity: thread 0 sums row q from one buffer while the other warps may
+  // already write row q+1 into the other, so one barrier per row suffices
+  int rowpar = 0;
+  volatile int* sh_flag = reinterpret_cast<volatile int*>(red + 160);
   auto accumulate = [&](double w, double d, double d2, float4 x0, float4 x1) {
     const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
@@ -254,8 +257,13 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     }
     const bool last = (f0 & kFlagLast) || (f1 & kFlagLast);
     const int ls = (f0 & kFlagLast) ? stage : s1;
-    StageMeta m;
-    if (last) m = meta[ls];   // row / chunk of the finished item (before the release)
+    int64_t m_row = 0;        // row / chunk of the finished item (read before the release)
+    int m_chunk = 0, m_nch = 1;
+    if (last) {
+      m_row = meta[ls].row;
+      m_chunk = meta[ls].chunk;
+      m_nch = meta[ls].nch;
+    }
     accumulate(w0, d0, e0d, a0, b0);
     if (two) accumulate(w1, d1, e1d, a1, b1);
     __syncwarp();
@@ -271,24 +279,24 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     if (!last) continue;
 
     // ---------------- item complete: finalize the row (or its partial) ----
-    const int64_t r = m.row;
+    const int64_t r = m_row;
     bool finish = true;
-    if (m.nch > 1) {
+    if (m_nch > 1) {
       const int64_t slot0 = items.slot_ptr[r];
       if (active) {
-        double* py = items.part_y + (slot0 + m.chunk) * ldk + c0;
-        double* pd = items.part_d + (slot0 + m.chunk) * ldk + c0;
+        double* py = items.part_y + (slot0 + m_chunk) * ldk + c0;
+        double* pd = items.part_d + (slot0 + m_chunk) * ldk + c0;
 #pragma unroll
         for (int v = 0; v < kCols; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
         if constexpr (kPair) {
-          double* pe = items.part_d2 + (slot0 + m.chunk) * ldk + c0;
+          double* pe = items.part_d2 + (slot0 + m_chunk) * ldk + c0;
 #pragma unroll
           for (int v = 0; v < kCols; ++v) pe[v] = ae[v];
         }
       }
       __threadfence();
       named_sync(1, nct);
-      if (t == 0) *sh_flag = (atomicAdd(&items.row_done[r], 1) == m.nch - 1) ? 1 : 0;
+      if (t == 0) *sh_flag = (atomicAdd(&items.row_done[r], 1) == m_nch - 1) ? 1 : 0;
       named_sync(1, nct);
       finish = *sh_flag != 0;
       if (finish) {
@@ -296,7 +304,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         if (active) {
 #pragma unroll
           for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
-          for (int k = 0; k < m.nch; ++k) {   // chunk order: deterministic sum
+          for (int k = 0; k < m_nch; ++k) {   // chunk order: deterministic sum
             const double* py = items.part_y + (slot0 + k) * ldk + c0;
             const double* pd = items.part_d + (slot0 + k) * ldk + c0;
 #pragma unroll
@@ -358,6 +366,8 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       b2 = wsum(b2);
       if constexpr (kPair) e2 = wsum(e2);
       const int cw = warp - 1;
+      double* sh_red = red + rowpar * 80;
+      rowpar ^= 1;
       if (lane == 0) {
         sh_red[cw] = d2;
         sh_red[16 + cw] = y2;
@@ -384,7 +394,6 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
           if (row_B) row_B[r] = __double2float_ru(sqrt(s3) * (1.0 + 1e-12));
         }
       }
-      named_sync(1, nct);
     }
 #pragma unroll
     for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
@@ -653,7 +662,7 @@ size_t spmm_tma_smem(int64_t ldk, int* stages) {
   if (const char* e = std::getenv("ACCORD_SPMM_STAGES")) want = std::max(2, std::atoi(e));
   int s = (int)std::min<int64_t>(want, std::max<int64_t>(2, (want * 4096) / sb));
   *stages = s;
-  return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 81 * 8 + 64;
+  return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 161 * 8 + 64;
 }
 
 size_t refine_tma_smem(int64_t ldk) {
