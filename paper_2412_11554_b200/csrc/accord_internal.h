@@ -249,6 +249,10 @@ int launch_refine_tma(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                       const int32_t* c_col, const float* Y, const float* Xt, float* c_g,
                       const int64_t* itm_ptr, const int32_t* item_row, int64_t n_items, int64_t L,
                       int sm_count, cudaStream_t st);
+// groups of 8 work items per block of 4 warps, Y rows staged (F32, ldk <= 1024)
+int launch_refine_group(int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
+                        const float* Y, const float* Xt, float* c_g, const int64_t* itm_ptr,
+                        const int32_t* item_row, int64_t n_items, int64_t L, cudaStream_t st);
 int launch_refine_flat(int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
                        const float* Y, const float* Xt, float* c_g, const int64_t* itm_ptr,
                        const int32_t* item_row, int64_t n_items, int64_t L, int sm_count,

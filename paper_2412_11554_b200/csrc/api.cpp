@@ -553,7 +553,11 @@ void refine_all(accord_ctx* c, const void* yrows = nullptr) {
   if (!c->sharded) {
     // hub rows (up to ~1.6e5 candidates) split over several work items
     if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
-    if (c->dtype == ACCORD_F32 && c->refine_kind == 2) {
+    if (c->dtype == ACCORD_F32 && c->refine_kind == 4 && c->ldk <= 1024) {
+      c->launches += launch_refine_group(c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
+                                         (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
+                                         c->item_row, c->n_items, kItemEntries, c->st);
+    } else if (c->dtype == ACCORD_F32 && c->refine_kind == 2) {
       c->launches += launch_refine_tma(c->pk, c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
                                        (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
                                        c->item_row, c->n_items, kItemEntries, c->sm_count, c->st);
@@ -1235,8 +1239,9 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   {
     const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
     c->pair_ls = !(e && e[0] == '0');
-    const char* r = std::getenv("ACCORD_REFINE");     // A-B switch: block | flat | tma | ff
-    if (r) c->refine_kind = r[0] == 'b' ? 0 : r[0] == 'f' && r[1] == 'l' ? 1 : r[0] == 't' ? 2 : 3;
+    const char* r = std::getenv("ACCORD_REFINE");     // A-B: block | flat | tma | ff | group
+    if (r) c->refine_kind = r[0] == 'b' ? 0 : r[0] == 'f' && r[1] == 'l' ? 1 : r[0] == 't' ? 2
+                                                          : r[0] == 'g' ? 4 : 3;
   }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);

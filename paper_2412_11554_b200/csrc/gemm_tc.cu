@@ -170,7 +170,11 @@ struct TileIt {
   __device__ bool unit_start() const { return start; }
 };
 
-// kDiag: 0 = the product epilogue; 1 = audit (also writes every raw fp32
+// kDiag: 0 = the product epilogue; 3 = the same for the symmetric first GEMM
+// across ranks (EpiParams::sym = 2: the only instantiation with the mirror
+// buffer path -- that branch, never taken elsewhere, cost ~2 % of the c5
+// GEMM through the power-capped clock when compiled into the product kernel);
+// 1 = audit (also writes every raw fp32
 // accumulator to ep.audit_acc, for the filter certification test); 2 = max
 // reduction (no emission: a certified lower bound on n max_{i!=k} |G_ik|
 // into *ep.max_out, the lambda_max of a path)
@@ -487,11 +491,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           // rank boundary (multiples of 256)
           const bool mirror = kMode == 1 && sched.sym && it.n() != sched.mt0 + it.m;
           const bool mir_local = mirror && (int64_t)c0 >= ep.r0 && (int64_t)c0 < ep.r0 + ep.pk;
-#ifdef ACCORD_NO_SYM2   // A-B diagnostic build: the single-rank epilogue only
-          const bool mir_remote = false;
-#else
-          const bool mir_remote = mirror && !mir_local;
-#endif
+          const bool mir_remote = kDiag == 3 && mirror && !mir_local;
           const int cnt = __popc(mask) << (mir_local ? 1 : 0);
           const int total = __reduce_add_sync(0xffffffffu, cnt);
           int incl = cnt;
@@ -513,7 +513,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           fill += total;
           row_count += cnt;
           int64_t rpos = 0;
-          if (mir_remote) {   // warp-aggregated reservation in the mirror buffer
+          if (kDiag == 3 && mir_remote) {   // warp-aggregated reservation in the mirror buffer
             const int rc = __popc(mask);
             int rincl = rc;
 #pragma unroll
@@ -548,7 +548,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                 }
                 ++pos;
                 atomicAdd(&pool.row_cnt[kr], 1);
-              } else if (mir_remote) {
+              } else if (kDiag == 3 && mir_remote) {
                 if (rpos < ep.mir_cap) {
                   ep.mir_row[rpos] = c0 + c;
                   ep.mir_col[rpos] = (int32_t)gi;
@@ -712,6 +712,8 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true, 2>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true, 3>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
     attr_done(attr_seen);
   }
   return p;
@@ -788,6 +790,9 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
         ACCORD_TC_ARGS(plan->b_hi[bsel]));
   else if (ep.max_out)
     gemm_tc_kernel<1, 6, true, 2><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
+  else if (ep.sym == 2)
+    gemm_tc_kernel<1, 6, true, 3><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_hi[bsel]));
   else if (var == 1)
     gemm_tc_kernel<1, 7, true><<<grid, kThreads, Cfg<1, 7>::kSmemBytes, st>>>(
