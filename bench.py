@@ -157,6 +157,25 @@ def cfg_problem(key, local_rank=0, local_world=1, barrier=None):
     return cfg, Xt
 
 
+def sample_rows(cfg, k, n_hub=16, seed=7):
+    """The oracle legs' row sample (SURVEY.md §8(c) sampled-row mode): seeded
+    random rows plus the n_hub highest-degree rows of the true graph Omega0.
+    The line-search sums are dominated by the few rows whose Delta has a
+    large support (high curvature ||Delta_i X^T||^2 / n ||Delta_i||^2), which
+    a purely random sample of 64 out of 1e6 rows almost never contains."""
+    from accord_inputs import make_omega0
+    p = cfg.p
+    rng = np.random.default_rng(seed)
+    rows = set(rng.choice(p, size=min(max(k - n_hub, 1), p), replace=False).tolist())
+    deg = np.zeros(p, dtype=np.int64)
+    off = 0
+    for b in make_omega0(cfg):
+        np.add.at(deg, off + b.rows, 1)
+        off += b.b
+    rows |= set(np.argsort(-deg, kind="stable")[:n_hub].tolist())
+    return np.array(sorted(rows), dtype=np.int64)
+
+
 def metric_name(cfg):
     return f"prox-grad iterations/s (ACCORD-FBS, p={cfg.p}, n={cfg.n})"
 
@@ -213,8 +232,7 @@ def _reference_rank0(args, world, cfg, Xt):
     from oracle import accord_oracle as O
     lam = cfg.lambdas[0]
     p = cfg.p
-    rng = np.random.default_rng(7)
-    rows = np.sort(rng.choice(p, size=min(args.ref_rows, p), replace=False))
+    rows = sample_rows(cfg, args.ref_rows)
     # 1/L as the GPU arm computes it (sigma_max(S)): the oracle's
     # eigvalsh of the n x n Gram (n <= 2000 for every config)
     t0 = time.perf_counter()
@@ -235,7 +253,8 @@ def _reference_rank0(args, world, cfg, Xt):
     per_iter = float(np.mean(times)) * p / len(rows)
     value = 1.0 / per_iter
     cores = threads_used()
-    sample = (f"{len(rows)} seeded rows of {cfg.name}: Algorithm 1 on the rows (every "
+    sample = (f"{len(rows)} rows of {cfg.name} (seeded random + the 16 highest-degree rows "
+              f"of Omega0): Algorithm 1 on the rows (every "
               f"line-search trial evaluated, the test on the sample's sums; "
               f"oracle.fbs_rows_ls), {args.warmup} untimed + {args.steps} timed iterations, "
               f"float64, mean time per iteration x p/{len(rows)} (extrapolated)")
@@ -268,8 +287,7 @@ def cpu_baseline_leg(Xt, cfg, lam, stats_all, n_warm, args):
     iterations untimed, then up to 5 of the timed ones."""
     from oracle import accord_oracle as O
     p = cfg.p
-    rng = np.random.default_rng(7)
-    rows = np.sort(rng.choice(p, size=min(args.cpu_rows, p), replace=False))
+    rows = sample_rows(cfg, args.cpu_rows)
     taus = [s["tau"] for s in stats_all]
     tt = [[cfg.tau0 * cfg.beta ** j for j in range(s["trials"])] for s in stats_all]
     Om = None
@@ -283,7 +301,8 @@ def cpu_baseline_leg(Xt, cfg, lam, stats_all, n_warm, args):
     per_iter = el * p / len(rows)
     return {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": threads_used(),
             "kind": "oracle",
-            "sample": f"{len(rows)} seeded rows of {cfg.name}: row replay of the GPU's "
+            "sample": f"{len(rows)} rows of {cfg.name} (seeded random + the 16 highest-degree "
+                      f"rows of Omega0): row replay of the GPU's "
                       f"iterations {n_warm + 1}..{n_warm + k} with its tau schedule and every "
                       f"trial evaluated (oracle.fbs_rows, trial_taus), float64, "
                       f"x p/{len(rows)} (extrapolated)"}

@@ -242,21 +242,6 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                     double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
                     cudaStream_t st, const float* wn2 = nullptr, double* row_D2b = nullptr);
 
-// TMA-staged refine (spmm_tma.cu), F32, all columns, over work items: one
-// producer warp streams the candidates' X^T rows (chunks of <= 4 KB, any n)
-// into private rings of 8 consumer warps (warp per candidate, f64 dot).
-int launch_refine_tma(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
-                      const int32_t* c_col, const float* Y, const float* Xt, float* c_g,
-                      const int64_t* itm_ptr, const int32_t* item_row, int64_t n_items, int64_t L,
-                      int sm_count, cudaStream_t st);
-// groups of 8 work items per block of 4 warps, Y rows staged (F32, ldk <= 1024)
-int launch_refine_group(int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
-                        const float* Y, const float* Xt, float* c_g, const int64_t* itm_ptr,
-                        const int32_t* item_row, int64_t n_items, int64_t L, cudaStream_t st);
-int launch_refine_flat(int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
-                       const float* Y, const float* Xt, float* c_g, const int64_t* itm_ptr,
-                       const int32_t* item_row, int64_t n_items, int64_t L, int sm_count,
-                       cudaStream_t st);
 // Columns [v0, v1) only, Xt row 0 = column v0 (one ring step of the sharded mode).
 // itm_ptr != NULL: one block per work item (row chunk of <= L candidates).
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,

@@ -214,7 +214,7 @@ struct accord_ctx {
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
-  int refine_kind = 0;                     // 0 block/f64, 1 flat, 2 TMA ring, 3 block/float-float (ACCORD_REFINE)
+  bool refine_ff = false;                  // refine in float-float (ACCORD_REFINE=ff: A-B, slower)
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
@@ -553,33 +553,18 @@ void refine_all(accord_ctx* c, const void* yrows = nullptr) {
   if (!c->sharded) {
     // hub rows (up to ~1.6e5 candidates) split over several work items
     if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
-    if (c->dtype == ACCORD_F32 && c->refine_kind == 4 && c->ldk <= 1024) {
-      c->launches += launch_refine_group(c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
-                                         (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
-                                         c->item_row, c->n_items, kItemEntries, c->st);
-    } else if (c->dtype == ACCORD_F32 && c->refine_kind == 2) {
-      c->launches += launch_refine_tma(c->pk, c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
-                                       (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
-                                       c->item_row, c->n_items, kItemEntries, c->sm_count, c->st);
-    } else if (c->dtype == ACCORD_F32 && c->refine_kind == 1) {
-      c->launches += launch_refine_flat(c->n, c->ldk, c->c_ptr, c->c_col, (const float*)Y,
-                                        (const float*)c->Xt, (float*)c->c_g, c->itm_ptr,
-                                        c->item_row, c->n_items, kItemEntries, c->sm_count, c->st);
-    } else {
-      c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
-                                   c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
-                                   kItemEntries, c->item_row, c->refine_kind == 3);
-    }
+    c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
+                                 c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
+                                 kItemEntries, c->item_row, c->refine_ff);
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
     c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, slab,
                                  c->c_g, c->st, v0, v1, nullptr, 0, 0, nullptr,
-                                 c->refine_kind == 3);
+                                 c->refine_ff);
   });
 }
 
-// (Re)allocate the entry-indexed arrays for capacity `cap`, preserving Omega.
 // Candidate-indexed arrays (C, sort keys, pool) at capacity `cap`; on an
 // allocation failure the ones allocated are released and the error rethrown.
 void alloc_entry_arrays(accord_ctx* c, int64_t cap) {
@@ -1239,9 +1224,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   {
     const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
     c->pair_ls = !(e && e[0] == '0');
-    const char* r = std::getenv("ACCORD_REFINE");     // A-B: block | flat | tma | ff | group
-    if (r) c->refine_kind = r[0] == 'b' ? 0 : r[0] == 'f' && r[1] == 'l' ? 1 : r[0] == 't' ? 2
-                                                          : r[0] == 'g' ? 4 : 3;
+    const char* r = std::getenv("ACCORD_REFINE");     // A-B: ff = float-float refine
+    c->refine_ff = r && r[0] == 'f' && r[1] == 'f';
   }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);

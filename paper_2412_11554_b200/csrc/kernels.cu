@@ -725,89 +725,6 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   }
 }
 
-// Refine over GROUPS of work items (float X, ldk <= 1024): in the steady state
-// an item (a row's candidates) holds ~13 entries at config 5, so a block per
-// item spends most of its life staging Y_i and synchronising; here a block of
-// 4 warps takes kRefGroup consecutive items, stages their Y rows in shared
-// memory in one go, and deals the group's candidates round-robin to its warps
-// (warp per candidate, float64 dot, fixed order per candidate).
-constexpr int kRefGroup = 8;
-
-__global__ void __launch_bounds__(128) refine_group_kernel(
-    int64_t n, int64_t ldk, const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_col,
-    const float* __restrict__ Y, const float* __restrict__ Xt, float* __restrict__ c_g,
-    const int64_t* __restrict__ itm_ptr, const int32_t* __restrict__ item_row, int64_t n_items,
-    int64_t L) {
-  extern __shared__ __align__(16) uint8_t ys_raw[];
-  float* ys = reinterpret_cast<float*>(ys_raw);                 // [kRefGroup][ldk]
-  __shared__ int64_t s_beg[kRefGroup], s_off[kRefGroup + 1];
-  __shared__ int32_t s_row[kRefGroup];
-  const int64_t it0 = (int64_t)blockIdx.x * kRefGroup;
-  const int ng = (int)min((int64_t)kRefGroup, n_items - it0);
-  if (threadIdx.x < kRefGroup) {
-    int64_t b = 0, e = 0;
-    int32_t r = 0;
-    if ((int)threadIdx.x < ng) {
-      const int64_t it = it0 + threadIdx.x;
-      r = item_row[it];
-      b = c_ptr[r] + (it - itm_ptr[r]) * L;
-      e = min(c_ptr[r + 1], b + L);
-    }
-    s_row[threadIdx.x] = r;
-    s_beg[threadIdx.x] = b;
-    s_off[threadIdx.x + 1] = e - b;                            // lengths, scanned below
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s_off[0] = 0;
-    for (int g = 0; g < kRefGroup; ++g) s_off[g + 1] += s_off[g];
-  }
-  // stage the group's Y rows (float4, all threads)
-  const int64_t l4 = ldk / 4;
-  for (int64_t q = threadIdx.x; q < (int64_t)ng * l4; q += blockDim.x) {
-    const int g = (int)(q / l4);
-    const int64_t m = (q - (int64_t)g * l4) * 4;
-    *reinterpret_cast<float4*>(ys + (int64_t)g * ldk + m) =
-        __ldg(reinterpret_cast<const float4*>(Y + (int64_t)s_row[g] * ldk + m));
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t total = s_off[kRefGroup];
-  const double inv_n = 1.0 / (double)n;
-  int g = 0;
-  for (int64_t f = wid; f < total; f += nw) {
-    while (f >= s_off[g + 1]) ++g;                             // item of flat candidate f
-    const int64_t e = s_beg[g] + (f - s_off[g]);
-    const float* xr = Xt + (int64_t)c_col[e] * ldk;
-    const float* yr = ys + (int64_t)g * ldk;
-    double acc = 0.0;
-    int64_t m = lane * 4;
-    for (; m + 7 * 128 < ldk; m += 8 * 128) {                  // 8 float4 in flight per lane
-      float4 x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(xr + m + u * 128));
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float4 y = *reinterpret_cast<const float4*>(yr + m + u * 128);
-        acc = fma((double)y.x, (double)x[u].x, acc);
-        acc = fma((double)y.y, (double)x[u].y, acc);
-        acc = fma((double)y.z, (double)x[u].z, acc);
-        acc = fma((double)y.w, (double)x[u].w, acc);
-      }
-    }
-    for (; m < ldk; m += 128) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(xr + m));
-      const float4 y = *reinterpret_cast<const float4*>(yr + m);
-      acc = fma((double)y.x, (double)x.x, acc);
-      acc = fma((double)y.y, (double)x.y, acc);
-      acc = fma((double)y.z, (double)x.z, acc);
-      acc = fma((double)y.w, (double)x.w, acc);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) c_g[e] = (float)(acc * inv_n);
-  }
-}
-
 // Values of Omega on a fixed structure (refit support): c_w[e] = omega_{i, c_col[e]}
 // or 0. Warp per row, binary search in Omega's sorted row.
 template <typename T>
@@ -1453,22 +1370,6 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                                                   (const float*)Y, (const float*)Xt,
                                                   (float*)c_g, v0, v1, itm_ptr, L, item_row,
                                                   y_global);
-  return 1;
-}
-
-int launch_refine_group(int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
-                        const float* Y, const float* Xt, float* c_g, const int64_t* itm_ptr,
-                        const int32_t* item_row, int64_t n_items, int64_t L, cudaStream_t st) {
-  if (n_items == 0) return 0;
-  const size_t smem = (size_t)kRefGroup * ldk * 4;
-  static unsigned long long attr_seen = 0;
-  if (attr_needed(attr_seen)) {
-    cudaFuncSetAttribute(refine_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)kRefGroup * 1024 * 4));
-    attr_done(attr_seen);
-  }
-  refine_group_kernel<<<(unsigned)((n_items + kRefGroup - 1) / kRefGroup), 128, smem, st>>>(
-      n, ldk, c_ptr, c_col, Y, Xt, c_g, itm_ptr, item_row, n_items, L);
   return 1;
 }
 

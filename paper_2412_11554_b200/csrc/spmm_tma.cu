@@ -400,230 +400,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
   }
 }
 
-// ---------------------------------------------------------------------------
-// a4' refine, TMA-staged: c_g[e] = (1/n) <Y_i, X^T_k> in
-// float64 for every candidate (i, k) of C. Like the SpMM it is a gather of
-// whole X^T rows of random columns, so the same structure applies: one
-// producer warp per block walks the block's work items and streams each
-// candidate's X^T row (in chunks of <= kRefChunk floats, so any n works)
-// into a shared-memory ring with cp.async.bulk; here every consumer warp owns
-// a private ring and whole candidates (the dot product ends in a warp
-// reduction, no block barrier), candidates dealt round-robin over the warps.
-// Y_i is read through L1 (the block's warps work on the same item, i.e. the
-// same row) and kept in registers as float64 while the row does not change.
-// ---------------------------------------------------------------------------
-constexpr int kRefWarps = 8;      // consumer warps per block
-constexpr int kRefStages = 3;     // ring stages per consumer warp
-constexpr int kRefChunk = 1024;   // floats per stage (4 KB)
-
-struct RefMeta {
-  int64_t e;                      // entry of C (-1: end of stream)
-  int32_t row, q, nq, pad;
-};
-
-__global__ void __launch_bounds__(32 + 32 * kRefWarps, 2)
-refine_tma_kernel(int64_t pk, int64_t n, int64_t ldk, const int64_t* __restrict__ c_ptr,
-                  const int32_t* __restrict__ c_col, const float* __restrict__ Y,
-                  const float* __restrict__ Xt, float* __restrict__ c_g,
-                  const int64_t* __restrict__ itm_ptr, const int32_t* __restrict__ item_row,
-                  int64_t n_items, int64_t L) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int64_t chunk = ldk < kRefChunk ? ldk : kRefChunk;
-  const int nq = (int)((ldk + chunk - 1) / chunk);
-  float* data = reinterpret_cast<float*>(sm);                           // [W][S][chunk]
-  RefMeta* meta = reinterpret_cast<RefMeta*>(sm + (size_t)kRefWarps * kRefStages * chunk * 4);
-  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kRefWarps * kRefStages);
-  uint64_t* empty = full + kRefWarps * kRefStages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kRefWarps * kRefStages; ++s) {
-      tc::mbar_init(tc::smem_u32(&full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&empty[s]), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ============================== producer ==============================
-    // candidate g goes to warp g % W; every candidate puts nq stages into its
-    // warp's ring, so the position in that ring follows from g and q alone
-    int64_t g = 0;
-    auto put = [&](int64_t gg, int64_t e, int32_t row, int q, int64_t k) {
-      const int w = (int)(gg % kRefWarps);
-      const int64_t pos = (gg / kRefWarps) * nq + q;
-      const int slot = w * kRefStages + (int)(pos % kRefStages);
-      const uint32_t ph = (uint32_t)((pos / kRefStages) & 1);
-      tc::mbar_wait(tc::smem_u32(&empty[slot]), ph ^ 1);
-      if (lane == 0) {
-        RefMeta& m = meta[slot];
-        m.e = e;
-        m.row = row;
-        m.q = q;
-        m.nq = nq;
-        const uint32_t fb = tc::smem_u32(&full[slot]);
-        if (e >= 0) {
-          const int64_t off = (int64_t)q * chunk;
-          const uint32_t bytes = (uint32_t)((ldk - off < chunk ? ldk - off : chunk) * 4);
-          tc::mbar_arrive_expect_tx(fb, bytes);
-          bulk_g2s(tc::smem_u32(data + (size_t)slot * chunk), Xt + k * ldk + off, bytes, fb);
-        } else {
-          tc::mbar_arrive(fb);
-        }
-      }
-      __syncwarp();
-    };
-    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int32_t r = item_row[it];
-      const int64_t beg = c_ptr[r] + (it - itm_ptr[r]) * L;
-      const int64_t end = min(c_ptr[r + 1], beg + L);
-      for (int64_t e0 = beg; e0 < end; e0 += 32) {
-        const int32_t kk = e0 + lane < end ? __ldg(c_col + e0 + lane) : 0;
-        const int cnt = (int)min((int64_t)32, end - e0);
-        for (int j = 0; j < cnt; ++j) {
-          const int64_t k = __shfl_sync(0xffffffffu, kk, j);
-          for (int q = 0; q < nq; ++q) put(g, e0 + j, r, q, k);
-          ++g;
-        }
-      }
-    }
-    for (int w = 0; w < kRefWarps; ++w, ++g) put(g, -1, 0, 0, 0);   // end marks, one per warp
-    return;
-  }
-  // ================================ consumers ===============================
-  const int w = warp - 1;
-  const double inv_n = 1.0 / (double)n;
-  constexpr int kV = kRefChunk / 128;      // float4 per lane per chunk (<= 8)
-  float4 yc[kV];                           // cached Y_i slice (single-chunk rows)
-  int32_t cached = -1;
-  double acc = 0.0;
-  int s = 0;
-  uint32_t phase = 0;
-  for (;;) {
-    const int slot = w * kRefStages + s;
-    tc::mbar_wait(tc::smem_u32(&full[slot]), phase);
-    const RefMeta m = meta[slot];
-    if (m.e < 0) break;
-    const int64_t off = (int64_t)m.q * chunk;
-    const int64_t len = ldk - off < chunk ? ldk - off : chunk;
-    const float* xs = data + (size_t)slot * chunk;
-    const float* yr = Y + (int64_t)m.row * ldk + off;
-    if (m.q == 0) acc = 0.0;
-    if (nq == 1) {
-      if (m.row != cached) {
-#pragma unroll
-        for (int u = 0; u < kV; ++u) {
-          const int64_t c = (int64_t)(lane + 32 * u) * 4;
-          yc[u] = c < len ? __ldg(reinterpret_cast<const float4*>(yr + c))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        cached = m.row;
-      }
-#pragma unroll
-      for (int u = 0; u < kV; ++u) {
-        const int64_t c = (int64_t)(lane + 32 * u) * 4;
-        if (c < len) {
-          const float4 x = *reinterpret_cast<const float4*>(xs + c);
-          acc = fma((double)yc[u].x, (double)x.x, acc);
-          acc = fma((double)yc[u].y, (double)x.y, acc);
-          acc = fma((double)yc[u].z, (double)x.z, acc);
-          acc = fma((double)yc[u].w, (double)x.w, acc);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < kV; ++u) {
-        const int64_t c = (int64_t)(lane + 32 * u) * 4;
-        if (c < len) {
-          const float4 x = *reinterpret_cast<const float4*>(xs + c);
-          const float4 y = __ldg(reinterpret_cast<const float4*>(yr + c));
-          acc = fma((double)y.x, (double)x.x, acc);
-          acc = fma((double)y.y, (double)x.y, acc);
-          acc = fma((double)y.z, (double)x.z, acc);
-          acc = fma((double)y.w, (double)x.w, acc);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[slot]));
-    if (++s == kRefStages) { s = 0; phase ^= 1; }
-    if (m.q == m.nq - 1) {
-      const double t = wsum(acc);
-      if (lane == 0) c_g[m.e] = (float)(t * inv_n);
-    }
-  }
-  (void)pk;
-}
-
 }  // namespace
-
-// Refine, flat variant (A-B against the TMA one): persistent warps, warp per
-// work item (the row's Y_i through L1), warp per candidate, the next
-// candidate's X^T row loaded while the current one is reduced (8 float4 per
-// lane in flight, two candidates deep).
-__global__ void __launch_bounds__(256) refine_flat_kernel(
-    int64_t n, int64_t ldk, const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_col,
-    const float* __restrict__ Y, const float* __restrict__ Xt, float* __restrict__ c_g,
-    const int64_t* __restrict__ itm_ptr, const int32_t* __restrict__ item_row, int64_t n_items,
-    int64_t L) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const double inv_n = 1.0 / (double)n;
-  constexpr int kU = 8;                       // float4 per lane per 4 KB piece
-  for (int64_t it = gw; it < n_items; it += nw) {
-    const int32_t r = item_row[it];
-    const int64_t beg = c_ptr[r] + (it - itm_ptr[r]) * L;
-    const int64_t end = min(c_ptr[r + 1], beg + L);
-    const float* yr = Y + (int64_t)r * ldk;
-    for (int64_t e0 = beg; e0 < end; e0 += 32) {
-      const int32_t kk = e0 + lane < end ? __ldg(c_col + e0 + lane) : 0;
-      const int cnt = (int)min((int64_t)32, end - e0);
-      for (int j = 0; j < cnt; ++j) {
-        const int64_t k = __shfl_sync(0xffffffffu, kk, j);
-        const float* xr = Xt + k * ldk;
-        double acc = 0.0;
-        for (int64_t m0 = 0; m0 < ldk; m0 += 32 * 4 * kU) {
-          float4 x[kU], y[kU];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int64_t c = m0 + (int64_t)(lane + 32 * u) * 4;
-            x[u] = c < ldk ? __ldg(reinterpret_cast<const float4*>(xr + c)) : make_float4(0, 0, 0, 0);
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int64_t c = m0 + (int64_t)(lane + 32 * u) * 4;
-            y[u] = c < ldk ? __ldg(reinterpret_cast<const float4*>(yr + c)) : make_float4(0, 0, 0, 0);
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            acc = fma((double)y[u].x, (double)x[u].x, acc);
-            acc = fma((double)y[u].y, (double)x[u].y, acc);
-            acc = fma((double)y[u].z, (double)x[u].z, acc);
-            acc = fma((double)y[u].w, (double)x[u].w, acc);
-          }
-        }
-        const double t = wsum(acc);
-        if (lane == 0) c_g[e0 + j] = (float)(t * inv_n);
-      }
-    }
-  }
-}
-
-int launch_refine_flat(int64_t n, int64_t ldk, const int64_t* c_ptr, const int32_t* c_col,
-                       const float* Y, const float* Xt, float* c_g, const int64_t* itm_ptr,
-                       const int32_t* item_row, int64_t n_items, int64_t L, int sm_count,
-                       cudaStream_t st) {
-  if (n_items == 0) return 0;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_flat_kernel, 256, 0) !=
-          cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  const int64_t grid = std::min<int64_t>((int64_t)sm_count * per_sm, (n_items + 7) / 8);
-  refine_flat_kernel<<<(unsigned)grid, 256, 0, st>>>(n, ldk, c_ptr, c_col, Y, Xt, c_g, itm_ptr,
-                                                     item_row, n_items, L);
-  return 1;
-}
 
 namespace {
 
@@ -663,34 +440,6 @@ size_t spmm_tma_smem(int64_t ldk, int* stages) {
   int s = (int)std::min<int64_t>(want, std::max<int64_t>(2, (want * 4096) / sb));
   *stages = s;
   return (size_t)s * sb + (size_t)s * sizeof(StageMeta) + 2 * s * 8 + 161 * 8 + 64;
-}
-
-size_t refine_tma_smem(int64_t ldk) {
-  const int64_t chunk = ldk < kRefChunk ? ldk : kRefChunk;
-  return (size_t)kRefWarps * kRefStages * (chunk * 4 + sizeof(RefMeta) + 16) + 64;
-}
-
-int launch_refine_tma(int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
-                      const int32_t* c_col, const float* Y, const float* Xt, float* c_g,
-                      const int64_t* itm_ptr, const int32_t* item_row, int64_t n_items, int64_t L,
-                      int sm_count, cudaStream_t st) {
-  if (n_items == 0) return 0;
-  const size_t smem = refine_tma_smem(ldk);
-  static unsigned long long attr_seen = 0;
-  if (attr_needed(attr_seen)) {
-    cudaFuncSetAttribute(refine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)refine_tma_smem(kRefChunk));
-    attr_done(attr_seen);
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_tma_kernel,
-                                                    32 + 32 * kRefWarps, smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  const int64_t grid = std::min<int64_t>((int64_t)sm_count * std::min(per_sm, 4), n_items);
-  refine_tma_kernel<<<(unsigned)grid, 32 + 32 * kRefWarps, smem, st>>>(
-      pk, n, ldk, c_ptr, c_col, Y, Xt, c_g, itm_ptr, item_row, n_items, L);
-  return 1;
 }
 
 bool spmm_tma_supported(int dtype, int64_t ldk) {

@@ -128,12 +128,12 @@ def test_lanczos_exactly_centered_and_zero_x():
     assert e.value.status == A.E_NUMERIC
 
 
-@pytest.mark.parametrize("refine", ["tma", "flat", "block"])
+@pytest.mark.parametrize("refine", ["block", "ff"])
 def test_filter_path_beyond_4096_samples(refine, monkeypatch):
-    """n = 5000 (ldk = 5056: the refine streams each X^T row in five chunks,
+    """n = 5000 (ldk = 5056; the refine reads each X^T row in 5 float4 passes,
     the last partial): AUTO is the certified bf16 filter for any n (round 1
-    fell back to BF16X3 above n = 4096); parity with the oracle, each refine
-    variant."""
+    fell back to BF16X3 above n = 4096); parity with the oracle, the float64
+    refine and its float-float A-B variant."""
     _cuda()
     monkeypatch.setenv("ACCORD_REFINE", refine)
     from accord_inputs import Config
