@@ -210,6 +210,7 @@ struct accord_ctx {
   int32_t* om_col = nullptr;
   void* om_val = nullptr;
   int64_t* c_ptr = nullptr;
+  int64_t* c_ptr2 = nullptr;               // C's row pointers after the support dedupe (swapped)
   int32_t* c_col = nullptr;
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
@@ -788,7 +789,7 @@ Footprint footprint(const accord_init_params* prm) {
     if (tc) a += 2 * R((size_t)rr * ldk * 2) * (x3 ? 2 : 1);
     a += 2 * R((size_t)pk_pad * ldk * 8);              // yacc, dacc
   }
-  a += 2 * R((pk + 1) * 8) + 2 * R(pk * 4) + R((pk + 1) * 4) + R(4);   // om/c ptr, counts
+  a += 3 * R((pk + 1) * 8) + 2 * R(pk * 4) + R((pk + 1) * 4) + R(4);   // om/c ptr, counts
   a += 9 * R(pk * 8) + 2 * R(pk * 4) + 4 * R(pk * 8) + R(4);          // per-row sums
   a += R(scan_tmp_bytes(pk + 1));
   a += 2 * R(pk * 4) + 2 * R((pk + 1) * 8) + R(pk * 4);               // work-item maps
@@ -1201,6 +1202,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   // ---- per-row and entry-indexed state ----
   c->om_ptr = c->dalloc<int64_t>(c->pk + 1);
   c->c_ptr = c->dalloc<int64_t>(c->pk + 1);
+  c->c_ptr2 = c->dalloc<int64_t>(c->pk + 1);
   c->row_cnt = c->dalloc<int32_t>(c->pk);
   c->rcur = c->dalloc<int32_t>(c->pk);
   c->long_rows = c->dalloc<int32_t>(c->pk + 1);
@@ -1430,21 +1432,26 @@ void mirror_exchange(accord_ctx* c, int64_t n_out) {
   csync(c, S);
 }
 
-// Append the received mirrored entries to the pool as chunks [used, used+needc).
-void mirror_append(accord_ctx* c, int64_t used, int64_t needc) {
+// Mark `count` entries written from chunk `used` on as pool chunks [used,
+// used + needc) (fill counts and the chunk counter the finalize reads).
+void pool_claim(accord_ctx* c, int64_t used, int64_t needc, int64_t count) {
   cudaStream_t S = c->st;
-  const int64_t R = c->mir_recv_n;
-  c->launches += launch_mirror_append(R, c->mir_recv, c->r0, c->pool_row, c->pool_col,
-                                      used * c->chunk, c->row_cnt, S);
   if (needc > 0) {
     std::vector<unsigned long long> fill(needc, (unsigned long long)c->chunk);
-    fill.back() = (unsigned long long)(R - (needc - 1) * c->chunk);
+    fill.back() = (unsigned long long)(count - (needc - 1) * c->chunk);
     CK(cudaMemcpyAsync(c->chunk_fill + used, fill.data(), needc * 8, cudaMemcpyHostToDevice, S));
     const unsigned int nx = (unsigned int)(used + needc);
     CK(cudaMemcpyAsync(c->chunk_next, &nx, 4, cudaMemcpyHostToDevice, S));
     csync(c, S);   // the host vectors go out of scope
   }
   c->h_seg[1] = used + needc;
+}
+
+// Append the received mirrored entries to the pool as chunks [used, used+needc).
+void mirror_append(accord_ctx* c, int64_t used, int64_t needc) {
+  c->launches += launch_mirror_append(c->mir_recv_n, c->mir_recv, c->r0, c->pool_row,
+                                      c->pool_col, used * c->chunk, c->row_cnt, c->st);
+  pool_claim(c, used, needc, c->mir_recv_n);
 }
 
 // Operands of a gradient pass other than the current iterate's (lambda_max:
@@ -1499,6 +1506,9 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     } else {
       CK(cudaMemsetAsync(c->chunk_next, 0, 4, S));
     }
+    // supp Omega joins C in the finalize (filter path); none for an override
+    // pass (lambda_max: empty support)
+    const int64_t n_sup = (c->gemm == ACCORD_GEMM_BF16_FILTER && !ov) ? c->nnz_local : 0;
     EpiParams ep{};
     ep.pk = c->pk;
     ep.p = c->p;
@@ -1592,18 +1602,29 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       if (!ovf) continue;
     }
     if (!ovf_any) {
-      if (!sym2) break;
-      if (!exchanged) {   // collective, once (a local redo regenerates the same entries)
+      // entries that join the pool after the GEMM: the mirrored positions
+      // received from other ranks (sym 2), and supp Omega with its diagonal
+      // (the filter's epilogue emits only its |acc| survivors)
+      if (sym2 && !exchanged) {   // collective, once (a local redo regenerates the same entries)
         mirror_exchange(c, (int64_t)h_mir);
         exchanged = true;
       }
-      const int64_t used = (int64_t)c->h_seg[1];
-      const int64_t needc = (c->mir_recv_n + c->chunk - 1) / c->chunk;
-      if (used + needc <= c->nchunks) {
-        mirror_append(c, used, needc);
+      int64_t used = (int64_t)c->h_seg[1];
+      const int64_t need_m = sym2 ? (c->mir_recv_n + c->chunk - 1) / c->chunk : 0;
+      const int64_t need_s = (n_sup + c->chunk - 1) / c->chunk;
+      if (used + need_m + need_s <= c->nchunks) {
+        if (sym2) {
+          mirror_append(c, used, need_m);
+          used += need_m;
+        }
+        if (n_sup) {
+          c->launches += launch_support_append(c->pk, omv.ptr, omv.col, c->pool_row, c->pool_col,
+                                               used * c->chunk, c->row_cnt, S);
+          pool_claim(c, used, need_s, n_sup);
+        }
         break;
       }
-      const int64_t want = (used + needc) * c->chunk;   // room for the received entries
+      const int64_t want = (used + need_m + need_s) * c->chunk;   // room for the appended entries
       grow(c, want + want / 4 + (1 << 20), c->nnz_local);
       continue;
     }
@@ -1628,6 +1649,13 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
   }
   c->launches += launch_finalize(c->dtype, c->pk, pv, c->c_ptr, c->rcur, c->keys,
                                  c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S);
+  if (filt && !ov) {
+    // the support entries the filter also emitted sit next to their twin after
+    // the row sort: keep one of each (C's new row pointers in c_ptr2, swapped in)
+    c->launches += launch_dedupe(c->pk, c->c_ptr, c->keys, c->row_cnt, c->c_ptr2, c->c_col,
+                                 c->scan_tmp, c->scan_tmp_sz, S);
+    std::swap(c->c_ptr, c->c_ptr2);
+  }
   c->items_of = nullptr;   // C changed
   if (filt) {
     const ProxItems* pit = nullptr;

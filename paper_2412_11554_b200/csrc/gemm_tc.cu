@@ -36,9 +36,13 @@
 //           atomicAdd per warp-chunk. The p x p gradient never reaches HBM;
 //           the epilogue of tile t overlaps the mainloop of tile t+1.
 //
-// Epilogue rule (derived from Eq. 3.5): emit
-// (i, k, g, omega_ik) iff k == i, or (i,k) in supp Omega (merge walk of the
-// thread's sorted CSR row), or the |G| > lambda test above passes.
+// Epilogue rule (derived from Eq. 3.5): C =
+// diag U supp Omega U {|G| > lambda}. BF16X3 emits (i, k, g, omega_ik) for all
+// three (merge walk of the thread's sorted CSR row); the filter emits only the
+// positions passing its |acc| test -- the diagonal and supp Omega are merged
+// in by the finalize (kernels.cu, support append + dedupe), which keeps the
+// support walk off the tensor-core epilogue (after iteration 1, ~240 support
+// entries per row at config 5).
 #include "accord_internal.h"
 #include "tc_ptx.cuh"
 
@@ -342,14 +346,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
         gi = ep.r0 + r;
         nxt = INT_MAX;
         if (row_ok) {
-          int64_t lo = om.ptr[r], hi = om.ptr[r + 1];
-          se = hi;
-          while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (om.col[mid] < n0) lo = mid + 1; else hi = mid;
+          if constexpr (kMode == 0) {
+            // BF16X3 emits values: walk Omega's sorted row for omega_ik (the
+            // filter emits positions only; diagonal and support join C in the
+            // finalize, so its epilogue tests |acc| alone)
+            int64_t lo = om.ptr[r], hi = om.ptr[r + 1];
+            se = hi;
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              if (om.col[mid] < n0) lo = mid + 1; else hi = mid;
+            }
+            sp = lo;
+            nxt = sp < se ? om.col[sp] : INT_MAX;
           }
-          sp = lo;
-          nxt = sp < se ? om.col[sp] : INT_MAX;
           if constexpr (kMode == 1) {
             // n*delta_ik = r1 * s_k + Bn * D_k, inflated by 1.0625 for the
             // float evaluation of the bound
@@ -449,7 +458,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             m0 = INFINITY;
           }
           const bool over = fmaxf(m0, m1) > tfast;
-          const bool hot = row_ok && (over || nxt < c0 + 32 || (gi >= c0 && gi < c0 + 32));
+          const bool hot =
+              row_ok && (over || (kMode == 0 && (nxt < c0 + 32 || (gi >= c0 && gi < c0 + 32))));
           if (!__any_sync(0xffffffffu, hot)) continue;
           uint32_t mask = 0, sup = 0;
           if (hot) {
@@ -473,8 +483,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                 }
               }
             }
-            if (gi >= c0 && gi < c0 + 32) mask |= 1u << (gi - c0);    // diagonal
-            while (nxt < c0 + 32) {                                   // support of Omega
+            if (kMode == 0 && gi >= c0 && gi < c0 + 32) mask |= 1u << (gi - c0);   // diagonal
+            while (kMode == 0 && nxt < c0 + 32) {                     // support of Omega
               sup |= 1u << (nxt - c0);
               ++sp;
               nxt = sp < se ? om.col[sp] : INT_MAX;

@@ -335,6 +335,58 @@ __global__ void gather_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
 }
 
 // ---------------------------------------------------------------------------
+// Filter path: supp Omega (diagonal included: Omega's rows always store it)
+// joins C in the finalize instead of the GEMM epilogue. The support entries
+// are appended to the pool, the row sort puts duplicates (entries the filter
+// also emitted) next to each other, and a count + write pass keeps one of
+// each (warp per row, order preserved).
+// ---------------------------------------------------------------------------
+__global__ void support_append_kernel(int64_t pk, const int64_t* __restrict__ om_ptr,
+                                      const int32_t* __restrict__ om_col,
+                                      int32_t* __restrict__ prow, int32_t* __restrict__ pcol,
+                                      int64_t start, int32_t* __restrict__ row_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const int64_t b = om_ptr[r], e = om_ptr[r + 1];
+  for (int64_t q = b + lane; q < e; q += 32) {
+    prow[start + q] = (int32_t)r;
+    pcol[start + q] = om_col[q];
+  }
+  if (lane == 0) row_cnt[r] += (int32_t)(e - b);
+}
+
+__global__ void dedupe_count_kernel(int64_t pk, const int64_t* __restrict__ ptr,
+                                    const uint64_t* __restrict__ keys, int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const int64_t b = ptr[r], e = ptr[r + 1];
+  int u = 0;
+  for (int64_t q = b + lane; q < e; q += 32)
+    u += (q == b || (keys[q] >> 32) != (keys[q - 1] >> 32)) ? 1 : 0;
+  u = warp_sum(u);
+  if (lane == 0) cnt[r] = u;
+}
+
+__global__ void dedupe_write_kernel(int64_t pk, const int64_t* __restrict__ ptr,
+                                    const uint64_t* __restrict__ keys,
+                                    const int64_t* __restrict__ optr, int32_t* __restrict__ col) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= pk) return;
+  const int64_t b = ptr[r], e = ptr[r + 1];
+  int64_t o = optr[r];
+  for (int64_t q0 = b; q0 < e; q0 += 32) {
+    const int64_t q = q0 + lane;
+    const bool u = q < e && (q == b || (keys[q] >> 32) != (keys[q - 1] >> 32));
+    const unsigned m = __ballot_sync(0xffffffffu, u);
+    if (u) col[o + __popc(m & ((1u << lane) - 1u))] = (int32_t)(keys[q] >> 32);
+    o += __popc(m);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // a5: prox at trial tau (Eq. 3.5), warp per row.
 // Forward step and prox are evaluated in double from the stored values; the
 // result is rounded to T. Diagonal root in the cancellation-free branch form.
@@ -1280,6 +1332,26 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
                                                   (const float*)pool.w, c_col, (float*)c_g,
                                                   (float*)c_w);
   return launches + 1;
+}
+
+int launch_support_append(int64_t pk, const int64_t* om_ptr, const int32_t* om_col,
+                          int32_t* prow, int32_t* pcol, int64_t start, int32_t* row_cnt,
+                          cudaStream_t st) {
+  if (pk == 0) return 0;
+  support_append_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, om_ptr, om_col, prow, pcol,
+                                                                  start, row_cnt);
+  return 1;
+}
+
+int launch_dedupe(int64_t pk, const int64_t* ptr, const uint64_t* keys, int32_t* cnt,
+                  int64_t* optr, int32_t* col, void* scan_tmp, size_t scan_tmp_bytes,
+                  cudaStream_t st) {
+  if (pk == 0) return 0;
+  const unsigned g = (unsigned)((pk + 7) / 8);
+  dedupe_count_kernel<<<g, 256, 0, st>>>(pk, ptr, keys, cnt);
+  int l = 1 + launch_scan_i32(cnt, optr, pk, scan_tmp, scan_tmp_bytes, st);
+  dedupe_write_kernel<<<g, 256, 0, st>>>(pk, ptr, keys, optr, col);
+  return l + 1;
 }
 
 int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_t* c_col,
