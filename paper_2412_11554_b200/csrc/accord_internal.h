@@ -147,14 +147,15 @@ size_t scan_tmp_bytes(int64_t N);
 // Finalize the candidate pool into the sorted per-row candidate set C.
 int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* c_ptr,
                     int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col,
-                    void* c_g, void* c_w, int32_t* long_rows, cudaStream_t st);
+                    void* c_g, void* c_w, int32_t* long_rows, cudaStream_t st,
+                    const int64_t* sup_ptr = nullptr, const int32_t* sup_col = nullptr);
 
-// Filter path: append supp Omega (its CSR, diagonal included) to the pool at
-// `start` (row_cnt += row lengths); after the row sort, keep one entry per
-// column (cnt: per-row unique counts, optr: their scan, col: the columns).
-int launch_support_append(int64_t pk, const int64_t* om_ptr, const int32_t* om_col,
-                          int32_t* prow, int32_t* pcol, int64_t start, int32_t* row_cnt,
-                          cudaStream_t st);
+// Filter path: supp Omega (its CSR, diagonal included) joins C in the
+// finalize: row_cnt += its row lengths before the scan, launch_finalize
+// scatters it next to the GEMM's entries (sup_ptr / sup_col), and after the
+// row sort one entry per column is kept (cnt: per-row unique counts, optr:
+// their scan, col: the columns).
+int launch_support_count(int64_t pk, const int64_t* om_ptr, int32_t* row_cnt, cudaStream_t st);
 int launch_dedupe(int64_t pk, const int64_t* ptr, const uint64_t* keys, int32_t* cnt,
                   int64_t* optr, int32_t* col, void* scan_tmp, size_t scan_tmp_bytes,
                   cudaStream_t st);

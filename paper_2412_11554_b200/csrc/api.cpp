@@ -1602,31 +1602,34 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       if (!ovf) continue;
     }
     if (!ovf_any) {
-      // entries that join the pool after the GEMM: the mirrored positions
-      // received from other ranks (sym 2), and supp Omega with its diagonal
-      // (the filter's epilogue emits only its |acc| survivors)
+      // the mirrored positions received from other ranks (sym 2) join the pool
       if (sym2 && !exchanged) {   // collective, once (a local redo regenerates the same entries)
         mirror_exchange(c, (int64_t)h_mir);
         exchanged = true;
       }
-      int64_t used = (int64_t)c->h_seg[1];
+      const int64_t used = (int64_t)c->h_seg[1];
       const int64_t need_m = sym2 ? (c->mir_recv_n + c->chunk - 1) / c->chunk : 0;
-      const int64_t need_s = (n_sup + c->chunk - 1) / c->chunk;
-      if (used + need_m + need_s <= c->nchunks) {
-        if (sym2) {
-          mirror_append(c, used, need_m);
-          used += need_m;
-        }
-        if (n_sup) {
-          c->launches += launch_support_append(c->pk, omv.ptr, omv.col, c->pool_row, c->pool_col,
-                                               used * c->chunk, c->row_cnt, S);
-          pool_claim(c, used, need_s, n_sup);
-        }
-        break;
+      if (used + need_m > c->nchunks) {
+        const int64_t want = (used + need_m) * c->chunk;   // room for the received entries
+        grow(c, want + want / 4 + (1 << 20), c->nnz_local);
+        continue;
       }
-      const int64_t want = (used + need_m + need_s) * c->chunk;   // room for the appended entries
-      grow(c, want + want / 4 + (1 << 20), c->nnz_local);
-      continue;
+      if (sym2) mirror_append(c, used, need_m);
+      // supp Omega with its diagonal joins C in the finalize (the filter's
+      // epilogue emits only its |acc| survivors): the key arrays must hold
+      // both before the dedupe
+      if (n_sup) c->launches += launch_support_count(c->pk, omv.ptr, c->row_cnt, S);
+      c->launches += launch_scan_i32(c->row_cnt, c->c_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
+      if (n_sup) {
+        int64_t tot = 0;
+        CK(cudaMemcpyAsync(&tot, c->c_ptr + c->pk, 8, cudaMemcpyDeviceToHost, S));
+        csync(c, S);
+        if (tot > c->cap) {
+          grow(c, tot + tot / 4 + (1 << 20), c->nnz_local);
+          continue;
+        }
+      }
+      break;
     }
     if (!ovf) continue;
     const int64_t want = need + need / 4 + (1 << 20);
@@ -1634,10 +1637,8 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       throw Fail{ACCORD_E_NOMEM, "candidate pool exceeds 2^32 entries"};
     grow(c, want, c->nnz_local);
   }
-  // ---------------- a4: finalize C ----------------
-  TR(c, "host_gap");
-  c->launches += launch_scan_i32(c->row_cnt, c->c_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
-  TR(c, "scan");
+  // ---------------- a4: finalize C (row counts scanned into c_ptr above) ----
+  TR(c, "host_gap+scan");
   CK(cudaMemsetAsync(c->rcur, 0, c->pk * 4, S));
   CK(cudaMemsetAsync(c->long_rows, 0, 4, S));
   TR(c, "memset");
@@ -1648,7 +1649,9 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     pv.w = nullptr;    // omega_ik from a lookup in Omega's sorted rows
   }
   c->launches += launch_finalize(c->dtype, c->pk, pv, c->c_ptr, c->rcur, c->keys,
-                                 c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S);
+                                 c->keys_tmp, c->c_col, c->c_g, c->c_w, c->long_rows, S,
+                                 filt && !ov ? c->om_ptr : nullptr,
+                                 filt && !ov ? c->om_col : nullptr);
   if (filt && !ov) {
     // the support entries the filter also emitted sit next to their twin after
     // the row sort: keep one of each (C's new row pointers in c_ptr2, swapped in)

@@ -336,24 +336,33 @@ __global__ void gather_kernel(int64_t pk, const int64_t* __restrict__ c_ptr,
 
 // ---------------------------------------------------------------------------
 // Filter path: supp Omega (diagonal included: Omega's rows always store it)
-// joins C in the finalize instead of the GEMM epilogue. The support entries
-// are appended to the pool, the row sort puts duplicates (entries the filter
-// also emitted) next to each other, and a count + write pass keeps one of
+// joins C in the finalize instead of the GEMM epilogue: its row lengths are
+// added to the candidate counts, its entries scattered into the rows' key
+// segments next to the GEMM's, the row sort puts duplicates (entries the
+// filter also emitted) side by side, and a count + write pass keeps one of
 // each (warp per row, order preserved).
 // ---------------------------------------------------------------------------
-__global__ void support_append_kernel(int64_t pk, const int64_t* __restrict__ om_ptr,
-                                      const int32_t* __restrict__ om_col,
-                                      int32_t* __restrict__ prow, int32_t* __restrict__ pcol,
-                                      int64_t start, int32_t* __restrict__ row_cnt) {
+__global__ void support_count_kernel(int64_t pk, const int64_t* __restrict__ om_ptr,
+                                     int32_t* __restrict__ row_cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < pk;
+       r += (int64_t)gridDim.x * blockDim.x)
+    row_cnt[r] += (int32_t)(om_ptr[r + 1] - om_ptr[r]);
+}
+
+__global__ void support_scatter_kernel(int64_t pk, const int64_t* __restrict__ om_ptr,
+                                       const int32_t* __restrict__ om_col,
+                                       const int64_t* __restrict__ c_ptr, int32_t* rcur,
+                                       uint64_t* __restrict__ keys) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= pk) return;
   const int64_t b = om_ptr[r], e = om_ptr[r + 1];
-  for (int64_t q = b + lane; q < e; q += 32) {
-    prow[start + q] = (int32_t)r;
-    pcol[start + q] = om_col[q];
-  }
-  if (lane == 0) row_cnt[r] += (int32_t)(e - b);
+  if (b == e) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(&rcur[r], (int)(e - b));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int64_t q = b + lane; q < e; q += 32)
+    keys[c_ptr[r] + base + (q - b)] = ((uint64_t)(uint32_t)om_col[q] << 32) | 0xffffffffull;
 }
 
 __global__ void dedupe_count_kernel(int64_t pk, const int64_t* __restrict__ ptr,
@@ -1312,7 +1321,8 @@ int launch_rowsort(int64_t rows, const int64_t* ptr, uint64_t* keys, uint64_t* t
 
 int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* c_ptr,
                     int32_t* rcur, uint64_t* keys, uint64_t* keys_tmp, int32_t* c_col, void* c_g,
-                    void* c_w, int32_t* long_rows, cudaStream_t st) {
+                    void* c_w, int32_t* long_rows, cudaStream_t st, const int64_t* sup_ptr,
+                    const int32_t* sup_col) {
   int launches = 0;
   {
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(pool.chunk / 256, 148 * 8));
@@ -1322,6 +1332,11 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
                                                  keys);
   }
   ++launches;
+  if (sup_ptr) {   // supp Omega into the same row segments (filter path)
+    support_scatter_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, sup_ptr, sup_col, c_ptr,
+                                                                     rcur, keys);
+    ++launches;
+  }
   launches += launch_rowsort(pk, c_ptr, keys, keys_tmp, long_rows, st);
   if (dtype == ACCORD_F64)
     gather_kernel<double><<<148 * 8, 256, 0, st>>>(pk, c_ptr, keys, (const double*)pool.g,
@@ -1334,12 +1349,9 @@ int launch_finalize(int dtype, int64_t pk, const PoolView& pool, const int64_t* 
   return launches + 1;
 }
 
-int launch_support_append(int64_t pk, const int64_t* om_ptr, const int32_t* om_col,
-                          int32_t* prow, int32_t* pcol, int64_t start, int32_t* row_cnt,
-                          cudaStream_t st) {
+int launch_support_count(int64_t pk, const int64_t* om_ptr, int32_t* row_cnt, cudaStream_t st) {
   if (pk == 0) return 0;
-  support_append_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, om_ptr, om_col, prow, pcol,
-                                                                  start, row_cnt);
+  support_count_kernel<<<grid_for(pk, 256), 256, 0, st>>>(pk, om_ptr, row_cnt);
   return 1;
 }
 
