@@ -2,7 +2,9 @@
 BASELINE config, printed as one JSON document.
 
   configs 1-2: full oracle (Algorithm 1 in float64), T from BASELINE.json
-  configs 3-5: sampled-row replay with the GPU's step schedule
+  config 3:    full oracle too, from tests/golden/c3_full_oracle.json (the
+               oracle's free-running 100 iterations, tools/golden_c3.py)
+  configs 3-6: sampled-row replay with the GPU's step schedule
 
 Run on the GPU box: python tools/parity_report.py > profiles/<round>/parity_report.json
 """
@@ -71,12 +73,50 @@ def sampled(key):
                 n_cand=int(st[-1]["n_cand"]))
 
 
+def golden_c3():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "c3_full_oracle.json")))
+    cfg = get_config(3)
+    pr = make_problem(cfg)
+    X = torch.from_numpy(pr.Xt).cuda()
+    with A.AccordSolver(X, g["lambda"], tau0=g["tau0"], beta=g["beta"],
+                        inv_L=float.fromhex(g["inv_L_hex"])) as s:
+        st = s.step(g["T"])
+        csr = s.export_csr()
+    taus = [x["tau"] for x in st]
+    f_g = np.array([x["f"] for x in st])
+    f_o = np.array(g["f"][1:])
+    worst, mism, exempt = 0.0, 0, 0
+    for i_s, r in g["rows"].items():
+        i = int(i_s)
+        oc = np.array(r["cols"], dtype=np.int64)
+        ov = np.array([float.fromhex(v) for v in r["vals"]])
+        gc = csr.col[csr.row_ptr[i]:csr.row_ptr[i + 1]].astype(np.int64)
+        gv = csr.val[csr.row_ptr[i]:csr.row_ptr[i + 1]].astype(np.float64)
+        d = set(oc.tolist()) ^ set(gc.tolist())
+        mism += len(d)
+        exempt += len(d & set(r["exempt"]))
+        allc = np.union1d(oc, gc)
+        a = np.zeros(len(allc))
+        b = np.zeros(len(allc))
+        a[np.searchsorted(allc, gc)] = gv
+        b[np.searchsorted(allc, oc)] = ov
+        worst = max(worst, float(np.abs(a - b).max()))
+    return dict(config=cfg.name, lam=g["lambda"], T=g["T"],
+                mode=f"full oracle (golden, {len(g['rows'])} stored rows)",
+                taus_equal=taus == g["taus"],
+                trials_equal=[x["trials"] for x in st] == g["trials"],
+                max_f_rel=float(np.max(np.abs(f_g - f_o) / np.abs(f_o))),
+                rel_err=worst / g["max_abs_omega"], support_mismatch=mism,
+                support_exempt=exempt, nnz_gpu=int(csr.row_ptr[-1]), nnz_oracle=g["nnz"][-1])
+
+
 if __name__ == "__main__":
     out = []
     for lam in get_config(1).lambdas:
         out.append(full(1, lam))
     for lam in get_config(2).lambdas:
         out.append(full(2, lam))
+    out.append(golden_c3())
     for key in (3, 4, 5, 6):
         out.append(sampled(key))
     print(json.dumps(out, indent=1))
