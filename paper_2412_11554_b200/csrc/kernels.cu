@@ -688,7 +688,38 @@ __device__ __forceinline__ void ff_madd(float& hi, float& lo, float x, float y) 
   hi = t;
 }
 
-template <typename T, bool kFF = false>
+// float -> double on the integer pipe (exponent rebias + mantissa shift),
+// exact for every finite float; denormals (never seen in practice) take the
+// F2F path. Moves one of the refine's two conversions per product off the XU
+// pipe (kArith 2).
+__device__ __forceinline__ bool f32_denormal(float f) {
+  return (__float_as_uint(f) & 0x7fffffffu) - 1u < 0x007fffffu;
+}
+__device__ __forceinline__ double f2d_alu(float f) {   // finite, not denormal
+  const uint32_t b = __float_as_uint(f);
+  const uint32_t mag = b & 0x7fffffffu;
+  const uint32_t hi = (b & 0x80000000u) | (mag ? (mag >> 3) + (896u << 20) : 0u);
+  return __hiloint2double((int)hi, (int)(b << 29));
+}
+// the 4 products of a float4 pair into s; Y on the integer pipe unless a lane
+// holds a denormal (warp-uniform branch, so the common path has no F2F for Y)
+__device__ __forceinline__ double dot4_alu(float4 y, float4 x, double s) {
+  const bool dn = f32_denormal(y.x) | f32_denormal(y.y) | f32_denormal(y.z) | f32_denormal(y.w);
+  if (__builtin_expect(__any_sync(0xffffffffu, dn), 0)) {
+    s = fma((double)y.x, (double)x.x, s);
+    s = fma((double)y.y, (double)x.y, s);
+    s = fma((double)y.z, (double)x.z, s);
+    return fma((double)y.w, (double)x.w, s);
+  }
+  s = fma(f2d_alu(y.x), (double)x.x, s);
+  s = fma(f2d_alu(y.y), (double)x.y, s);
+  s = fma(f2d_alu(y.z), (double)x.z, s);
+  return fma(f2d_alu(y.w), (double)x.w, s);
+}
+
+// kArith: 0 = float64 products (both operands converted by F2F), 1 =
+// float-float (kFF), 2 = float64 with Y_i converted on the integer pipe
+template <typename T, int kArith = 0>
 __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
                                                      const int64_t* __restrict__ c_ptr,
                                                      const int32_t* __restrict__ c_col,
@@ -733,7 +764,7 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   constexpr int kStep = 32 * V;           // elements per lane-pass over the row
   for (int64_t e = beg + wid; e < end; e += nw) {
     const T* xr = Xt + (int64_t)(c_col[e] - v0) * ldk;
-    if constexpr (kFF) {
+    if constexpr (kArith == 1) {
       // two (hi, lo) accumulators: shorter dependent chains
       float h0 = 0.f, l0 = 0.f, h1 = 0.f, l1 = 0.f;
       int64_t m = lane * V;
@@ -771,15 +802,23 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const VT yv = *reinterpret_cast<const VT*>(ys + m + u * kStep);
+        if constexpr (kArith == 2) {
+          s = dot4_alu(yv, x[u], s);
+        } else {
 #pragma unroll
-        for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
+          for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
+        }
       }
     }
     for (; m < ldk; m += kStep) {
       const VT x = __ldg(reinterpret_cast<const VT*>(xr + m));
       const VT yv = *reinterpret_cast<const VT*>(ys + m);
+      if constexpr (kArith == 2) {
+        s = dot4_alu(yv, x, s);
+      } else {
 #pragma unroll
-      for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
+        for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
+      }
     }
     s = warp_sum(s);
     if (lane == 0) c_g[e] = (T)(s * inv_n);
@@ -1416,7 +1455,7 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
                   cudaStream_t st, int64_t v0, int64_t v1, const int64_t* itm_ptr,
-                  int64_t n_items, int64_t L, const int32_t* item_row, bool ff) {
+                  int64_t n_items, int64_t L, const int32_t* item_row, int ff) {
   const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
   size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
@@ -1435,7 +1474,9 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                          200 * 1024);
     cudaFuncSetAttribute(refine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    cudaFuncSetAttribute(refine_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(refine_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(refine_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_done(attr_seen);
   }
@@ -1444,8 +1485,13 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                                                    (const double*)Y, (const double*)Xt,
                                                    (double*)c_g, v0, v1, itm_ptr, L, item_row,
                                                    y_global);
+  else if (ff == 2)
+    refine_kernel<float, 2><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                     (const float*)Y, (const float*)Xt,
+                                                     (float*)c_g, v0, v1, itm_ptr, L, item_row,
+                                                     y_global);
   else if (ff)
-    refine_kernel<float, true><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+    refine_kernel<float, 1><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                         (const float*)Y, (const float*)Xt,
                                                         (float*)c_g, v0, v1, itm_ptr, L, item_row,
                                                         y_global);
