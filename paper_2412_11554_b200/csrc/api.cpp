@@ -1085,8 +1085,10 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   const int64_t ldx = prm->ldx ? prm->ldx : cols_src;
   const void* Xsrc = prm->X;
   void* staging = nullptr;
+  phase("X^T alloc");
   if (!prm->x_on_device) {
     staging = c->dalloc_bytes((size_t)rows_src * cols_src * T);
+    phase("staging alloc");
     if (ldx == cols_src)   // dense: one linear copy (a 2-D copy of 4 KB rows is ~8x slower)
       CK(cudaMemcpyAsync(staging, prm->X, (size_t)rows_src * cols_src * T,
                          cudaMemcpyHostToDevice, c->st));
@@ -1094,6 +1096,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
       CK(cudaMemcpy2DAsync(staging, cols_src * T, prm->X, ldx * T, cols_src * T, rows_src,
                            cudaMemcpyHostToDevice, c->st));
     Xsrc = staging;
+    phase("H2D copy");
   }
   unsigned long long* badidx = c->dalloc<unsigned long long>(1);
   CK(cudaMemsetAsync(badidx, 0xff, 8, c->st));
