@@ -688,37 +688,8 @@ __device__ __forceinline__ void ff_madd(float& hi, float& lo, float x, float y) 
   hi = t;
 }
 
-// float -> double on the integer pipe (exponent rebias + mantissa shift),
-// exact for every finite float; denormals (never seen in practice) take the
-// F2F path. Moves one of the refine's two conversions per product off the XU
-// pipe (kArith 2).
-__device__ __forceinline__ bool f32_denormal(float f) {
-  return (__float_as_uint(f) & 0x7fffffffu) - 1u < 0x007fffffu;
-}
-__device__ __forceinline__ double f2d_alu(float f) {   // finite, not denormal
-  const uint32_t b = __float_as_uint(f);
-  const uint32_t mag = b & 0x7fffffffu;
-  const uint32_t hi = (b & 0x80000000u) | (mag ? (mag >> 3) + (896u << 20) : 0u);
-  return __hiloint2double((int)hi, (int)(b << 29));
-}
-// the 4 products of a float4 pair into s; Y on the integer pipe unless a lane
-// holds a denormal (warp-uniform branch, so the common path has no F2F for Y)
-__device__ __forceinline__ double dot4_alu(float4 y, float4 x, double s) {
-  const bool dn = f32_denormal(y.x) | f32_denormal(y.y) | f32_denormal(y.z) | f32_denormal(y.w);
-  if (__builtin_expect(__any_sync(0xffffffffu, dn), 0)) {
-    s = fma((double)y.x, (double)x.x, s);
-    s = fma((double)y.y, (double)x.y, s);
-    s = fma((double)y.z, (double)x.z, s);
-    return fma((double)y.w, (double)x.w, s);
-  }
-  s = fma(f2d_alu(y.x), (double)x.x, s);
-  s = fma(f2d_alu(y.y), (double)x.y, s);
-  s = fma(f2d_alu(y.z), (double)x.z, s);
-  return fma(f2d_alu(y.w), (double)x.w, s);
-}
-
 // kArith: 0 = float64 products (both operands converted by F2F), 1 =
-// float-float (kFF), 2 = float64 with Y_i converted on the integer pipe
+// float-float (A-B variant, slower; ACCORD_REFINE=ff)
 template <typename T, int kArith = 0>
 __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
                                                      const int64_t* __restrict__ c_ptr,
@@ -802,23 +773,15 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const VT yv = *reinterpret_cast<const VT*>(ys + m + u * kStep);
-        if constexpr (kArith == 2) {
-          s = dot4_alu(yv, x[u], s);
-        } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
-        }
+        for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
       }
     }
     for (; m < ldk; m += kStep) {
       const VT x = __ldg(reinterpret_cast<const VT*>(xr + m));
       const VT yv = *reinterpret_cast<const VT*>(ys + m);
-      if constexpr (kArith == 2) {
-        s = dot4_alu(yv, x, s);
-      } else {
 #pragma unroll
-        for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
-      }
+      for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
     }
     s = warp_sum(s);
     if (lane == 0) c_g[e] = (T)(s * inv_n);
@@ -1476,8 +1439,6 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                          200 * 1024);
     cudaFuncSetAttribute(refine_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    cudaFuncSetAttribute(refine_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
     attr_done(attr_seen);
   }
   if (dtype == ACCORD_F64)
@@ -1485,11 +1446,6 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                                                    (const double*)Y, (const double*)Xt,
                                                    (double*)c_g, v0, v1, itm_ptr, L, item_row,
                                                    y_global);
-  else if (ff == 2)
-    refine_kernel<float, 2><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
-                                                     (const float*)Y, (const float*)Xt,
-                                                     (float*)c_g, v0, v1, itm_ptr, L, item_row,
-                                                     y_global);
   else if (ff)
     refine_kernel<float, 1><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                         (const float*)Y, (const float*)Xt,
