@@ -292,6 +292,10 @@ int launch_mirror_scatter(int64_t n, const int32_t* row, const int32_t* col, con
 int launch_mirror_append(int64_t n, const int32_t* in, int64_t r0, int32_t* prow, int32_t* pcol,
                          int64_t start, int32_t* row_cnt, cudaStream_t st);
 
+// Diagnostic: one thread spinning `ms` milliseconds on the stream (the
+// NCCL watchdog test's stand-in for a slow or dead peer).
+int launch_spin(int ms, cudaStream_t st);
+
 // Per-column constants of the filter bound from Xt (f32).
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st);
 

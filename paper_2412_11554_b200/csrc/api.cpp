@@ -312,12 +312,9 @@ namespace {
 // failure the communicators are aborted (they cannot be reused) and the call
 // returns ACCORD_E_NCCL.
 double nccl_timeout_s() {
-  static const double t = [] {
-    const char* e = std::getenv("ACCORD_NCCL_TIMEOUT_S");
-    const double v = e ? std::atof(e) : 0.0;
-    return v > 0 ? v : 1800.0;
-  }();
-  return t;
+  const char* e = std::getenv("ACCORD_NCCL_TIMEOUT_S");
+  const double v = e ? std::atof(e) : 0.0;
+  return v > 0 ? v : 1800.0;
 }
 
 void nccl_abort(accord_ctx* c) {
@@ -336,12 +333,14 @@ void csync(accord_ctx* c, cudaStream_t s) {
   }
   NcclApi* api = nccl_api();
   const auto t0 = std::chrono::steady_clock::now();
+  const double limit = nccl_timeout_s();
   for (int spin = 0;; ++spin) {
     const cudaError_t q = cudaStreamQuery(s);
     if (q == cudaSuccess) return;
     if (q != cudaErrorNotReady) CK(q);
-    if (api->CommGetAsyncError && (spin & 63) == 0) {
+    if ((spin & 63) == 0) {
       for (ncclComm_t cm : {c->nccl, c->nccl_ring}) {
+        if (!api->CommGetAsyncError) break;
         if (!cm) continue;
         ncclResult_t r = ncclSuccess;
         api->CommGetAsyncError(cm, &r);
@@ -353,7 +352,7 @@ void csync(accord_ctx* c, cudaStream_t s) {
       }
       const double el =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      if (el > nccl_timeout_s()) {
+      if (el > limit) {
         nccl_abort(c);
         throw Fail{ACCORD_E_NCCL, "NCCL watchdog: stream not done after " +
                                       std::to_string((int)el) +
@@ -366,6 +365,8 @@ void csync(accord_ctx* c, cudaStream_t s) {
 
 void allreduce(accord_ctx* c, double* d_buf, double* h_buf, int count) {
   // d_buf (device) -> h_buf (host), summed over ranks. Synchronizes the stream.
+  if (const char* h = std::getenv("ACCORD_DEBUG_STALL_MS"))   // test of the watchdog only:
+    c->launches += launch_spin(std::atoi(h), c->st);           // a slow "peer" on the stream
   if (c->comm == ACCORD_COMM_NCCL) {   // (a 1-rank communicator is exercised by the tests)
     NK(nccl_api()->AllReduce(d_buf, d_buf, count, ncclDouble, ncclSum, c->nccl, c->st));
   }

@@ -1558,6 +1558,22 @@ int launch_mirror_append(int64_t n, const int32_t* in, int64_t r0, int32_t* prow
   return 1;
 }
 
+__global__ void spin_kernel(long long ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if ((long long)(t - t0) >= ns) break;
+  }
+}
+
+int launch_spin(int ms, cudaStream_t st) {
+  if (ms <= 0) return 0;
+  spin_kernel<<<1, 1, 0, st>>>((long long)ms * 1000000ll);
+  return 1;
+}
+
 int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st) {
   col_norms_kernel<<<(unsigned)((p + 7) / 8), 256, 0, st>>>(p, ldk, Xt, col_sd);
   return 1;

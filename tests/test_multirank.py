@@ -557,3 +557,31 @@ def test_nccl_code_path_with_one_rank():
     assert a == b and ka == kb
     assert np.array_equal(ca.row_ptr, cb.row_ptr) and np.array_equal(ca.col, cb.col)
     assert np.array_equal(ca.val, cb.val)
+
+
+@pytest.mark.gpu
+def test_nccl_watchdog_gives_up_on_a_stalled_stream(monkeypatch):
+    """Every host wait on a stream with NCCL work is a watchdog: with the
+    stream held for 4 s (ACCORD_DEBUG_STALL_MS, a stand-in for a dead peer
+    that never joins the allreduce) and ACCORD_NCCL_TIMEOUT_S = 1, the step
+    returns ACCORD_E_NCCL after ~1 s instead of waiting, and the context can
+    still be destroyed."""
+    import time
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA not available on a -m gpu run")
+    from accord_inputs import make_problem
+    pr = make_problem("t_ba_f32")
+    X = torch.from_numpy(pr.Xt).cuda()
+    s = A.AccordSolver(X, 0.1, inv_L=0.01, comm=A.COMM_NCCL, nccl_id=A.nccl_unique_id())
+    s.step(1)
+    monkeypatch.setenv("ACCORD_DEBUG_STALL_MS", "4000")
+    monkeypatch.setenv("ACCORD_NCCL_TIMEOUT_S", "1")
+    t0 = time.perf_counter()
+    with pytest.raises(A.AccordError) as e:
+        s.step(1)
+    el = time.perf_counter() - t0
+    assert e.value.status == A.E_NCCL and "watchdog" in str(e.value)
+    assert el < 3.5, el
+    torch.cuda.synchronize()
+    s.close()
