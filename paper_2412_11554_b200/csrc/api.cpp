@@ -1624,7 +1624,9 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       // both before the dedupe
       if (n_sup) c->launches += launch_support_count(c->pk, omv.ptr, c->row_cnt, S);
       c->launches += launch_scan_i32(c->row_cnt, c->c_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
-      if (n_sup) {
+      // the pool's chunks bound the GEMM's entries: read the exact total
+      // (one more host sync) only when that bound does not already fit
+      if (n_sup && (int64_t)c->h_seg[1] * c->chunk + n_sup > c->cap) {
         int64_t tot = 0;
         CK(cudaMemcpyAsync(&tot, c->c_ptr + c->pk, 8, cudaMemcpyDeviceToHost, S));
         csync(c, S);
