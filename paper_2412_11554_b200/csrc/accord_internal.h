@@ -259,7 +259,7 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
                   cudaStream_t st, int64_t v0 = 0, int64_t v1 = INT64_MAX,
                   const int64_t* itm_ptr = nullptr, int64_t n_items = 0, int64_t L = 0,
-                  const int32_t* item_row = nullptr, int arith = 0);   // 1 float-float, 2 Y in regs
+                  const int32_t* item_row = nullptr, int arith = 0);   // 1: float-float
 
 
 

@@ -215,7 +215,7 @@ struct accord_ctx {
   void *c_g = nullptr, *c_w = nullptr, *c_wn = nullptr;
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
-  int refine_ff = 0;                       // refine arithmetic (ACCORD_REFINE: ff = float-float, yreg)
+  int refine_ff = 0;                       // 1: float-float refine (ACCORD_REFINE=ff; A-B, slower)
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
@@ -1231,7 +1231,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     const char* e = std::getenv("ACCORD_LS_PAIRS");   // A-B switch
     c->pair_ls = !(e && e[0] == '0');
     const char* r = std::getenv("ACCORD_REFINE");     // A-B: ff = float-float refine
-    c->refine_ff = (r && r[0] == 'f' && r[1] == 'f') ? 1 : (r && r[0] == 'y') ? 2 : 0;
+    c->refine_ff = (r && r[0] == 'f' && r[1] == 'f') ? 1 : 0;
   }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);

@@ -689,10 +689,7 @@ __device__ __forceinline__ void ff_madd(float& hi, float& lo, float x, float y) 
 }
 
 // kArith: 0 = float64 products (both operands converted by F2F), 1 =
-// float-float (A-B variant, slower; ACCORD_REFINE=ff), 2 = Y_i converted to
-// float64 once per warp and kept in registers (float, ldk == 1024: one F2F per
-// product instead of two; the F2F.F64.F32 on the XU pipe bounds the refine
-// when X^T is L2-resident, config 3)
+// float-float (A-B variant, slower; ACCORD_REFINE=ff)
 template <typename T, int kArith = 0>
 __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
                                                      const int64_t* __restrict__ c_ptr,
@@ -736,29 +733,6 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double inv_n = 1.0 / (double)n;
   constexpr int kStep = 32 * V;           // elements per lane-pass over the row
-  if constexpr (kArith == 2) {
-    double yd[32];                      // lane's Y_i slice: columns 4 lane + 128 u + v
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const VT yv = *reinterpret_cast<const VT*>(ys + lane * V + u * kStep);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) yd[u * 4 + v] = (double)vget(yv, v);
-    }
-    for (int64_t e = beg + wid; e < end; e += nw) {
-      const T* xr = Xt + (int64_t)(c_col[e] - v0) * ldk + lane * V;
-      VT x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const VT*>(xr + u * kStep));
-      double s = 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) s = fma(yd[u * 4 + v], (double)vget(x[u], v), s);
-      s = warp_sum(s);
-      if (lane == 0) c_g[e] = (T)(s * inv_n);
-    }
-    return;
-  }
   for (int64_t e = beg + wid; e < end; e += nw) {
     const T* xr = Xt + (int64_t)(c_col[e] - v0) * ldk;
     if constexpr (kArith == 1) {
@@ -1465,8 +1439,6 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                          200 * 1024);
     cudaFuncSetAttribute(refine_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    cudaFuncSetAttribute(refine_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
     attr_done(attr_seen);
   }
   if (dtype == ACCORD_F64)
@@ -1474,11 +1446,6 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                                                    (const double*)Y, (const double*)Xt,
                                                    (double*)c_g, v0, v1, itm_ptr, L, item_row,
                                                    y_global);
-  else if (ff == 2 && ldk == 1024 && !y_global)
-    refine_kernel<float, 2><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
-                                                     (const float*)Y, (const float*)Xt,
-                                                     (float*)c_g, v0, v1, itm_ptr, L, item_row,
-                                                     y_global);
   else if (ff == 1)
     refine_kernel<float, 1><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                         (const float*)Y, (const float*)Xt,
