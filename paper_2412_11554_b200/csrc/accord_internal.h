@@ -40,6 +40,17 @@ __device__ __forceinline__ __nv_bfloat162 filter_bf16x2(float a, float b) {
   return __halves2bfloat162(filter_bf16(a), filter_bf16(b));
 #endif
 }
+// The X^T operand rounded to 7 - drop mantissa bits (round to nearest even;
+// drop = 0: plain bf16). Fewer toggling bits lower the MMAs' energy and so
+// raise the power-capped clock; the filter bound uses this very rounding's
+// residual, so the candidate set stays certified.
+__device__ __forceinline__ __nv_bfloat16 filter_bf16_x(float x, int drop) {
+  if (drop == 0) return filter_bf16(x);
+  const int s = 16 + drop;
+  uint32_t u = __float_as_uint(x);
+  u += ((1u << (s - 1)) - 1) + ((u >> s) & 1u);
+  return __ushort_as_bfloat16((unsigned short)((u & ~((1u << s) - 1)) >> 16));
+}
 #endif
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -130,7 +141,7 @@ int launch_load_xt(int dtype, const void* X, int64_t ldx, int layout, int64_t n,
                    cudaStream_t st);
 // Xt f32 -> hi = bf16_rn(x), lo = bf16_rn(x - hi) (rows x ldk)
 int launch_split_bf16(const float* src, int64_t elems, __nv_bfloat16* hi,
-                      __nv_bfloat16* lo, cudaStream_t st);
+                      __nv_bfloat16* lo, cudaStream_t st, int drop = 0);
 
 // w = X (X^T u) / n (the samples' Gram operator; its top eigenvalue is L =
 // sigma_max(S)) on this rank's Xt (p x ldk). t: p doubles,
@@ -220,7 +231,7 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
                 const int32_t* col, const void* wn, const void* wo, const void* Xt,
                 void* Yout, __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A,
                 float* row_B, double* row_D2, double* row_Y2, cudaStream_t st,
-                const SpmmRing* ring = nullptr);
+                const SpmmRing* ring = nullptr, int ydrop = 0);
 
 // Exact candidate values: c_g[e] = (1/n) sum_m Y_im Xt_km in float64
 // accumulation, for every entry of C (block per row). BF16_FILTER refine and
@@ -251,7 +262,8 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                     const float* wn, const float* wo, const float* Xt, float* Yout,
                     __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
                     double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
-                    cudaStream_t st, const float* wn2 = nullptr, double* row_D2b = nullptr);
+                    cudaStream_t st, const float* wn2 = nullptr, double* row_D2b = nullptr,
+                    int ydrop = 0);
 
 // Columns [v0, v1) only, Xt row 0 = column v0 (one ring step of the sharded mode).
 // itm_ptr != NULL: one block per work item (row chunk of <= L candidates).
@@ -259,7 +271,8 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
                   cudaStream_t st, int64_t v0 = 0, int64_t v1 = INT64_MAX,
                   const int64_t* itm_ptr = nullptr, int64_t n_items = 0, int64_t L = 0,
-                  const int32_t* item_row = nullptr, int arith = 0);   // 1: float-float
+                  const int32_t* item_row = nullptr, int arith = 0,   // 1: float-float
+                  int sym = 0);   // 1: C = C^T at Omega = I, entries k < i from their twins
 
 
 
@@ -273,7 +286,7 @@ int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const in
 // columns [v0, v1) of |<x_i, x_k>| / n (CUDA cores; out may be NULL: ring steps
 // accumulate into row_max with accumulate = 1, then launch once more or reduce).
 int launch_row_ab(int64_t pk, int64_t ldk, const float* Xt_rows, float* row_A, float* row_B,
-                  cudaStream_t st);
+                  cudaStream_t st, int drop = 0);
 int launch_cand_dot_max(int dtype, int64_t pk, int64_t r0, int64_t n, int64_t ldk,
                         const int64_t* c_ptr, const int32_t* c_col, const void* Xi, const void* Xt,
                         int64_t v0, int64_t v1, int accumulate, double* row_max, double* out,
@@ -297,7 +310,8 @@ int launch_mirror_append(int64_t n, const int32_t* in, int64_t r0, int32_t* prow
 int launch_spin(int ms, cudaStream_t st);
 
 // Per-column constants of the filter bound from Xt (f32).
-int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st);
+int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st,
+                     int drop = 0);
 
 // Omega stats over the current CSR: l1, logdiag, nnz, diagonal check.
 int launch_omega_stats(int dtype, int64_t pk, int64_t r0, const int64_t* ptr,
@@ -318,7 +332,7 @@ int launch_diag_trial(int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_
                       double* row_a, cudaStream_t st);
 int launch_diag_apply(int64_t pk, int64_t ldk, int64_t xrow0, const float* Xt, float* Y,
                       __nv_bfloat16* Yhi, const double* row_a, double tau, float* row_A,
-                      float* row_B, cudaStream_t st);
+                      float* row_B, cudaStream_t st, int ydrop = 0);
 int launch_reduce_rows(int64_t pk, const double* row_D2, const double* row_dd,
                        const double* row_logd, const double* row_Y2, const double* row_l1,
                        const int32_t* row_nnz, const int64_t* c_ptr, double* out,

@@ -216,7 +216,12 @@ struct accord_ctx {
   void* c_wn2 = nullptr;                   // prox at the second step of a paired trial
   bool pair_ls = true;                     // paired line-search passes (ACCORD_LS_PAIRS=0: off)
   int refine_ff = 0;                       // 1: float-float refine (ACCORD_REFINE=ff; A-B, slower)
+  int x_drop = 0;                          // mantissa bits dropped from X^T_hi (filter path)
+  int x_drop_target = 0;                   // ACCORD_XDROP: width once |C| is small (A-B)
+  int y_drop = 0, y_drop_target = 0;       // the same for the Y_hi operand (ACCORD_YDROP)
+  double x_drop_at = 64.0;                 // ACCORD_XDROP_AT: switch at |C| / p below this
   bool omega_identity = false;             // Omega is exactly I (set at create, cleared on change)
+  bool c_sym = false;                      // C = C^T from the symmetric first GEMM (sym 1)
   double *row_dd2 = nullptr, *row_l1_2 = nullptr, *row_logd2 = nullptr, *row_D2b = nullptr;
   double *diag_xx = nullptr, *diag_xz = nullptr, *diag_zz = nullptr, *diag_a = nullptr;
   int32_t* row_nnz2 = nullptr;
@@ -531,20 +536,20 @@ void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void*
     c->launches += launch_spmm_tma(c->pk, c->ldk, ptr, col, (const float*)wn, (const float*)wo,
                                    (const float*)c->Xt, (float*)c->Y[yb], c->Yhi[yb], c->Ylo[yb],
                                    c->row_A[yb], c->row_B[yb], row_D2, row_Y2, items_view(c),
-                                   c->sm_count, c->st);
+                                   c->sm_count, c->st, nullptr, nullptr, c->y_drop);
     return;
   }
   if (!c->sharded) {
     c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, ptr, col, wn, wo, c->Xt, c->Y[yb],
                                c->Yhi[yb], c->Ylo[yb], c->row_A[yb], c->row_B[yb], row_D2,
-                               row_Y2, c->st);
+                               row_Y2, c->st, nullptr, c->y_drop);
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool first, bool last) {
     SpmmRing rg{v0, v1, c->yacc, c->dacc, first ? 1 : 0, last ? 1 : 0};
     c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, ptr, col, wn, wo, slab, c->Y[yb],
                                c->Yhi[yb], c->Ylo[yb], c->row_A[yb], c->row_B[yb], row_D2,
-                               row_Y2, c->st, &rg);
+                               row_Y2, c->st, &rg, c->y_drop);
   });
 }
 
@@ -555,9 +560,15 @@ void refine_all(accord_ctx* c, const void* yrows = nullptr) {
   if (!c->sharded) {
     // hub rows (up to ~1.6e5 candidates) split over several work items
     if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
+    // C = C^T at Omega = I (Y = X^T, G = S): half the gathers, the rest mirrored
+    // (ACCORD_REFINE_NOSYM: off; ACCORD_DEBUG_MIRROR_MISS: every twin looked up
+    // is treated as missing, a test of the fallback)
+    const int sym = c->c_sym && !yrows && !std::getenv("ACCORD_REFINE_NOSYM")
+                        ? (std::getenv("ACCORD_DEBUG_MIRROR_MISS") ? 2 : 1)
+                        : 0;
     c->launches += launch_refine(c->dtype, c->pk, c->n, c->ldk, c->c_ptr, c->c_col, Y, c->Xt,
                                  c->c_g, c->st, 0, INT64_MAX, c->itm_ptr, c->n_items,
-                                 kItemEntries, c->item_row, c->refine_ff);
+                                 kItemEntries, c->item_row, c->refine_ff, sym);
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool, bool) {
@@ -1232,6 +1243,9 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     c->pair_ls = !(e && e[0] == '0');
     const char* r = std::getenv("ACCORD_REFINE");     // A-B: ff = float-float refine
     c->refine_ff = (r && r[0] == 'f' && r[1] == 'f') ? 1 : 0;
+    if (const char* x = std::getenv("ACCORD_XDROP")) c->x_drop_target = std::clamp(std::atoi(x), 0, 4);
+    if (const char* x = std::getenv("ACCORD_YDROP")) c->y_drop_target = std::clamp(std::atoi(x), 0, 4);
+    if (const char* x = std::getenv("ACCORD_XDROP_AT")) c->x_drop_at = std::atof(x);
   }
   c->bad_diag = c->dalloc<int32_t>(1);
   c->scan_tmp_sz = scan_tmp_bytes(c->pk + 1);
@@ -1480,6 +1494,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     CK(cudaEventRecord(c->ev[2], S));
     CK(cudaMemcpyAsync(c->c_ptr, c->refit_ptr, (c->pk + 1) * 8, cudaMemcpyDeviceToDevice, S));
     c->items_of = nullptr;
+    c->c_sym = false;
     CK(cudaMemcpyAsync(c->c_col, c->refit_col, c->refit_nnz * 4, cudaMemcpyDeviceToDevice, S));
     c->launches += launch_lookup(c->dtype, c->pk, c->c_ptr, c->c_col, c->om_ptr, c->om_col,
                                  c->om_val, c->c_w, S);
@@ -1554,6 +1569,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       ep.audit_acc = nullptr;
       omv = ov->om;
     }
+    c->c_sym = !ov && ep.sym == 1;
     CK(cudaEventRecord(c->ev[1], S));
     const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
     auto gemm = [&](const void* xt, int bsel, int64_t v0, int64_t v1) {
@@ -1692,6 +1708,18 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
   st.ms_refine = ev_ms(c, 3, 4);
 }
 
+// X^T_hi rounded to 7 - drop mantissa bits (filter path, X replicated): the
+// bf16 copy, the per-column bound constants and the tile maxima are rebuilt
+// from the f32 X^T, so the filter stays certified. The
+// candidate set only grows (the bound widens), never loses an entry.
+void set_x_width(accord_ctx* c, int drop) {
+  c->launches += launch_split_bf16((const float*)c->Xt, c->xrows_pad * c->ldk, c->Xhi, nullptr,
+                                   c->st, drop);
+  c->launches += launch_col_norms(c->p, c->ldk, (const float*)c->Xt, c->col_sd, c->st, drop);
+  c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
+  c->x_drop = drop;
+}
+
 void step_one(accord_ctx* c, accord_iter_stats* s) {
   accord_iter_stats st{};
   cudaStream_t S = c->st;
@@ -1753,7 +1781,8 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
                                      (const float*)c->c_w, (const float*)c->Xt,
                                      (float*)c->Y[nb], c->Yhi[nb], c->Ylo[nb], c->row_A[nb],
                                      c->row_B[nb], c->row_D2, c->row_Y2, items_view(c),
-                                     c->sm_count, S, (const float*)c->c_wn2, c->row_D2b);
+                                     c->sm_count, S, (const float*)c->c_wn2, c->row_D2b,
+                                     c->y_drop);
     } else {
       spmm_all(c, c->c_ptr, c->c_col, c->c_wn, c->c_w, nb, c->row_D2, c->row_Y2);
     }
@@ -1823,7 +1852,8 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   // ---------------- accept: Omega <- Omega+, Y <- Y+ ----------------
   if (diag_ls)
     c->launches += launch_diag_apply(c->pk, c->ldk, xrow0, (const float*)c->Xt, (float*)c->Y[nb],
-                                     c->Yhi[nb], c->diag_a, tau, c->row_A[nb], c->row_B[nb], S);
+                                     c->Yhi[nb], c->diag_a, tau, c->row_A[nb], c->row_B[nb], S,
+                                     c->y_drop);
   c->launches += launch_scan_i32(c->row_nnz, c->om_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
   c->launches += launch_compact(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_wn, c->om_ptr,
                                 c->om_col, c->om_val, S);
@@ -1855,6 +1885,10 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   st.ms_total = ev_ms(c, 0, 7);
   TR_flush(c);
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
+  if (c->plan && c->col_sd && !c->sharded && (double)st.n_cand <= c->x_drop_at * (double)c->p) {
+    if (c->x_drop != c->x_drop_target) set_x_width(c, c->x_drop_target);
+    c->y_drop = c->y_drop_target;   // from the next Y on (each Y carries its own row norms)
+  }
   if (s) *s = st;
 }
 
@@ -1911,7 +1945,7 @@ double lambda_max_impl(accord_ctx* c) {
   tmp.v.push_back({dmax, 4});
   CK(cudaMemsetAsync(eptr, 0, (c->pk + 1) * 8, S));
   CK(cudaMemsetAsync(dmax, 0, 4, S));
-  c->launches += launch_row_ab(c->pk, c->ldk, (const float*)xrows, rA, rB, S);
+  c->launches += launch_row_ab(c->pk, c->ldk, (const float*)xrows, rA, rB, S, c->x_drop);
   GradOverride ov{2, rA, rB, OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax,
                   c->world == 1 && !c->sharded && c->r0 == 0 && c->pk == c->p &&
                       !std::getenv("ACCORD_GEMM_NOSYM")};

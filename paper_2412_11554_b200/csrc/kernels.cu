@@ -92,12 +92,14 @@ __global__ void load_xt_kernel(const T* __restrict__ X, int64_t ldx, int layout,
 
 __global__ void split_bf16_kernel(const float4* __restrict__ src, int64_t n4,
                                   __nv_bfloat162* __restrict__ hi,
-                                  __nv_bfloat162* __restrict__ lo) {
+                                  __nv_bfloat162* __restrict__ lo, int drop) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 v = src[i];
-    __nv_bfloat162 h0 = filter_bf16x2(v.x, v.y);
-    __nv_bfloat162 h1 = filter_bf16x2(v.z, v.w);
+    __nv_bfloat162 h0 = drop ? __halves2bfloat162(filter_bf16_x(v.x, drop), filter_bf16_x(v.y, drop))
+                             : filter_bf16x2(v.x, v.y);
+    __nv_bfloat162 h1 = drop ? __halves2bfloat162(filter_bf16_x(v.z, drop), filter_bf16_x(v.w, drop))
+                             : filter_bf16x2(v.z, v.w);
     float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
     hi[2 * i] = h0;
     hi[2 * i + 1] = h1;
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
     const int32_t* __restrict__ col, const T* __restrict__ wn, const T* __restrict__ wo,
     const T* __restrict__ Xt, T* __restrict__ Yout, __nv_bfloat16* __restrict__ Yhi,
     __nv_bfloat16* __restrict__ Ylo, float* __restrict__ row_A, float* __restrict__ row_B,
-    double* __restrict__ row_D2, double* __restrict__ row_Y2, SpmmRing rg) {
+    double* __restrict__ row_D2, double* __restrict__ row_Y2, SpmmRing rg, int ydrop) {
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   __shared__ int32_t s_col[kSpmmMaxThreads];
@@ -633,7 +635,7 @@ __global__ void __launch_bounds__(1024) spmm_kernel(
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const float y = (float)yt[v];
-          const __nv_bfloat16 h = filter_bf16(y);
+          const __nv_bfloat16 h = filter_bf16_x(y, ydrop);
           const float hf = __bfloat162float(h);
           Yhi[r * ldk + c + v] = h;
           if (Ylo) Ylo[r * ldk + c + v] = __float2bfloat16_rn(y - hf);
@@ -688,8 +690,41 @@ __device__ __forceinline__ void ff_madd(float& hi, float& lo, float x, float y) 
   hi = t;
 }
 
+// <y, x> over ldk elements in float64 (exact f32 products), lanes striding
+// the row, 8 loads in flight per lane, warp-reduced: the refine's dot product
+// (its summation order is fixed, so (i,k) and (k,i) at Omega = I agree bitwise)
+template <typename T>
+__device__ __forceinline__ double warp_dot_f64(const T* ys, const T* __restrict__ xr, int64_t ldk,
+                                               int lane) {
+  using VT = typename Vec<T>::type;
+  constexpr int V = Vec<T>::V;
+  constexpr int kStep = 32 * V;           // elements per lane-pass over the row
+  double s = 0.0;
+  int64_t m = lane * V;
+  for (; m + 7 * kStep < ldk; m += 8 * kStep) {
+    VT x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const VT*>(xr + m + u * kStep));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const VT yv = *reinterpret_cast<const VT*>(ys + m + u * kStep);
+#pragma unroll
+      for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
+    }
+  }
+  for (; m < ldk; m += kStep) {
+    const VT x = __ldg(reinterpret_cast<const VT*>(xr + m));
+    const VT yv = *reinterpret_cast<const VT*>(ys + m);
+#pragma unroll
+    for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
+  }
+  return warp_sum(s);
+}
+
 // kArith: 0 = float64 products (both operands converted by F2F), 1 =
 // float-float (A-B variant, slower; ACCORD_REFINE=ff)
+// sym (Omega = I on one rank, C = C^T): only the entries with k >= i; the
+// others are copied from their twins afterwards (sym_mirror_kernel)
 template <typename T, int kArith = 0>
 __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int64_t ldk,
                                                      const int64_t* __restrict__ c_ptr,
@@ -699,7 +734,7 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
                                                      T* __restrict__ c_g, int64_t v0,
                                                      int64_t v1, const int64_t* __restrict__ itm_ptr,
                                                      int64_t L, const int32_t* __restrict__ item_row,
-                                                     int y_global) {
+                                                     int y_global, int sym) {
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   extern __shared__ __align__(16) uint8_t ys_raw[];
@@ -719,7 +754,7 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   }
   // columns [v0, v1) only (Xt row 0 = column v0): one ring step of the
   // sharded mode (NEXT(3)); v0 = 0, v1 = p otherwise
-  beg = lower_bound_col(c_col, beg, end, v0);
+  beg = lower_bound_col(c_col, beg, end, sym ? max(v0, r) : v0);
   end = lower_bound_col(c_col, beg, end, v1);
   if (beg == end) return;
   if (y_global) {
@@ -764,27 +799,45 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
       if (lane == 0) c_g[e] = (T)(s * inv_n);
       continue;
     }
-    double s = 0.0;
-    int64_t m = lane * V;
-    for (; m + 7 * kStep < ldk; m += 8 * kStep) {   // 8 loads in flight per lane
-      VT x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const VT*>(xr + m + u * kStep));
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const VT yv = *reinterpret_cast<const VT*>(ys + m + u * kStep);
-#pragma unroll
-        for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x[u], v), s);
-      }
-    }
-    for (; m < ldk; m += kStep) {
-      const VT x = __ldg(reinterpret_cast<const VT*>(xr + m));
-      const VT yv = *reinterpret_cast<const VT*>(ys + m);
-#pragma unroll
-      for (int v = 0; v < V; ++v) s = fma((double)vget(yv, v), (double)vget(x, v), s);
-    }
-    s = warp_sum(s);
+    const double s = warp_dot_f64<T>(ys, xr, ldk, lane);
     if (lane == 0) c_g[e] = (T)(s * inv_n);
+  }
+}
+
+// The entries k < i of a symmetric C (Omega = I on one rank, G = S): c_g from
+// the twin (k, i), found by binary search in row k's sorted columns. The
+// filter decides the entries of a diagonal tile one by one, so a twin can be
+// missing near the threshold: that entry's dot product is computed here, by
+// the whole warp in the refine's order. Warp per row. all_miss: every entry
+// takes that path (test of the fallback).
+template <typename T>
+__global__ void sym_mirror_kernel(int64_t pk, int64_t ldk, const int64_t* __restrict__ c_ptr,
+                                  const int32_t* __restrict__ c_col, const T* __restrict__ Y,
+                                  const T* __restrict__ Xt, T* __restrict__ c_g, double inv_n,
+                                  int all_miss) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= pk) return;
+  const int64_t beg = c_ptr[i];
+  const int64_t end = lower_bound_col(c_col, beg, c_ptr[i + 1], i);
+  for (int64_t e0 = beg; e0 < end; e0 += 32) {
+    const int64_t e = e0 + lane;
+    bool miss = false;
+    if (e < end) {
+      const int64_t k = c_col[e];
+      const int64_t kb = c_ptr[k], ke = c_ptr[k + 1];
+      const int64_t pos = lower_bound_col(c_col, kb, ke, i);
+      if (!all_miss && pos < ke && c_col[pos] == (int32_t)i) c_g[e] = c_g[pos];
+      else miss = true;
+    }
+    unsigned mm = __ballot_sync(0xffffffffu, miss);
+    while (mm) {
+      const int l = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int64_t ee = e0 + l;
+      const double s = warp_dot_f64<T>(Y + i * ldk, Xt + (int64_t)c_col[ee] * ldk, ldk, lane);
+      if (lane == 0) c_g[ee] = (T)(s * inv_n);
+    }
   }
 }
 
@@ -866,14 +919,14 @@ __global__ void __launch_bounds__(1024) reduce_max_kernel(int64_t pk, const doub
 // Filter row constants of A = the rank's rows of X^T (Omega = I): A_i =
 // ||x_i - bf16(x_i)||, B_i = ||x_i||, rounded up (warp per row).
 __global__ void xrow_ab_kernel(int64_t pk, int64_t ldk, const float* __restrict__ Xt,
-                               float* __restrict__ row_A, float* __restrict__ row_B) {
+                               float* __restrict__ row_A, float* __restrict__ row_B, int drop) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= pk) return;
   double xx = 0, ee = 0;
   for (int64_t m = lane; m < ldk; m += 32) {
     const float x = Xt[r * ldk + m];
-    const double e = (double)x - (double)__bfloat162float(filter_bf16(x));
+    const double e = (double)x - (double)__bfloat162float(filter_bf16_x(x, drop));
     xx += (double)x * x;
     ee += e * e;
   }
@@ -1000,14 +1053,14 @@ __global__ void mirror_append_kernel(int64_t n, const int32_t* __restrict__ in, 
 
 // per-column constants of the filter bound (warp per column of X = row of Xt)
 __global__ void col_norms_kernel(int64_t p, int64_t ldk, const float* __restrict__ Xt,
-                                 float2* __restrict__ col_sd) {
+                                 float2* __restrict__ col_sd, int drop) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (k >= p) return;
   double xx = 0, ee = 0;
   for (int64_t m = lane; m < ldk; m += 32) {
     const float x = Xt[k * ldk + m];
-    const double e = (double)x - (double)__bfloat162float(filter_bf16(x));
+    const double e = (double)x - (double)__bfloat162float(filter_bf16_x(x, drop));
     xx += (double)x * x;
     ee += e * e;
   }
@@ -1278,11 +1331,11 @@ int launch_load_xt(int dtype, const void* X, int64_t ldx, int layout, int64_t n,
 }
 
 int launch_split_bf16(const float* src, int64_t elems, __nv_bfloat16* hi, __nv_bfloat16* lo,
-                      cudaStream_t st) {
+                      cudaStream_t st, int drop) {
   const int64_t n4 = elems / 4;
   split_bf16_kernel<<<grid_for(n4, 256, 148 * 64), 256, 0, st>>>(
       reinterpret_cast<const float4*>(src), n4, reinterpret_cast<__nv_bfloat162*>(hi),
-      reinterpret_cast<__nv_bfloat162*>(lo));
+      reinterpret_cast<__nv_bfloat162*>(lo), drop);
   return 1;
 }
 
@@ -1394,7 +1447,8 @@ int launch_prox(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const i
 int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* ptr,
                 const int32_t* col, const void* wn, const void* wo, const void* Xt, void* Yout,
                 __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
-                double* row_D2, double* row_Y2, cudaStream_t st, const SpmmRing* ring) {
+                double* row_D2, double* row_Y2, cudaStream_t st, const SpmmRing* ring,
+                int ydrop) {
   const SpmmRing rg = ring ? *ring : SpmmRing{0, 0, nullptr, nullptr, 1, 1};
   const int V = dtype == ACCORD_F64 ? 2 : 4;
   int threads = (int)std::min<int64_t>(kSpmmMaxThreads, round_up(ldk / V, 32));
@@ -1402,15 +1456,15 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
   if (dtype == ACCORD_F64) {
     spmm_kernel<double, false><<<(unsigned)pk, threads, 0, st>>>(
         pk, n, ldk, ptr, col, (const double*)wn, (const double*)wo, (const double*)Xt,
-        (double*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2, rg);
+        (double*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2, rg, 0);
   } else if (Yhi) {
     spmm_kernel<float, true><<<(unsigned)pk, threads, 0, st>>>(
         pk, n, ldk, ptr, col, (const float*)wn, (const float*)wo, (const float*)Xt,
-        (float*)Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2, rg);
+        (float*)Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2, rg, Ylo ? 0 : ydrop);
   } else {
     spmm_kernel<float, false><<<(unsigned)pk, threads, 0, st>>>(
         pk, n, ldk, ptr, col, (const float*)wn, (const float*)wo, (const float*)Xt,
-        (float*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2, rg);
+        (float*)Yout, nullptr, nullptr, nullptr, nullptr, row_D2, row_Y2, rg, 0);
   }
   return 1;
 }
@@ -1418,7 +1472,7 @@ int launch_spmm(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* pt
 int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* c_ptr,
                   const int32_t* c_col, const void* Y, const void* Xt, void* c_g,
                   cudaStream_t st, int64_t v0, int64_t v1, const int64_t* itm_ptr,
-                  int64_t n_items, int64_t L, const int32_t* item_row, int ff) {
+                  int64_t n_items, int64_t L, const int32_t* item_row, int ff, int sym) {
   const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
   size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
@@ -1445,18 +1499,28 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
     refine_kernel<double><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                    (const double*)Y, (const double*)Xt,
                                                    (double*)c_g, v0, v1, itm_ptr, L, item_row,
-                                                   y_global);
+                                                   y_global, sym);
   else if (ff == 1)
     refine_kernel<float, 1><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                         (const float*)Y, (const float*)Xt,
                                                         (float*)c_g, v0, v1, itm_ptr, L, item_row,
-                                                        y_global);
+                                                        y_global, sym);
   else
     refine_kernel<float><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                   (const float*)Y, (const float*)Xt,
                                                   (float*)c_g, v0, v1, itm_ptr, L, item_row,
-                                                  y_global);
-  return 1;
+                                                  y_global, sym);
+  if (!sym) return 1;
+  const unsigned mg = (unsigned)((pk + 7) / 8);
+  if (dtype == ACCORD_F64)
+    sym_mirror_kernel<double><<<mg, 256, 0, st>>>(pk, ldk, c_ptr, c_col, (const double*)Y,
+                                                  (const double*)Xt, (double*)c_g, 1.0 / (double)n,
+                                                  sym == 2);
+  else
+    sym_mirror_kernel<float><<<mg, 256, 0, st>>>(pk, ldk, c_ptr, c_col, (const float*)Y,
+                                                 (const float*)Xt, (float*)c_g, 1.0 / (double)n,
+                                                 sym == 2);
+  return 2;
 }
 
 int launch_lookup(int dtype, int64_t pk, const int64_t* c_ptr, const int32_t* c_col,
@@ -1490,9 +1554,9 @@ int launch_kkt(int dtype, int64_t pk, int64_t r0, const int64_t* c_ptr, const in
 }
 
 int launch_row_ab(int64_t pk, int64_t ldk, const float* Xt_rows, float* row_A, float* row_B,
-                  cudaStream_t st) {
+                  cudaStream_t st, int drop) {
   if (pk == 0) return 0;
-  xrow_ab_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, ldk, Xt_rows, row_A, row_B);
+  xrow_ab_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, ldk, Xt_rows, row_A, row_B, drop);
   return 1;
 }
 
@@ -1574,8 +1638,9 @@ int launch_spin(int ms, cudaStream_t st) {
   return 1;
 }
 
-int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st) {
-  col_norms_kernel<<<(unsigned)((p + 7) / 8), 256, 0, st>>>(p, ldk, Xt, col_sd);
+int launch_col_norms(int64_t p, int64_t ldk, const float* Xt, float2* col_sd, cudaStream_t st,
+                     int drop) {
+  col_norms_kernel<<<(unsigned)((p + 7) / 8), 256, 0, st>>>(p, ldk, Xt, col_sd, drop);
   return 1;
 }
 
@@ -1745,7 +1810,8 @@ __global__ void diag_apply_kernel(int64_t pk, int64_t ldk, int64_t xrow0,
                                   const float* __restrict__ Xt, float* __restrict__ Y,
                                   __nv_bfloat16* __restrict__ Yhi,
                                   const double* __restrict__ row_a, double tau,
-                                  float* __restrict__ row_A, float* __restrict__ row_B) {
+                                  float* __restrict__ row_A, float* __restrict__ row_B,
+                                  int ydrop) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= pk) return;
@@ -1756,7 +1822,7 @@ __global__ void diag_apply_kernel(int64_t pk, int64_t ldk, int64_t xrow0,
   for (int64_t m = lane; m < ldk; m += 32) {
     const float v = (float)(a * (double)x[m] + tau * (double)y[m]);
     y[m] = v;
-    const __nv_bfloat16 h = filter_bf16(v);
+    const __nv_bfloat16 h = filter_bf16_x(v, ydrop);
     Yhi[r * ldk + m] = h;
     const double e = (double)v - (double)__bfloat162float(h);
     a2 += e * e;
@@ -1796,10 +1862,10 @@ int launch_diag_trial(int64_t pk, int64_t r0, const int64_t* c_ptr, const int32_
 
 int launch_diag_apply(int64_t pk, int64_t ldk, int64_t xrow0, const float* Xt, float* Y,
                       __nv_bfloat16* Yhi, const double* row_a, double tau, float* row_A,
-                      float* row_B, cudaStream_t st) {
+                      float* row_B, cudaStream_t st, int ydrop) {
   if (pk == 0) return 0;
   diag_apply_kernel<<<(unsigned)((pk + 7) / 8), 256, 0, st>>>(pk, ldk, xrow0, Xt, Y, Yhi, row_a,
-                                                               tau, row_A, row_B);
+                                                               tau, row_A, row_B, ydrop);
   return 1;
 }
 

@@ -71,7 +71,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
                 __nv_bfloat16* __restrict__ Yhi, __nv_bfloat16* __restrict__ Ylo,
                 float* __restrict__ row_A, float* __restrict__ row_B, double* __restrict__ row_D2,
                 double* __restrict__ row_Y2, const float* __restrict__ wn2,
-                double* __restrict__ row_D2b, SpmmItems items) {
+                double* __restrict__ row_D2b, SpmmItems items, int ydrop) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t stage_bytes = (uint32_t)(ldk * 4);
   float* data = reinterpret_cast<float*>(sm);
@@ -341,7 +341,9 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
           uint32_t hp[kCols / 2], lp[kCols / 2];
 #pragma unroll
           for (int v = 0; v < kCols; v += 2) {
-            const __nv_bfloat162 h2 = filter_bf16x2(yt[v], yt[v + 1]);
+            const __nv_bfloat162 h2 =
+                ydrop ? __halves2bfloat162(filter_bf16_x(yt[v], ydrop), filter_bf16_x(yt[v + 1], ydrop))
+                      : filter_bf16x2(yt[v], yt[v + 1]);
             const float2 hf = __bfloat1622float2(h2);
             const __nv_bfloat162 l2 = __floats2bfloat162_rn(yt[v] - hf.x, yt[v + 1] - hf.y);
             hp[v / 2] = *reinterpret_cast<const uint32_t*>(&h2);
@@ -461,7 +463,7 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                     const float* wn, const float* wo, const float* Xt, float* Yout,
                     __nv_bfloat16* Yhi, __nv_bfloat16* Ylo, float* row_A, float* row_B,
                     double* row_D2, double* row_Y2, const SpmmItems& items, int sm_count,
-                    cudaStream_t st, const float* wn2, double* row_D2b) {
+                    cudaStream_t st, const float* wn2, double* row_D2b, int ydrop) {
   if (pk == 0) return 0;
   int stages = 0;
   const size_t smem = spmm_tma_smem(ldk, &stages);
@@ -493,7 +495,7 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
       per_sm = 1;
     kern<<<sm_count * std::min(per_sm, 8), 32 + consumers, smem, st>>>(
         pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2,
-        wn2, row_D2b, items);
+        wn2, row_D2b, items, Ylo ? 0 : ydrop);
   };
   if (cols == 4) {
     if (wn2) launch(spmm_tma_kernel<true, 4>);

@@ -326,6 +326,10 @@ def test_symmetric_first_gemm_matches_full(p, n, lam, T, monkeypatch):
     different certified superset, the refine recomputes every value exactly,
     so the iterates, tau schedule and objective are bitwise those of the full
     GEMM (ACCORD_GEMM_NOSYM=1); ragged p (not a multiple of 256) included.
+    The refine of that C gathers only the entries k >= i and copies the rest
+    from their twins (C = C^T; the float64 dot product of exact f32 products
+    in a fixed order is symmetric bitwise); a twin the filter did not emit is
+    recomputed, which ACCORD_DEBUG_MIRROR_MISS forces for every entry.
     (Rows stay below one work item, 2048 candidates, so the extra zero-valued
     candidates cannot regroup any partial sum.)"""
     _cuda()
@@ -335,17 +339,25 @@ def test_symmetric_first_gemm_matches_full(p, n, lam, T, monkeypatch):
     Xt -= Xt.mean(axis=1, keepdims=True)
     inv_L = 1.0 / O.spectral_bound(Xt.astype(np.float64))
     out = {}
-    for nosym in ("0", "1"):
-        if nosym == "1":
-            monkeypatch.setenv("ACCORD_GEMM_NOSYM", "1")
-        else:
-            monkeypatch.delenv("ACCORD_GEMM_NOSYM", raising=False)
+    modes = {"sym": {}, "miss": {"ACCORD_DEBUG_MIRROR_MISS": "1"},
+             "refine_nosym": {"ACCORD_REFINE_NOSYM": "1"}, "nosym": {"ACCORD_GEMM_NOSYM": "1"}}
+    for mode, env in modes.items():
+        for k in ("ACCORD_DEBUG_MIRROR_MISS", "ACCORD_REFINE_NOSYM", "ACCORD_GEMM_NOSYM"):
+            if k in env:
+                monkeypatch.setenv(k, env[k])
+            else:
+                monkeypatch.delenv(k, raising=False)
         with A.AccordSolver(torch.from_numpy(Xt).cuda(), lam, inv_L=inv_L,
                             gemm=A.GEMM_BF16_FILTER) as s:
             st = s.step(T)
-            out[nosym] = ([(x["tau"], x["trials"], x["f"], x["nnz"]) for x in st],
-                          st[0]["n_cand"], s.export_csr())
-    (s1, nc1, c1), (s0, nc0, c0) = out["0"], out["1"]
+            out[mode] = ([(x["tau"], x["trials"], x["f"], x["nnz"]) for x in st],
+                         st[0]["n_cand"], s.export_csr())
+    for mode in ("miss", "refine_nosym"):
+        s_, nc_, c_ = out[mode]
+        assert s_ == out["sym"][0] and nc_ == out["sym"][1], mode
+        assert np.array_equal(c_.col, out["sym"][2].col), mode
+        assert np.array_equal(c_.val, out["sym"][2].val), mode
+    (s1, nc1, c1), (s0, nc0, c0) = out["sym"], out["nosym"]
     assert s1 == s0
     assert s1[0][3] > p                          # off-diagonal support after iteration 1
     assert nc1 >= s1[0][3] and nc0 >= s0[0][3]
