@@ -457,6 +457,11 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
     # the slowest rank's GEMM (max over ranks; rank 0's row block is the largest)
     achieved = 2.0 * pk0 * p * n / (ms_gemm_max / 1e3) / 1e12
     peak = float(pk_.get("bf16_tflops_sustained", pk_.get("bf16_tflops")))
+    i8 = info0["gemm"] == A.GEMM_I8_FILTER
+    # int8 tensor rate = 2x bf16 on B200 (4.5 vs 2.25 POP/s dense, the fp8 row
+    # of B200_PROFILING.md's table): the measured bf16 peak x the nominal ratio
+    peak_mult = 2.0 if i8 else 1.0
+    peak *= peak_mult
     # the same peak at the clock this run held (the measured sustained figure
     # was taken at MEASURED_PEAKS' median clock under load)
     ref_mhz = (pk_.get("clocks_under_load") or {}).get("sm_mhz_median")
@@ -467,7 +472,8 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
         try:
             with open(tf) as f:
                 tj = json.load(f)
-            if tj.get("workload") == cfg.name and tj.get("world") == world:
+            if (tj.get("workload") == cfg.name and tj.get("world") == world
+                    and tj.get("gemm", "bf16_filter_tcgen05+sddmm") == A.GEMM_NAMES[info0["gemm"]]):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -480,16 +486,22 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32",
-        "gemm_arith": "bf16 x bf16 -> fp32 TMEM (certified filter) + f64-accumulated refine",
+        "gemm_arith": ("int8 x int8 -> exact s32 TMEM (certified filter) + f64-accumulated refine"
+                       if i8 else
+                       "bf16 x bf16 -> fp32 TMEM (certified filter) + f64-accumulated refine"),
         "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
         "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]], shard, flush),
         "effective_tflops": flops_iter * value / 1e12,
         # whole step against the same peak (2 p_k p n / Peak / t_iter)
         "step_roofline_frac": flops_iter * value / 1e12 / peak,
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel<1,6,true> (bf16 filter + epilogue)",
+        "roofline": {"bound": "tensor",
+                     "kernel": ("gemm_tc_kernel<2,6,true> (int8 filter + epilogue)" if i8 else
+                                "gemm_tc_kernel<1,6,true> (bf16 filter + epilogue)"),
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": f"bf16_tflops_sustained, {pdata}",
+                     "peak_source": (f"int8 = 2 x bf16_tflops_sustained (nominal dense ratio, "
+                                     f"B200_PROFILING.md), {pdata}" if i8 else
+                                     f"bf16_tflops_sustained, {pdata}"),
                      "peak_at_run_clock": peak_clk,
                      "frac_at_run_clock": achieved / peak_clk if peak_clk else None,
                      "algorithmic": f"2*p_k*p*n = {2.0 * pk0 * p * n:.3e} FLOP per launch",

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define ACCORD_ABI_VERSION 3
+#define ACCORD_ABI_VERSION 4
 
 typedef enum {
   ACCORD_OK = 0,
@@ -68,15 +68,26 @@ typedef enum {
 } accord_dtype;
 
 typedef enum {
-  ACCORD_GEMM_AUTO = 0,         /* F32: BF16_FILTER on sm_100, else SIMT. F64: SIMT. */
+  ACCORD_GEMM_AUTO = 0,         /* F32 on sm_100: the certified filter with ADAPTIVE operands -- bf16
+                                   while the candidate set is large (|C| / p > 48, the first
+                                   iterations), then int8 (I8_FILTER's GEMM); X sharded: BF16_FILTER.
+                                   Otherwise SIMT. F64: SIMT. info.gemm reports BF16_FILTER, or
+                                   I8_FILTER once an int8 GEMM ran (gemm_launches_i8). */
   ACCORD_GEMM_BF16X3 = 1,       /* tcgen05 GEMM, split-bf16 operands, 3 MMAs (hi*hi + hi*lo + lo*hi),
                                    fp32 TMEM accumulator; candidate values taken from the tensor cores
                                    (~2^-16 relative product error) */
   ACCORD_GEMM_SIMT = 2,         /* CUDA-core GEMM in the context dtype (reference path; the only F64 path) */
-  ACCORD_GEMM_BF16_FILTER = 3   /* tcgen05 single-pass bf16 GEMM as a certified filter: emits (i,k) when
+  ACCORD_GEMM_BF16_FILTER = 3,  /* tcgen05 single-pass bf16 GEMM as a certified filter: emits (i,k) when
                                    |G~_ik| > lambda - delta_ik (delta_ik a rigorous bound on the bf16
                                    rounding + fp32 accumulation error), then every candidate value is
                                    recomputed exactly (float64 accumulation) by an SDDMM */
+  ACCORD_GEMM_I8_FILTER = 4     /* the same certified filter on int8 operands (tcgen05 kind::i8, exact
+                                   s32 accumulation, twice the bf16 MMA rate): Y rows quantised with a
+                                   per-row scale, X^T with a per-256-variable block scale; the bound is
+                                   the quantisation error alone (Cauchy-Schwarz on the actual error
+                                   vectors); values recomputed exactly by the SDDMM. F32, sm_100,
+                                   X replicated (not x_sharded). Every GEMM in int8 (AUTO switches
+                                   adaptively). DESIGN.md §5. */
 } accord_gemm;
 
 typedef enum {
@@ -175,6 +186,8 @@ typedef struct {
   float ms_reduce;    /* reductions + collectives + host decision, all trials */
   float ms_total;     /* whole iteration */
   int64_t max_row_cand; /* longest candidate row of this rank (diagnostic) */
+  int32_t gemm_i8;      /* 1 if this iteration's gradient GEMM ran on int8 operands (I8_FILTER) */
+  int32_t pad_;
 } accord_iter_stats;
 
 typedef struct {
@@ -193,6 +206,7 @@ typedef struct {
   size_t workspace_high;        /* high-water mark of the workspace in use */
   int64_t mirrored_sent;        /* candidate positions this rank sent to their row's owner in the
                                    symmetric first GEMM across ranks (cumulative, diagnostic) */
+  int64_t gemm_launches_i8;     /* of gemm_launches, those on int8 operands */
 } accord_info;
 
 typedef struct accord_ctx accord_ctx;

@@ -25,12 +25,12 @@ STATUS = {0: "ok", 1: "invalid", 2: "cuda", 3: "nccl", 4: "capacity", 5: "numeri
  E_COMM) = range(1, 10)
 LAYOUT_SAMPLES, LAYOUT_VARIABLES = 0, 1
 F32, F64 = 0, 1
-GEMM_AUTO, GEMM_BF16X3, GEMM_SIMT, GEMM_BF16_FILTER = 0, 1, 2, 3
+GEMM_AUTO, GEMM_BF16X3, GEMM_SIMT, GEMM_BF16_FILTER, GEMM_I8_FILTER = 0, 1, 2, 3, 4
 COMM_NONE, COMM_NCCL, COMM_HOST = 0, 1, 2
 SCOPE_LOCAL, SCOPE_GATHER = 0, 1
 EXPORT_OMEGA, EXPORT_THETA, EXPORT_PCORR = 0, 1, 2
 GEMM_NAMES = {GEMM_AUTO: "auto", GEMM_BF16X3: "bf16x3_tcgen05", GEMM_SIMT: "simt",
-              GEMM_BF16_FILTER: "bf16_filter_tcgen05+sddmm"}
+              GEMM_BF16_FILTER: "bf16_filter_tcgen05+sddmm", GEMM_I8_FILTER: "i8_filter_tcgen05+sddmm"}
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int32)
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
@@ -69,7 +69,7 @@ class IterStats(C.Structure):
         ("ms_gemm", C.c_float), ("ms_finalize", C.c_float), ("ms_refine", C.c_float),
         ("ms_prox", C.c_float),
         ("ms_spmm", C.c_float), ("ms_reduce", C.c_float), ("ms_total", C.c_float),
-        ("max_row_cand", C.c_int64),
+        ("max_row_cand", C.c_int64), ("gemm_i8", C.c_int32), ("pad_", C.c_int32),
     ]
 
     def as_dict(self):
@@ -88,7 +88,7 @@ class Info(C.Structure):
         ("kernel_launches", C.c_int64), ("gemm_launches", C.c_int64),
         ("f", C.c_double), ("device_bytes", C.c_size_t),
         ("workspace_bytes", C.c_size_t), ("workspace_high", C.c_size_t),
-        ("mirrored_sent", C.c_int64),
+        ("mirrored_sent", C.c_int64), ("gemm_launches_i8", C.c_int64),
     ]
 
     def as_dict(self):

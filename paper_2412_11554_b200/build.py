@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libaccord.so")
-SOURCES = ["api.cpp", "kernels.cu", "gemm_simt.cu", "gemm_tc.cu", "postproc.cu", "spmm_tma.cu"]
+SOURCES = ["api.cpp", "kernels.cu", "gemm_simt.cu", "gemm_tc.cu", "postproc.cu", "spmm_tma.cu",
+           "quant_i8.cu"]
 HEADERS = ["accord_internal.h", "tc_ptx.cuh"]
 
 NVCC_FLAGS = [

@@ -108,6 +108,10 @@ struct EpiParams {            // candidate rule of the fused epilogue (SURVEY P1
   const float* row_B;         // ||y_i||
   const float2* col_sd;       // (||x_k|| + ||x_k - bf16(x_k)||, ||x_k - bf16(x_k)||)
   float gamma;                // accumulation-error factor
+  // I8_FILTER only: y^_i = row_scale[i] q_i, x^_k = blk_scale[k / 256] q_k
+  // (row_A / row_B / col_sd then hold the int8 quantisation errors)
+  const float* row_scale;
+  const float* blk_scale;
   int exact_cols;             // 1: re-test tile-test survivors with their own column's bound
   // Omega is exactly I (the first iteration of a solve), so G = X^T X / n is
   // symmetric and each off-diagonal tile pair runs once, its survivors (i,k)
@@ -352,6 +356,16 @@ int launch_gemm_simt(int dtype, const void* Y, const void* Xt, int64_t ldk, int6
                      const EpiParams& ep, const OmegaView& om, const PoolView& pool,
                      cudaStream_t st);
 
+// int8 operands of the I8_FILTER GEMM and its bound constants (quant_i8.cu).
+// Y: per-row scale; rows [0, rows) of Y (f32, stride ldk) -> Yq, scale, A = ||e||, B = ||y||.
+int launch_quant_y_i8(int64_t rows, int64_t n, int64_t ldk, const float* Y, int8_t* Yq,
+                      float* scale, float* rA, float* rB, cudaStream_t st);
+// X^T: per-256-row block scale -> Xq, blk_scale[rows/256], col_sd[k] = (C + D, D);
+// rows [row0, row0 + nrow) also as per-row scale / D / C into rs, rA, rB (optional).
+int launch_quant_x_i8(int64_t rows, int64_t n, int64_t ldk, const float* Xt, int8_t* Xq,
+                      float* blk_scale, float2* col_sd, int64_t row0, int64_t nrow, float* rs,
+                      float* rA, float* rB, cudaStream_t st);
+
 // tcgen05 split-bf16 GEMM + fused epilogue (gemm_tc.cu).
 struct TcGemmPlan;   // opaque: tensor maps for both Y buffers
 TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
@@ -362,17 +376,24 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                            std::string* err);
 void tc_plan_destroy(TcGemmPlan*);
 // per-256-column maxima of the filter's column constants (after launch_col_norms)
-int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st);
+int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st,
+                          bool i8 = false);
 int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs
 // A operand idx 2 = this rank's rows of X^T_hi (the Omega = I operand of the
 // lambda_max pass); rows_pad rows from `hi`
 bool tc_plan_set_a(TcGemmPlan* plan, int idx, const __nv_bfloat16* hi, int64_t rows_pad,
                    std::string* err);
+// I8_FILTER operands: the two int8 Y buffers and int8 X^T (pk_pad / xrows_pad
+// x ldk bytes, K-major); idx 2 of the A maps = an override (lambda_max)
+bool tc_plan_set_i8(TcGemmPlan* plan, const int8_t* Yq0, const int8_t* Yq1, const int8_t* Xq,
+                    int64_t xrows_pad, float2* blk_q /* [p_pad/256], zeroed */, std::string* err);
+bool tc_plan_set_a_i8(TcGemmPlan* plan, int idx, const int8_t* q, int64_t rows_pad,
+                      std::string* err);
 // B operand idx 1/2 = ring buffers of the sharded mode (rows_pad x ldk bf16)
 bool tc_plan_set_b(TcGemmPlan* plan, int idx, const __nv_bfloat16* hi, const __nv_bfloat16* lo,
                    int64_t rows_pad, std::string* err);
 // columns [ep.col_base, ep.col_end) against B operand `bsel`
-int launch_gemm_tc(TcGemmPlan* plan, int mode /* accord_gemm: BF16X3 or BF16_FILTER */,
+int launch_gemm_tc(TcGemmPlan* plan, int mode /* accord_gemm: BF16X3, BF16_FILTER, I8_FILTER */,
                    int ybuf, int bsel, int sm_count, const EpiParams& ep,
                    const OmegaView& om, const PoolView& pool, cudaStream_t st);
 bool tc_supported(int cc_major, int cc_minor);

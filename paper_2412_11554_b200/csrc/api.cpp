@@ -204,6 +204,21 @@ struct accord_ctx {
   float* row_B[2] = {nullptr, nullptr};   // ||y_i||
   float2* col_sd = nullptr;               // per-column constants of the filter bound
   int cur = 0;
+  // int8 GEMM operands (I8_FILTER, or AUTO's adaptive switch; gemm stays
+  // BF16_FILTER internally: the same certified-filter pipeline)
+  bool i8 = false;                         // int8 operands allocated
+  bool i8_force = false;                   // I8_FILTER requested: every GEMM in int8
+  bool i8_on = false;                      // the next GEMM in int8
+  bool i8_last = false;                    // the last GEMM ran in int8 (filter audit)
+  double i8_at = 48.0, i8_off = 384.0;     // AUTO: on at |C|/p <= i8_at (bf16), off above i8_off
+  int64_t gemm_launches_i8 = 0;
+  float2* col_sd_q = nullptr;              // int8 column constants of the bound
+  float2* blk_q = nullptr;                 // their 256-column tile maxima
+  int8_t* Xq = nullptr;                    // X^T int8, block scale per 256 variables
+  float* xq_scale = nullptr;               // [p_pad / 256]
+  int8_t* Yq[2] = {nullptr, nullptr};      // Y int8, per-row scale (quantised before each GEMM)
+  float *yq_s[2] = {}, *yq_A[2] = {}, *yq_B[2] = {};
+  float *xr_s = nullptr, *xr_A = nullptr, *xr_B = nullptr;   // local X^T rows as an A operand
 
   int64_t cap = 0;  // entries of pool / C / keys / Omega arrays
   int64_t* om_ptr = nullptr;
@@ -734,10 +749,15 @@ void validate(const accord_init_params* prm) {
   if (shard && prm->comm == ACCORD_COMM_HOST && !prm->sendrecv)
     bad("x_sharded with the host communicator needs a sendrecv callback");
 
-  if (prm->gemm < ACCORD_GEMM_AUTO || prm->gemm > ACCORD_GEMM_BF16_FILTER) bad("bad gemm kind");
+  if (prm->gemm < ACCORD_GEMM_AUTO || prm->gemm > ACCORD_GEMM_I8_FILTER) bad("bad gemm kind");
   if (prm->dtype == ACCORD_F64 &&
-      (prm->gemm == ACCORD_GEMM_BF16X3 || prm->gemm == ACCORD_GEMM_BF16_FILTER))
+      (prm->gemm == ACCORD_GEMM_BF16X3 || prm->gemm == ACCORD_GEMM_BF16_FILTER ||
+       prm->gemm == ACCORD_GEMM_I8_FILTER))
     bad("tensor-core GEMM kinds need dtype F32");
+  if (prm->gemm == ACCORD_GEMM_I8_FILTER && shard)
+    bad("I8_FILTER needs X replicated (x_sharded uses BF16_FILTER)");
+  if (prm->gemm == ACCORD_GEMM_I8_FILTER && prm->n >= 133000)
+    bad("I8_FILTER needs n < 133000 (exact s32 accumulation)");
 }
 
 // Default candidate-pool capacity (entries): the first iteration (G = S) has
@@ -755,6 +775,20 @@ int64_t default_capacity(int64_t pk, int64_t p) {
 // no rank's slab exceeds max(p_k, ceil(p / world)) rows, and the per-iteration
 // scratch of hub rows (work items split at kItemEntries) is reserved for
 // 64 + p_k / 64 split slots.
+// The GEMM kind a create resolves to (AUTO: F32 on sm_100 -> the certified
+// filter, I8 operands unless X is sharded; else SIMT).
+// *i8_ops: int8 operands are allocated (I8_FILTER, or AUTO's adaptive
+// bf16 -> int8 switch; ACCORD_AUTO_GEMM=bf16 turns the switch off).
+int resolve_gemm(const accord_init_params* prm, bool tc_ok, bool* i8_ops) {
+  const bool sharded = prm->x_sharded && prm->world > 1;
+  *i8_ops = prm->gemm == ACCORD_GEMM_I8_FILTER;
+  if (prm->gemm != ACCORD_GEMM_AUTO) return prm->gemm;
+  if (prm->dtype != ACCORD_F32 || !tc_ok) return ACCORD_GEMM_SIMT;
+  const char* e = std::getenv("ACCORD_AUTO_GEMM");   // A-B: "bf16" = no int8 switch
+  *i8_ops = !sharded && !(e && std::strcmp(e, "bf16") == 0);
+  return ACCORD_GEMM_BF16_FILTER;
+}
+
 struct Footprint {
   size_t total = 0, transient = 0;
   int64_t cap = 0;
@@ -766,12 +800,12 @@ Footprint footprint(const accord_init_params* prm) {
   const int64_t ldk = round_up(n, kKPad), p_pad = round_up(p, kRowPad),
                 pk_pad = round_up(pk, kRowPad);
   const size_t T = prm->dtype == ACCORD_F64 ? 8 : 4;
-  int gemm = prm->gemm;
-  if (gemm == ACCORD_GEMM_AUTO)
-    gemm = prm->dtype == ACCORD_F32 ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_SIMT;
-  const bool x3 = gemm == ACCORD_GEMM_BF16X3, filt = gemm == ACCORD_GEMM_BF16_FILTER,
-             tc = x3 || filt;
   const bool sharded = prm->x_sharded && prm->world > 1;
+  bool i8 = false;
+  const int gemm = resolve_gemm(prm, true, &i8);
+  const bool x3 = gemm == ACCORD_GEMM_BF16X3,
+             filt = gemm == ACCORD_GEMM_BF16_FILTER || gemm == ACCORD_GEMM_I8_FILTER,
+             tc = x3 || filt;
   const int64_t pv = sharded ? pk : p;
   const int64_t xrows_pad = sharded ? pk_pad : p_pad;
   size_t a = 0;
@@ -794,6 +828,12 @@ Footprint footprint(const accord_init_params* prm) {
     a += 4 * R(pk * 4);                                // row_A, row_B (x2)
     if (filt) a += R(p * 8);                           // col_sd
     a += R((p_pad / kRowPad) * 8);                     // tile maxima of col_sd
+  }
+  if (i8) {
+    a += R((size_t)xrows_pad * ldk) + R((p_pad / kRowPad) * 4);   // X^T int8, block scales
+    a += R(p * 8) + R((p_pad / kRowPad) * 8);                     // int8 col_sd, tile maxima
+    a += 2 * R((size_t)pk_pad * ldk) + 6 * R(pk * 4);            // Y int8 (x2), row consts
+    a += 3 * R(pk * 4);                                          // local X^T rows' consts
   }
   if (sharded) {
     const int64_t rr = std::max(pk_pad, round_up((p + prm->world - 1) / prm->world, kRowPad));
@@ -994,10 +1034,13 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   const bool tc_ok = tc_supported(c->cc_major, c->cc_minor);
   // F32 on sm_100: the certified bf16 filter for any n (the refine streams
   // X^T rows in 4 KB chunks; the filter bound's gamma grows with n)
-  if (prm->gemm == ACCORD_GEMM_AUTO)
-    c->gemm = (c->dtype == ACCORD_F32 && tc_ok) ? ACCORD_GEMM_BF16_FILTER : ACCORD_GEMM_SIMT;
-  else
-    c->gemm = prm->gemm;
+  c->gemm = resolve_gemm(prm, tc_ok, &c->i8);
+  if (c->gemm == ACCORD_GEMM_I8_FILTER) {   // the filter pipeline with int8 operands
+    c->gemm = ACCORD_GEMM_BF16_FILTER;
+    c->i8_force = c->i8_on = true;
+  }
+  if (const char* e = std::getenv("ACCORD_I8_AT")) c->i8_at = std::atof(e);     // tuning
+  if (const char* e = std::getenv("ACCORD_I8_OFF")) c->i8_off = std::atof(e);
   const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
   if (tc && !tc_ok) throw Fail{ACCORD_E_UNSUPPORTED, "tcgen05 GEMM needs an sm_100 device"};
   if (tc && prm->x_sharded && prm->world > 1 && prm->row_begin % kRowPad != 0)
@@ -1173,6 +1216,30 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
       c->col_sd = c->dalloc<float2>(c->p);
       const int64_t off = c->sharded ? c->r0 : 0;
       c->launches += launch_col_norms(pv, c->ldk, (const float*)c->Xt, c->col_sd + off, c->st);
+      if (c->i8) {
+        // int8 X^T (block scale per 256 variables) and the bound's column
+        // constants of that quantisation; the local rows' constants too (the
+        // A operand of the lambda_max pass at Omega = I)
+        c->col_sd_q = c->dalloc<float2>(c->p);
+        c->blk_q = c->dalloc<float2>(c->p_pad / kRowPad);
+        CK(cudaMemsetAsync(c->blk_q, 0, (c->p_pad / kRowPad) * sizeof(float2), c->st));
+        c->Xq = c->dalloc<int8_t>((size_t)c->xrows_pad * c->ldk);
+        CK(cudaMemsetAsync(c->Xq, 0, (size_t)c->xrows_pad * c->ldk, c->st));
+        c->xq_scale = c->dalloc<float>(c->p_pad / kRowPad);
+        c->xr_s = c->dalloc<float>(c->pk);
+        c->xr_A = c->dalloc<float>(c->pk);
+        c->xr_B = c->dalloc<float>(c->pk);
+        c->launches += launch_quant_x_i8(pv, c->n, c->ldk, (const float*)c->Xt, c->Xq,
+                                         c->xq_scale, c->col_sd_q, c->r0, c->pk, c->xr_s, c->xr_A,
+                                         c->xr_B, c->st);
+        for (int b = 0; b < 2; ++b) {
+          c->Yq[b] = c->dalloc<int8_t>((size_t)c->pk_pad * c->ldk);
+          CK(cudaMemsetAsync(c->Yq[b], 0, (size_t)c->pk_pad * c->ldk, c->st));
+          c->yq_s[b] = c->dalloc<float>(c->pk);
+          c->yq_A[b] = c->dalloc<float>(c->pk);
+          c->yq_B[b] = c->dalloc<float>(c->pk);
+        }
+      }
       if (c->sharded) gather_col_sd(c);
     }
     std::string e;
@@ -1182,7 +1249,10 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
                              x3 ? c->Ylo[1] : c->Yhi[1], c->pk_pad, c->Xhi,
                              x3 ? c->Xlo : c->Xhi, c->xrows_pad, c->p_pad, c->n, c->ldk, bsd, &e);
     if (!c->plan) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
+    if (c->i8 && !tc_plan_set_i8(c->plan, c->Yq[0], c->Yq[1], c->Xq, c->xrows_pad, c->blk_q, &e))
+      throw Fail{ACCORD_E_CUDA, "tensor map (int8): " + e};
     if (filt) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
+    if (c->i8) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd_q, c->p, c->st, true);
   }
 
   phase("operands (Y, bf16 copies, column norms, tensor maps)");
@@ -1477,6 +1547,7 @@ void mirror_append(accord_ctx* c, int64_t used, int64_t needc) {
 struct GradOverride {
   int ybuf;                 // plan A map
   const float *row_A, *row_B;
+  const float* row_scale;   // I8_FILTER: per-row scale of the A operand
   OmegaView om;
   double lam_cand;
   unsigned int* max_out;    // != NULL: max-reduce pass only (no candidates)
@@ -1516,6 +1587,16 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
                     c->gemm == ACCORD_GEMM_BF16_FILTER && !std::getenv("ACCORD_GEMM_NOSYM");
   bool exchanged = false;
   if (sym2 && !c->mir_row) grow_mirror(c, std::max<int64_t>(c->pk * 64, 1 << 20));
+  // int8 GEMM (I8_FILTER, or AUTO once |C| is small; an override pass --
+  // lambda_max at Omega = I -- whenever int8 operands exist): the int8 copy of
+  // the current Y and its bound constants (a read of Y per GEMM: ~1 ms at c5)
+  const bool use_i8 = c->i8 && (ov ? true : c->i8_on);
+  c->i8_last = use_i8;
+  st.gemm_i8 = use_i8 ? 1 : 0;
+  if (use_i8 && !ov)
+    c->launches += launch_quant_y_i8(c->pk, c->n, c->ldk, (const float*)c->Y[c->cur],
+                                     c->Yq[c->cur], c->yq_s[c->cur], c->yq_A[c->cur],
+                                     c->yq_B[c->cur], S);
   for (;;) {
     CK(cudaMemsetAsync(c->row_cnt, 0, c->pk * 4, S));
     CK(cudaMemsetAsync(c->chunk_fill, 0, c->nchunks * 8, S));
@@ -1541,6 +1622,13 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
     ep.col_sd = c->col_sd;
     // fp32-accumulation term of the filter bound: (n/16 + 17) * 2^-22 * sum|y^ x^|
     ep.gamma = (float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
+    if (use_i8) {   // exact s32 accumulation: no accumulation term
+      ep.gamma = 0.f;
+      ep.row_A = c->yq_A[c->cur];
+      ep.row_B = c->yq_B[c->cur];
+      ep.row_scale = c->yq_s[c->cur];
+      ep.blk_scale = c->xq_scale;
+    }
     ep.exact_cols = std::getenv("ACCORD_FILTER_EXACT") != nullptr;   // A-B diagnostic
     // Omega = I on one rank: G = S is symmetric, half the tiles (ACCORD_GEMM_NOSYM: off)
     ep.sym = c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && c->world == 1 &&
@@ -1563,6 +1651,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       ybuf = ov->ybuf;
       ep.row_A = ov->row_A;
       ep.row_B = ov->row_B;
+      ep.row_scale = ov->row_scale;
       ep.lam_cand = ov->lam_cand;
       ep.max_out = ov->max_out;
       ep.sym = ov->sym;
@@ -1576,8 +1665,9 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       ep.col_base = v0;
       ep.col_end = v1;
       if (tc) {
-        const int l = launch_gemm_tc(c->plan, c->gemm, ybuf, bsel, c->sm_count, ep, omv,
-                                     pool_view(c), S);
+        const int l = launch_gemm_tc(c->plan, use_i8 ? (int)ACCORD_GEMM_I8_FILTER : c->gemm, ybuf,
+                                     bsel, c->sm_count, ep, omv, pool_view(c), S);
+        if (use_i8) c->gemm_launches_i8++;
         if (l < 0) throw Fail{ACCORD_E_CUDA, "tcgen05 GEMM launch failed"};
         c->launches += l;
       } else {
@@ -1885,7 +1975,14 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   st.ms_total = ev_ms(c, 0, 7);
   TR_flush(c);
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
-  if (c->plan && c->col_sd && !c->sharded && (double)st.n_cand <= c->x_drop_at * (double)c->p) {
+  // AUTO's operand switch (global |C|, so every rank takes the same
+  // decision): int8 once the bf16 filter's |C| / p is small, back to bf16 if
+  // the int8 filter's grows large
+  if (c->i8 && !c->i8_force && !c->refit)
+    c->i8_on = c->i8_on ? (double)st.n_cand <= c->i8_off * (double)c->p
+                        : (double)st.n_cand <= c->i8_at * (double)c->p;
+  if (c->plan && c->col_sd && !c->sharded && !c->i8 &&
+      (double)st.n_cand <= c->x_drop_at * (double)c->p) {
     if (c->x_drop != c->x_drop_target) set_x_width(c, c->x_drop_target);
     c->y_drop = c->y_drop_target;   // from the next Y on (each Y carries its own row norms)
   }
@@ -1933,6 +2030,8 @@ double lambda_max_impl(accord_ctx* c) {
     std::string e;
     const __nv_bfloat16* xh = c->Xhi + (size_t)xrow0 * c->ldk;
     if (!tc_plan_set_a(c->plan, 2, xh, c->pk_pad, &e)) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
+    if (c->i8 && !tc_plan_set_a_i8(c->plan, 2, c->Xq + (size_t)xrow0 * c->ldk, c->pk_pad, &e))
+      throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
     c->plan_a_x = true;
   }
   float* rA = c->dalloc<float>(std::max<int64_t>(c->pk, 1));
@@ -1946,7 +2045,9 @@ double lambda_max_impl(accord_ctx* c) {
   CK(cudaMemsetAsync(eptr, 0, (c->pk + 1) * 8, S));
   CK(cudaMemsetAsync(dmax, 0, 4, S));
   c->launches += launch_row_ab(c->pk, c->ldk, (const float*)xrows, rA, rB, S, c->x_drop);
-  GradOverride ov{2, rA, rB, OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax,
+  // I8_FILTER: the int8 X^T rows with their block scales (quant_i8.cu)
+  GradOverride ov{2, c->i8 ? c->xr_A : rA, c->i8 ? c->xr_B : rB, c->i8 ? c->xr_s : nullptr,
+                  OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax,
                   c->world == 1 && !c->sharded && c->r0 == 0 && c->pk == c->p &&
                       !std::getenv("ACCORD_GEMM_NOSYM")};
   accord_iter_stats st{};
@@ -2533,12 +2634,18 @@ accord_status accord_filter_audit(accord_ctx* c, float* acc, int64_t ld, float* 
     if (y)
       CK(cudaMemcpy2DAsync(y, ldy * 4, c->Y[c->cur], c->ldk * 4, c->n * 4, c->pk,
                            cudaMemcpyDeviceToDevice, S));
+    const bool q = c->i8_last;   // the audited GEMM ran in int8: its constants, gamma = 0
     if (row_ab) {
-      CK(cudaMemcpyAsync(row_ab, c->row_A[c->cur], c->pk * 4, cudaMemcpyDeviceToHost, S));
-      CK(cudaMemcpyAsync(row_ab + c->pk, c->row_B[c->cur], c->pk * 4, cudaMemcpyDeviceToHost, S));
+      CK(cudaMemcpyAsync(row_ab, q ? c->yq_A[c->cur] : c->row_A[c->cur], c->pk * 4,
+                         cudaMemcpyDeviceToHost, S));
+      CK(cudaMemcpyAsync(row_ab + c->pk, q ? c->yq_B[c->cur] : c->row_B[c->cur], c->pk * 4,
+                         cudaMemcpyDeviceToHost, S));
     }
-    if (col_sd) CK(cudaMemcpyAsync(col_sd, c->col_sd, c->p * 8, cudaMemcpyDeviceToHost, S));
-    if (gamma) *gamma = (double)(float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
+    if (col_sd)
+      CK(cudaMemcpyAsync(col_sd, q ? c->col_sd_q : c->col_sd, c->p * 8, cudaMemcpyDeviceToHost, S));
+    if (gamma)
+      *gamma = q ? 0.0
+                     : (double)(float)(((double)c->ldk / 16.0 + 17.0) * std::ldexp(1.0, -22));
     int64_t nc = 0;
     CK(cudaMemcpyAsync(&nc, c->c_ptr + c->pk, 8, cudaMemcpyDeviceToHost, S));
     csync(c, S);
@@ -2581,7 +2688,8 @@ accord_status accord_get_info(accord_ctx* c, accord_info* info) {
   info->tau0 = c->tau0;
   info->beta = c->beta;
   info->dtype = c->dtype;
-  info->gemm = c->gemm;
+  info->gemm = (c->i8_force || c->gemm_launches_i8 > 0) ? (int)ACCORD_GEMM_I8_FILTER : c->gemm;
+  info->gemm_launches_i8 = c->gemm_launches_i8;
   info->sm_count = c->sm_count;
   info->cc_major = c->cc_major;
   info->cc_minor = c->cc_minor;

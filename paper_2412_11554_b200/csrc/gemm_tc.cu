@@ -17,6 +17,17 @@
 //   kMode 0, BF16X3: operands split hi = bf16(v), lo = bf16(v - hi); three
 //     MMA passes hi*hi + hi*lo + lo*hi into the same fp32 accumulator; values
 //     come from TMEM (relative product error ~2^-16).
+//   kMode 2, I8_FILTER: the same certified filter with int8 operands
+//     (kind::i8, twice the bf16 MMA rate, half the operand bytes): Y rows
+//     quantised with a per-row scale a_i, X^T rows with a per-256-row block
+//     scale b_K, so y^ = a_i q_i and x^ = b_K q_k. The s32 accumulator is
+//     EXACT (|acc| <= n 127^2 < 2^31 for n < 133,000), so a_i b_K acc =
+//     <y^_i, x^_k> exactly and the bound needs no accumulation model:
+//     |<y^,x^> - <y,x>| = |e_y.x^ + y.e_x| <= A_i (C_k + D_k) + B_i D_k with
+//     A = ||e_y||, B = ||y||, C = ||x||, D = ||e_x|| (the actual quantisation
+//     errors, quant_i8.cu). The epilogue turns n lambda - n delta into an
+//     integer threshold per row and tile (double arithmetic, rounded down)
+//     and tests |acc| against it with integer min/max.
 //
 // Structure (persistent, one 256 x 256 tile per CTA pair per step):
 //   cluster of 2 CTAs; CTA r holds rows [128r, 128r+128) of the A tile (Y)
@@ -61,7 +72,7 @@ namespace {
 constexpr int BM = 128;                         // rows of A per CTA (256 per pair)
 constexpr int BN = 256;                         // columns of the tile (N of one MMA)
 constexpr int BNH = BN / 2;                     // rows of B held per CTA
-constexpr int BK = 64;                          // bf16 elements = 128-B rows
+constexpr int BK = 64;                          // bf16 elements = 128-B rows (128 int8)
 constexpr int kAccStages = 2;
 constexpr int kTmemCols = 512;
 constexpr uint32_t kTileA = BM * BK * 2;        // 16 KB
@@ -71,6 +82,7 @@ constexpr int kEpiWarp0 = 4;
 
 template <int kMode, int kStagesT> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
+  static constexpr int kBKe = kMode == 2 ? 2 * BK : BK;                  // elements per 128-B row
   static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 64 / 32 KB
   static constexpr int kStages = kStagesT;
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
@@ -207,7 +219,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const Sched sched(num_m, num_n, group_n, unit_n, kMode == 1 ? ep.sym : 0, ep.mt0, ep.nt);
+  const Sched sched(num_m, num_n, group_n, unit_n, kMode != 0 ? ep.sym : 0, ep.mt0, ep.nt);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&mA_hi);
@@ -247,7 +259,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           uint8_t* s = smem + stage * kStageBytes;
           const uint32_t fb_local = tc::smem_u32(&full[stage]);
           const uint32_t fb = tc::mapa_shared(fb_local, 0);                  // leader's barrier
-          const int kx = kb * BK;
+          const int kx = kb * Cfg<kMode, kStagesT>::kBKe;
           if (tc::elect_one()) {
             if (leader) tc::mbar_arrive_expect_tx(fb_local, 2 * kStageBytes);   // both CTAs' bytes
             // stage layout: A_hi | B_hi | (A_lo | B_lo)
@@ -274,7 +286,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     // The whole warp runs the loop (so the descriptors stay warp-uniform and
     // live in uniform registers); one elected lane issues the MMAs/commits.
     if (leader) {
-      constexpr uint32_t idesc = tc::idesc_bf16_f32(2 * BM, BN);
+      constexpr uint32_t idesc =
+          kMode == 2 ? tc::idesc_s8_s32(2 * BM, BN) : tc::idesc_bf16_f32(2 * BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -298,9 +311,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               if (kk >= nkk) break;
-              const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 = 32 B along K
+              const uint64_t off = (uint64_t)(kk * 32) >> 4;   // 16 bf16 / 32 int8 = 32 B along K
               const uint32_t accum = (kb | kk) != 0;
-              if (dbg != 2) tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
+              if constexpr (kMode == 2) {
+                if (dbg != 2) tc::mma_i8<2>(d, a_hi + off, b_hi + off, idesc, accum);
+              } else {
+                if (dbg != 2) tc::mma_bf16<2>(d, a_hi + off, b_hi + off, idesc, accum);
+              }
               if constexpr (kMode == 0) {
                 tc::mma_bf16<2>(d, a_hi + off, b_lo + off, idesc, 1);
                 tc::mma_bf16<2>(d, a_lo + off, b_hi + off, idesc, 1);
@@ -321,6 +338,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     // ============================ epilogue (both CTAs) ====================
     const int q = warp - kEpiWarp0;                 // TMEM lane quarter (= warp % 4)
     const float thr = (float)(ep.lam_cand / ep.inv_n);   // n * lambda
+    const double thr_d = ep.lam_cand / ep.inv_n;
     const float inv_nf = (float)ep.inv_n;
     const float gam = ep.gamma;
     const float* omv = (const float*)om.val;
@@ -335,6 +353,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     bool row_ok = false;
     int32_t nxt = INT_MAX;
     float r1 = 0.f, Bn = 0.f;
+    double asc = 0.0;                               // kMode 2: a_i (row scale)
     float wmax = 0.f;                               // kDiag == 2
     for (TileIt it(sched, cluster, nclusters); it.ok; it.next()) {
       const int n0 = (int)ep.col_base + it.n() * BN;   // global column of the tile
@@ -366,12 +385,34 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             r1 = (A + gam * (A + B)) * 1.0625f;
             Bn = B * 1.0625f;
           }
+          if constexpr (kMode == 2) {
+            // exact accumulation: n*delta_ik = A_i s_k + B_i D_k (the norms
+            // are rounded up; the tile threshold is evaluated in double)
+            r1 = ep.row_A[r];
+            Bn = ep.row_B[r];
+            asc = (double)ep.row_scale[r];
+          }
         }
       }
       float tfast = thr;
+      int tint = -1;                             // kMode 2: emit iff |acc| > tint
+      double sc = 0.0, ndel = 0.0;               // kMode 2: a_i b_K, tile bound n*delta
       if (kMode == 1 && row_ok) {
         const float2 mx = blk_sdmax[n0 / BN];    // tile max of the column constants
         tfast = thr - fmaf(r1, mx.x, Bn * mx.y);
+      }
+      if (kMode == 2 && row_ok) {
+        // |acc| a_i b_K > n lambda - n delta  <=>  |acc| > t; the integer acc
+        // passes iff |acc| > floor(t') for any t' <= t: t is taken 1e-12
+        // relative and 1 unit low (double evaluation of t itself)
+        const float2 mx = blk_sdmax[n0 / BN];
+        ndel = fma((double)r1, (double)mx.x, (double)Bn * (double)mx.y) * (1.0 + 1e-9);
+        sc = asc * (double)ep.blk_scale[n0 / BN];
+        const double t = (thr_d - ndel) / sc;
+        if (!(t > 0.0)) tint = -1;
+        else if (t >= 2.0e9) tint = INT_MAX;
+        else tint = (int)floor(t * (1.0 - 1e-12)) - 1;
+        if (tint < -1) tint = -1;
       }
       tc::mbar_wait(tc::smem_u32(&tfull[acc]), acc_phase);
       tc::tc_fence_after();
@@ -425,9 +466,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               for (int c = 0; c < 32; ++c) {
                 const int64_t k = c0 + c;
                 if (k < col_end) {
-                  ep.audit_acc[r * ep.audit_ld + k] = __uint_as_float(v[c]);
+                  // kMode 2: the accumulator in the units of n G (a_i b_K acc)
+                  const float a = kMode == 2 ? (float)((double)(int)v[c] * sc)
+                                             : __uint_as_float(v[c]);
+                  ep.audit_acc[r * ep.audit_ld + k] = a;
                   if (mir && k >= ep.r0 && k < ep.r0 + ep.pk)
-                    ep.audit_acc[(k - ep.r0) * ep.audit_ld + gi] = __uint_as_float(v[c]);
+                    ep.audit_acc[(k - ep.r0) * ep.audit_ld + gi] = a;
                 }
               }
             }
@@ -436,37 +480,65 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             // max |acc| off the diagonal minus this row's tile bound n*delta
             // (= thr - tfast): a lower bound on n |G_ik| of the maximiser
             if (row_ok) {
-              float mm = 0.f;
+              if constexpr (kMode == 2) {
+                int mi = 0;
 #pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (c0 + c < col_end && c0 + c != gi) mm = fmaxf(mm, fabsf(__uint_as_float(v[c])));
-              wmax = fmaxf(wmax, mm - (thr - tfast));
+                for (int c = 0; c < 32; ++c)
+                  if (c0 + c < col_end && c0 + c != gi) mi = max(mi, abs((int)v[c]));
+                wmax = fmaxf(wmax, __double2float_rd((double)mi * sc - ndel));
+              } else {
+                float mm = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  if (c0 + c < col_end && c0 + c != gi) mm = fmaxf(mm, fabsf(__uint_as_float(v[c])));
+                wmax = fmaxf(wmax, mm - (thr - tfast));
+              }
             }
             continue;
           }
           // common case first, one vote per 32 columns: no lane has an |acc|
           // above the tile's threshold (one FMNMX3 per two values), its
           // diagonal or a support entry of Omega in these columns
-          float m0 = 0.f, m1 = 0.f;
-          if constexpr (kFast) {
+          bool over;
+          if constexpr (kMode == 2) {
+            // integer max / min over the 32 accumulators (3-input VIMNMX)
+            int hi = (int)v[0], lo = (int)v[0];
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
-              m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
+            for (int c = 1; c < 31; c += 2) {
+              hi = __vimax3_s32(hi, (int)v[c], (int)v[c + 1]);
+              lo = __vimin3_s32(lo, (int)v[c], (int)v[c + 1]);
             }
+            hi = max(hi, (int)v[31]);
+            lo = min(lo, (int)v[31]);
+            over = hi > tint || lo < -tint;
           } else {
-            m0 = INFINITY;
+            float m0 = 0.f, m1 = 0.f;
+            if constexpr (kFast) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                m0 = fmaxf(m0, fabsf(__uint_as_float(v[c])));
+                m1 = fmaxf(m1, fabsf(__uint_as_float(v[c + 1])));
+              }
+            } else {
+              m0 = INFINITY;
+            }
+            over = fmaxf(m0, m1) > tfast;
           }
-          const bool over = fmaxf(m0, m1) > tfast;
           const bool hot =
               row_ok && (over || (kMode == 0 && (nxt < c0 + 32 || (gi >= c0 && gi < c0 + 32))));
           if (!__any_sync(0xffffffffu, hot)) continue;
           uint32_t mask = 0, sup = 0;
           if (hot) {
             if (over) {
+              if constexpr (kMode == 2) {
 #pragma unroll
-              for (int c = 0; c < 32; ++c)
-                mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
+                for (int c = 0; c < 32; ++c)
+                  mask |= (abs((int)v[c]) > tint ? 1u : 0u) << c;
+              } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  mask |= (fabsf(__uint_as_float(v[c])) > tfast ? 1u : 0u) << c;
+              }
             }
             if (kMode == 1 && ep.exact_cols && mask) {
               // exact per-column bound for the survivors of the tile-level test
@@ -499,7 +571,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           // this rank's (into the pool) or another rank's (into the mirror
           // buffer, sent after the GEMM); a 32-column chunk never straddles a
           // rank boundary (multiples of 256)
-          const bool mirror = kMode == 1 && sched.sym && it.n() != sched.mt0 + it.m;
+          const bool mirror = kMode != 0 && sched.sym && it.n() != sched.mt0 + it.m;
           const bool mir_local = mirror && (int64_t)c0 >= ep.r0 && (int64_t)c0 < ep.r0 + ep.pk;
           const bool mir_remote = kDiag == 3 && mirror && !mir_local;
           const int cnt = __popc(mask) << (mir_local ? 1 : 0);
@@ -537,7 +609,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
             base = __shfl_sync(0xffffffffu, base, 0);
             rpos = (int64_t)base + rincl - rc;
           }
-          if constexpr (kMode == 1) {
+          if constexpr (kMode != 0) {
             // candidate positions only: the exact values come from the refine
             // SDDMM and omega_ik from a lookup in Omega's CSR after the sort
             // (no dependent load of Omega's values on the epilogue's path)
@@ -648,17 +720,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // rows x kdim bf16 (row stride ldk elements); the box runs past kdim into TMA
 // zero fill, so the padding columns [kdim, ldk) are never read
 bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t kdim, int64_t ldk,
-              int box_rows, std::string* err) {
+              int box_rows, std::string* err, bool i8 = false) {
   auto fn = encode_fn();
   if (!fn) {
     *err = "cuTensorMapEncodeTiled unavailable";
     return false;
   }
   cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ldk * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  // int8: 128 elements per 128-B swizzle row (the same bytes as 64 bf16)
+  cuuint64_t strides[1] = {(cuuint64_t)(ldk * (i8 ? 1 : 2))};
+  cuuint32_t box[2] = {(cuuint32_t)(i8 ? 2 * BK : BK), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(m, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -676,6 +750,11 @@ struct TcGemmPlan {
   // A operand maps: [0], [1] = the two Y buffers, [2] = this rank's rows of
   // X^T_hi (Omega = I operand of the lambda_max pass, tc_plan_set_a)
   CUtensorMap a_hi[3], a_lo[3], b_hi[3], b_lo[3];
+  // I8_FILTER: A maps over the two int8 Y buffers (+ [2] = an override), B
+  // over int8 X^T
+  CUtensorMap a_q[3], b_q;
+  bool has_i8 = false;
+  float2* blk_q = nullptr;       // [p_pad / 256] tile maxima of the int8 constants
   int64_t pk_pad = 0, p_pad = 0, ldk = 0, kdim = 0;   // p_pad: padded column count (all p)
   float2* blk_sdmax = nullptr;   // [p_pad / 256] (BF16_FILTER; caller-owned, zeroed)
 };
@@ -724,6 +803,14 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true, 3>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg<2, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true, 1>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true, 2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true, 3>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2, 6>::kSmemBytes);
     attr_done(attr_seen);
   }
   return p;
@@ -741,9 +828,25 @@ bool tc_plan_set_b(TcGemmPlan* p, int idx, const __nv_bfloat16* hi, const __nv_b
          make_map(&p->b_lo[idx], lo, rows_pad, p->kdim, p->ldk, BNH, err);
 }
 
-int tc_plan_set_col_norms(TcGemmPlan* p, const float2* col_sd, int64_t pcols, cudaStream_t st) {
+bool tc_plan_set_i8(TcGemmPlan* p, const int8_t* Yq0, const int8_t* Yq1, const int8_t* Xq,
+                    int64_t xrows_pad, float2* blk_q, std::string* err) {
+  p->blk_q = blk_q;
+  p->has_i8 = make_map(&p->a_q[0], Yq0, p->pk_pad, p->kdim, p->ldk, BM, err, true) &&
+              make_map(&p->a_q[1], Yq1, p->pk_pad, p->kdim, p->ldk, BM, err, true) &&
+              make_map(&p->b_q, Xq, xrows_pad, p->kdim, p->ldk, BNH, err, true);
+  p->a_q[2] = p->a_q[0];
+  return p->has_i8;
+}
+
+bool tc_plan_set_a_i8(TcGemmPlan* p, int idx, const int8_t* q, int64_t rows_pad,
+                      std::string* err) {
+  return make_map(&p->a_q[idx], q, rows_pad, p->kdim, p->ldk, BM, err, true);
+}
+
+int tc_plan_set_col_norms(TcGemmPlan* p, const float2* col_sd, int64_t pcols, cudaStream_t st,
+                          bool i8) {
   const int nblk = (int)(p->p_pad / BN);
-  blk_max_kernel<<<nblk, 256, 0, st>>>(col_sd, pcols, nblk, p->blk_sdmax);
+  blk_max_kernel<<<nblk, 256, 0, st>>>(col_sd, pcols, nblk, i8 ? p->blk_q : p->blk_sdmax);
   return 1;
 }
 
@@ -764,8 +867,12 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   const int num_m = (int)(plan->pk_pad / (2 * BM));
   const int num_n = (int)((ep.col_end - ep.col_base + BN - 1) / BN);
   const int64_t kdim = plan->kdim;
-  const int num_kb = (int)((kdim + BK - 1) / BK);
-  const int kk_last = (int)((kdim - (int64_t)(num_kb - 1) * BK + 15) / 16);   // 1..4
+  const bool i8 = mode == ACCORD_GEMM_I8_FILTER;
+  if (i8 && !plan->has_i8) return -1;
+  const int bke = i8 ? 2 * BK : BK;                       // K elements per 128-B k-block
+  const int kmma = i8 ? 32 : 16;                          // K per MMA
+  const int num_kb = (int)((kdim + bke - 1) / bke);
+  const int kk_last = (int)((kdim - (int64_t)(num_kb - 1) * bke + kmma - 1) / kmma);   // 1..4
   const int grid = tc_grid_size(plan, sm_count);
   // A group of <= 64 N-blocks (<= 32 MB of X^T_hi at n = 1000) stays in L2;
   // units small enough that the per-cluster imbalance is <= ~6% of its work
@@ -792,7 +899,20 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
 #define ACCORD_TC_ARGS(bsel_lo)                                                               \
   plan->a_hi[ybuf], plan->a_lo[ybuf], plan->b_hi[bsel], bsel_lo, num_kb, kk_last, num_m,   \
       num_n, group_n, unit_n, dbg, l2hint, ep, plan->blk_sdmax, om, pool
-  if (mode == ACCORD_GEMM_BF16X3)
+#define ACCORD_TC_ARGS_I8                                                                    \
+  plan->a_q[ybuf], plan->a_q[ybuf], plan->b_q, plan->b_q, num_kb, kk_last, num_m, num_n,     \
+      group_n, unit_n, dbg, l2hint, ep, plan->blk_q, om, pool
+  if (i8) {
+    if (bsel != 0) return -1;   // no sharded-X ring in int8
+    if (ep.audit_acc)
+      gemm_tc_kernel<2, 6, true, 1><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+    else if (ep.max_out)
+      gemm_tc_kernel<2, 6, true, 2><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+    else if (ep.sym == 2)
+      gemm_tc_kernel<2, 6, true, 3><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+    else
+      gemm_tc_kernel<2, 6, true><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+  } else if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0, 3, true><<<grid, kThreads, Cfg<0, 3>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_lo[bsel]));
   else if (ep.audit_acc)
@@ -814,6 +934,7 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
     gemm_tc_kernel<1, 6, true><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_hi[bsel]));
 #undef ACCORD_TC_ARGS
+#undef ACCORD_TC_ARGS_I8
   return 1;
 }
 

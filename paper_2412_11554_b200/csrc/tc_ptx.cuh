@@ -167,6 +167,20 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint6
         : "memory");
 }
 
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::i8 (signed int8 inputs, exact s32
+// accumulate; K = 32 per instruction = 32 B, the same bytes as bf16 K16)
+template <int kGroup>
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  static_assert(kGroup == 2, "cta_group::2 only");
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Arrive on an mbarrier when all prior tcgen05.mma of this thread complete.
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -216,6 +230,15 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4)                      // D format F32      [4,6)
          | (1u << 7)                    // A format BF16     [7,10)
          | (1u << 10)                   // B format BF16     [10,13)
+         | ((uint32_t)(N >> 3) << 17)   // N >> 3            [17,23)
+         | ((uint32_t)(M >> 4) << 24);  // M >> 4            [24,29)
+}
+
+// Instruction descriptor: kind::i8, A/B = signed 8 bit, D = S32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_s8_s32(int M, int N) {
+  return (2u << 4)                      // D format S32      [4,6)
+         | (1u << 7)                    // A format signed   [7,10)
+         | (1u << 10)                   // B format signed   [10,13)
          | ((uint32_t)(N >> 3) << 17)   // N >> 3            [17,23)
          | ((uint32_t)(M >> 4) << 24);  // M >> 4            [24,29)
 }

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in decl if not hasattr(L, n)]
     assert not missing, missing
     assert set(decl) == set(A.EXPORTED)
-    assert A.lib().accord_abi_version() == 3
+    assert A.lib().accord_abi_version() == 4
 
 
 def test_status_strings_and_create_error_without_gpu():
@@ -65,6 +65,7 @@ int main(void) {
   P(accord_init_params, workspace) P(accord_init_params, workspace_bytes)
   P(accord_info, workspace_bytes) P(accord_info, workspace_high) P(accord_info, mirrored_sent)
   P(accord_iter_stats, nnz) P(accord_iter_stats, trials) P(accord_iter_stats, ms_total)
+  P(accord_iter_stats, gemm_i8) P(accord_info, gemm_launches_i8)
   P(accord_info, f) P(accord_info, device_bytes) P(accord_info, kernel_launches)
   return 0;
 }
@@ -150,13 +151,14 @@ def test_workspace_size_query_is_pure_and_accounts_the_layout():
     """accord_workspace_size without a GPU: config 5 needs
     X^T (4 GB f32) + its bf16 copy (2 GB) + Y x 2 (8 GB) + their bf16 copies
     (4 GB) + the pool at ~512 candidates per row (52 B per entry, 26.6 GB)
-    + the host-X staging (4 GB); monotone in the pool capacity; bad
-    parameters are rejected like accord_create."""
+    + the host-X staging (4 GB) + AUTO's int8 operands (X^T 1 GB, Y x 2
+    2 GB); monotone in the pool capacity; bad parameters are rejected like
+    accord_create."""
     st, b = _size(_prm(1000, 1000000))
     assert st == 0
     p, ldk = 1000000, 1024
     parts = p * ldk * 4 + p * ldk * 2 + 2 * p * ldk * 4 + 2 * p * ldk * 2 + 512 * p * 52 \
-        + 1000 * p * 4
+        + 1000 * p * 4 + 3 * p * ldk
     assert parts <= b <= parts * 1.05, (b, parts)
     st2, b2 = _size(_prm(1000, 1000000, x_on_device=1))
     assert st2 == 0 and b2 < b                       # no host staging
