@@ -386,7 +386,8 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
     if dist:
         dist.barrier()
     clocks = sampler.stop()
-    launches = solver.info()["kernel_launches"] - launches0
+    info1 = solver.info()
+    launches = info1["kernel_launches"] - launches0
     ms_gemm = float(np.mean([s["ms_gemm"] for s in stats]))
     per_rank = None
     if dist:
@@ -457,7 +458,14 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
     # the slowest rank's GEMM (max over ranks; rank 0's row block is the largest)
     achieved = 2.0 * pk0 * p * n / (ms_gemm_max / 1e3) / 1e12
     peak = float(pk_.get("bf16_tflops_sustained", pk_.get("bf16_tflops")))
-    i8 = info0["gemm"] == A.GEMM_I8_FILTER
+    # the GEMM kind of the TIMED steps (AUTO switches bf16 -> int8 once |C| is small)
+    n_i8 = sum(int(s_["gemm_i8"]) for s_ in stats)
+    i8 = n_i8 == len(stats) and n_i8 > 0
+    gkind = "i8_filter_tcgen05+sddmm" if i8 else (
+        "bf16_filter_tcgen05+sddmm" if n_i8 == 0 else "mixed")
+    gname = A.GEMM_NAMES[info0["gemm"]]
+    if info1["gemm_launches_i8"] > 0 and info0["gemm"] != A.GEMM_I8_FILTER:
+        gname = "adaptive: bf16_filter_tcgen05 -> i8_filter_tcgen05 (+sddmm)"
     # int8 tensor rate = 2x bf16 on B200 (4.5 vs 2.25 POP/s dense, the fp8 row
     # of B200_PROFILING.md's table): the measured bf16 peak x the nominal ratio
     peak_mult = 2.0 if i8 else 1.0
@@ -473,7 +481,7 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
             with open(tf) as f:
                 tj = json.load(f)
             if (tj.get("workload") == cfg.name and tj.get("world") == world
-                    and tj.get("gemm", "bf16_filter_tcgen05+sddmm") == A.GEMM_NAMES[info0["gemm"]]):
+                    and tj.get("gemm", "bf16_filter_tcgen05+sddmm") == gkind):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -490,7 +498,7 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
                        if i8 else
                        "bf16 x bf16 -> fp32 TMEM (certified filter) + f64-accumulated refine"),
         "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
-        "config": workload_config(cfg, world, A.GEMM_NAMES[info0["gemm"]], shard, flush),
+        "config": workload_config(cfg, world, gname, shard, flush),
         "effective_tflops": flops_iter * value / 1e12,
         # whole step against the same peak (2 p_k p n / Peak / t_iter)
         "step_roofline_frac": flops_iter * value / 1e12 / peak,
@@ -510,6 +518,8 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
                           ("ms_gemm", "ms_finalize", "ms_refine", "ms_prox", "ms_spmm",
                            "ms_reduce", "ms_total")},
         "iterate": {"tau": [s["tau"] for s in stats], "trials": [s["trials"] for s in stats],
+                    "gemm_i8": [int(s["gemm_i8"]) for s in stats],
+                    "n_cand_per_step": [int(s["n_cand"]) for s in stats],
                     "nnz": final["nnz"], "n_cand": final["n_cand"], "f": final["f"]},
         "gpu_launches": int(launches),
         "clocks": clocks,
