@@ -475,7 +475,7 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
     ref_mhz = (pk_.get("clocks_under_load") or {}).get("sm_mhz_median")
     peak_clk = peak * clocks["sm_mhz"] / ref_mhz if (ref_mhz and clocks.get("sm_mhz")) else None
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "gemm_traffic_i8.json" if i8 else "gemm_traffic.json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
