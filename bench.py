@@ -517,6 +517,11 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
         "step_split_ms": {k: float(np.mean([s[k] for s in stats])) for k in
                           ("ms_gemm", "ms_finalize", "ms_refine", "ms_prox", "ms_spmm",
                            "ms_reduce", "ms_total")},
+        "warmup_iterate": {"tau": [s["tau"] for s in ws], "trials": [s["trials"] for s in ws],
+                           "gemm_i8": [int(s["gemm_i8"]) for s in ws],
+                           "n_cand": [int(s["n_cand"]) for s in ws],
+                           "nnz": [int(s["nnz"]) for s in ws],
+                           "ms_total": [float(s["ms_total"]) for s in ws]},
         "iterate": {"tau": [s["tau"] for s in stats], "trials": [s["trials"] for s in stats],
                     "gemm_i8": [int(s["gemm_i8"]) for s in stats],
                     "n_cand_per_step": [int(s["n_cand"]) for s in stats],

@@ -112,6 +112,7 @@ struct EpiParams {            // candidate rule of the fused epilogue (SURVEY P1
   // (row_A / row_B / col_sd then hold the int8 quantisation errors)
   const float* row_scale;
   const float* blk_scale;
+  const int32_t* col_perm;    // I8_FILTER: B row (= G column) k' holds variable col_perm[k']
   int exact_cols;             // 1: re-test tile-test survivors with their own column's bound
   // Omega is exactly I (the first iteration of a solve), so G = X^T X / n is
   // symmetric and each off-diagonal tile pair runs once, its survivors (i,k)
@@ -360,11 +361,13 @@ int launch_gemm_simt(int dtype, const void* Y, const void* Xt, int64_t ldk, int6
 // Y: per-row scale; rows [0, rows) of Y (f32, stride ldk) -> Yq, scale, A = ||e||, B = ||y||.
 int launch_quant_y_i8(int64_t rows, int64_t n, int64_t ldk, const float* Y, int8_t* Yq,
                       float* scale, float* rA, float* rB, cudaStream_t st);
-// X^T: per-256-row block scale -> Xq, blk_scale[rows/256], col_sd[k] = (C + D, D);
-// rows [row0, row0 + nrow) also as per-row scale / D / C into rs, rA, rB (optional).
-int launch_quant_x_i8(int64_t rows, int64_t n, int64_t ldk, const float* Xt, int8_t* Xq,
-                      float* blk_scale, float2* col_sd, int64_t row0, int64_t nrow, float* rs,
-                      float* rA, float* rB, cudaStream_t st);
+// X^T: Xq row k' = variable perm[k'] with the scale of its block of 256
+// permuted rows -> blk_scale[rows/256], col_sd[variable] = (C + D, D).
+int launch_quant_x_i8(int64_t rows, int64_t n, int64_t ldk, const float* Xt, const int32_t* perm,
+                      int8_t* Xq, float* blk_scale, float2* col_sd, cudaStream_t st);
+// max |x| per X^T row (the permutation key)
+int launch_row_absmax(int64_t rows, int64_t n, int64_t ldk, const float* Xt, float* out,
+                      cudaStream_t st);
 
 // tcgen05 split-bf16 GEMM + fused epilogue (gemm_tc.cu).
 struct TcGemmPlan;   // opaque: tensor maps for both Y buffers
@@ -377,7 +380,7 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
 void tc_plan_destroy(TcGemmPlan*);
 // per-256-column maxima of the filter's column constants (after launch_col_norms)
 int tc_plan_set_col_norms(TcGemmPlan* plan, const float2* col_sd, int64_t p, cudaStream_t st,
-                          bool i8 = false);
+                          bool i8 = false, const int32_t* perm = nullptr);
 int tc_grid_size(const TcGemmPlan* plan, int sm_count);   // persistent CTAs
 // A operand idx 2 = this rank's rows of X^T_hi (the Omega = I operand of the
 // lambda_max pass); rows_pad rows from `hi`

@@ -218,7 +218,7 @@ struct accord_ctx {
   float* xq_scale = nullptr;               // [p_pad / 256]
   int8_t* Yq[2] = {nullptr, nullptr};      // Y int8, per-row scale (quantised before each GEMM)
   float *yq_s[2] = {}, *yq_A[2] = {}, *yq_B[2] = {};
-  float *xr_s = nullptr, *xr_A = nullptr, *xr_B = nullptr;   // local X^T rows as an A operand
+  int32_t* xperm = nullptr;                // [p_pad] Xq row k' holds variable xperm[k']
 
   int64_t cap = 0;  // entries of pool / C / keys / Omega arrays
   int64_t* om_ptr = nullptr;
@@ -777,6 +777,30 @@ int64_t default_capacity(int64_t pk, int64_t p) {
 // 64 + p_k / 64 split slots.
 // The GEMM kind a create resolves to (AUTO: F32 on sm_100 -> the certified
 // filter, I8 operands unless X is sharded; else SIMT).
+// Order of the variables in the int8 X^T (quant_i8.cu): a stable counting
+// sort by log2 max|x_k| in 1/32-octave buckets, so each 256-variable block
+// (one block scale) holds nearly equal maxima; deterministic (ties keep the
+// variable order). Entries [p, p_pad) are the padding rows themselves.
+std::vector<int32_t> scale_permutation(const std::vector<float>& mx, int64_t p_pad) {
+  const int64_t p = (int64_t)mx.size();
+  constexpr int kB = 32 * 160;                      // 2^-80 .. 2^80
+  std::vector<int32_t> key(p);
+  std::vector<int64_t> cnt(kB + 1, 0);
+  for (int64_t k = 0; k < p; ++k) {
+    const float m = mx[k];
+    int b = 0;
+    if (m > 0.f && std::isfinite(m))
+      b = std::clamp((int)std::floor(32.0 * std::log2((double)m)) + kB / 2, 1, kB - 1);
+    key[k] = b;
+    cnt[b + 1]++;
+  }
+  for (int b = 0; b < kB; ++b) cnt[b + 1] += cnt[b];
+  std::vector<int32_t> perm(p_pad);
+  for (int64_t k = 0; k < p; ++k) perm[cnt[key[k]]++] = (int32_t)k;
+  for (int64_t k = p; k < p_pad; ++k) perm[k] = (int32_t)k;
+  return perm;
+}
+
 // *i8_ops: int8 operands are allocated (I8_FILTER, or AUTO's adaptive
 // bf16 -> int8 switch; ACCORD_AUTO_GEMM=bf16 turns the switch off).
 int resolve_gemm(const accord_init_params* prm, bool tc_ok, bool* i8_ops) {
@@ -831,9 +855,9 @@ Footprint footprint(const accord_init_params* prm) {
   }
   if (i8) {
     a += R((size_t)xrows_pad * ldk) + R((p_pad / kRowPad) * 4);   // X^T int8, block scales
-    a += R(p * 8) + R((p_pad / kRowPad) * 8);                     // int8 col_sd, tile maxima
+    a += R(p * 8) + R((p_pad / kRowPad) * 8) + R(p_pad * 4);      // int8 col_sd, tile maxima, perm
+    a += R(p * 4);                                               // max |x_k| (transient)
     a += 2 * R((size_t)pk_pad * ldk) + 6 * R(pk * 4);            // Y int8 (x2), row consts
-    a += 3 * R(pk * 4);                                          // local X^T rows' consts
   }
   if (sharded) {
     const int64_t rr = std::max(pk_pad, round_up((p + prm->world - 1) / prm->world, kRowPad));
@@ -1217,21 +1241,29 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
       const int64_t off = c->sharded ? c->r0 : 0;
       c->launches += launch_col_norms(pv, c->ldk, (const float*)c->Xt, c->col_sd + off, c->st);
       if (c->i8) {
-        // int8 X^T (block scale per 256 variables) and the bound's column
-        // constants of that quantisation; the local rows' constants too (the
-        // A operand of the lambda_max pass at Omega = I)
+        // int8 X^T (block scale per 256 variables, variables permuted so that
+        // a block holds nearly equal max |x|: quant_i8.cu) and the bound's
+        // column constants of that quantisation
+        c->xperm = c->dalloc<int32_t>(c->p_pad);
+        {
+          float* mx = c->dalloc<float>(c->p);
+          c->launches += launch_row_absmax(c->p, c->n, c->ldk, (const float*)c->Xt, mx, c->st);
+          std::vector<float> hm(c->p);
+          CK(cudaMemcpyAsync(hm.data(), mx, c->p * 4, cudaMemcpyDeviceToHost, c->st));
+          csync(c, c->st);
+          c->dfree(mx, c->p * 4);
+          const std::vector<int32_t> perm = scale_permutation(hm, c->p_pad);
+          CK(cudaMemcpyAsync(c->xperm, perm.data(), c->p_pad * 4, cudaMemcpyHostToDevice, c->st));
+          csync(c, c->st);   // perm is a local vector
+        }
         c->col_sd_q = c->dalloc<float2>(c->p);
         c->blk_q = c->dalloc<float2>(c->p_pad / kRowPad);
         CK(cudaMemsetAsync(c->blk_q, 0, (c->p_pad / kRowPad) * sizeof(float2), c->st));
         c->Xq = c->dalloc<int8_t>((size_t)c->xrows_pad * c->ldk);
         CK(cudaMemsetAsync(c->Xq, 0, (size_t)c->xrows_pad * c->ldk, c->st));
         c->xq_scale = c->dalloc<float>(c->p_pad / kRowPad);
-        c->xr_s = c->dalloc<float>(c->pk);
-        c->xr_A = c->dalloc<float>(c->pk);
-        c->xr_B = c->dalloc<float>(c->pk);
-        c->launches += launch_quant_x_i8(pv, c->n, c->ldk, (const float*)c->Xt, c->Xq,
-                                         c->xq_scale, c->col_sd_q, c->r0, c->pk, c->xr_s, c->xr_A,
-                                         c->xr_B, c->st);
+        c->launches += launch_quant_x_i8(pv, c->n, c->ldk, (const float*)c->Xt, c->xperm, c->Xq,
+                                         c->xq_scale, c->col_sd_q, c->st);
         for (int b = 0; b < 2; ++b) {
           c->Yq[b] = c->dalloc<int8_t>((size_t)c->pk_pad * c->ldk);
           CK(cudaMemsetAsync(c->Yq[b], 0, (size_t)c->pk_pad * c->ldk, c->st));
@@ -1252,7 +1284,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
     if (c->i8 && !tc_plan_set_i8(c->plan, c->Yq[0], c->Yq[1], c->Xq, c->xrows_pad, c->blk_q, &e))
       throw Fail{ACCORD_E_CUDA, "tensor map (int8): " + e};
     if (filt) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd, c->p, c->st);
-    if (c->i8) c->launches += tc_plan_set_col_norms(c->plan, c->col_sd_q, c->p, c->st, true);
+    if (c->i8)
+      c->launches += tc_plan_set_col_norms(c->plan, c->col_sd_q, c->p, c->st, true, c->xperm);
   }
 
   phase("operands (Y, bf16 copies, column norms, tensor maps)");
@@ -1402,8 +1435,9 @@ void TR(accord_ctx* c, const char* name) {
 void TR_flush(accord_ctx* c) {
   if (!c->trace || c->tr_marks.empty()) return;
   CK(cudaEventSynchronize(c->tr_marks.back().second));
-  std::fprintf(stderr, "[accord trace] it=%lld maxrow=%.0f ncand=%.0f", (long long)c->iters,
-               c->h_red[7], c->h_red[6]);
+  std::fprintf(stderr, "[accord trace] it=%lld maxrow=%.0f ncand=%.0f nnz=%lld i8=%d",
+               (long long)c->iters, c->h_red[7], c->h_red[6], (long long)c->nnz_global,
+               c->i8_last ? 1 : 0);
   for (size_t i = 1; i < c->tr_marks.size(); ++i) {
     float ms = 0;
     cudaEventElapsedTime(&ms, c->tr_marks[i - 1].second, c->tr_marks[i].second);
@@ -1583,14 +1617,14 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
   // the mirrored entries of other ranks' rows exchanged after it
   // (not under the filter audit: another rank's mirrored accumulators would
   // be missing from this rank's dump)
-  const bool sym2 = !ov && !c->audit_acc && c->sym2_ok && c->omega_identity &&
-                    c->gemm == ACCORD_GEMM_BF16_FILTER && !std::getenv("ACCORD_GEMM_NOSYM");
-  bool exchanged = false;
-  if (sym2 && !c->mir_row) grow_mirror(c, std::max<int64_t>(c->pk * 64, 1 << 20));
   // int8 GEMM (I8_FILTER, or AUTO once |C| is small; an override pass --
   // lambda_max at Omega = I -- whenever int8 operands exist): the int8 copy of
   // the current Y and its bound constants (a read of Y per GEMM: ~1 ms at c5)
   const bool use_i8 = c->i8 && (ov ? true : c->i8_on);
+  const bool sym2 = !use_i8 && !ov && !c->audit_acc && c->sym2_ok && c->omega_identity &&
+                    c->gemm == ACCORD_GEMM_BF16_FILTER && !std::getenv("ACCORD_GEMM_NOSYM");
+  bool exchanged = false;
+  if (sym2 && !c->mir_row) grow_mirror(c, std::max<int64_t>(c->pk * 64, 1 << 20));
   c->i8_last = use_i8;
   st.gemm_i8 = use_i8 ? 1 : 0;
   if (use_i8 && !ov)
@@ -1627,11 +1661,15 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
       ep.row_A = c->yq_A[c->cur];
       ep.row_B = c->yq_B[c->cur];
       ep.row_scale = c->yq_s[c->cur];
+    }
+    if (use_i8) {
       ep.blk_scale = c->xq_scale;
+      ep.col_perm = c->xperm;
     }
     ep.exact_cols = std::getenv("ACCORD_FILTER_EXACT") != nullptr;   // A-B diagnostic
     // Omega = I on one rank: G = S is symmetric, half the tiles (ACCORD_GEMM_NOSYM: off)
-    ep.sym = c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && c->world == 1 &&
+    // (not on the int8 operands: their columns are permuted variables)
+    ep.sym = !use_i8 && c->omega_identity && c->gemm == ACCORD_GEMM_BF16_FILTER && c->world == 1 &&
              !c->sharded && c->r0 == 0 && c->pk == c->p && !std::getenv("ACCORD_GEMM_NOSYM");
     if (sym2) {
       ep.sym = 2;
@@ -2030,8 +2068,6 @@ double lambda_max_impl(accord_ctx* c) {
     std::string e;
     const __nv_bfloat16* xh = c->Xhi + (size_t)xrow0 * c->ldk;
     if (!tc_plan_set_a(c->plan, 2, xh, c->pk_pad, &e)) throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
-    if (c->i8 && !tc_plan_set_a_i8(c->plan, 2, c->Xq + (size_t)xrow0 * c->ldk, c->pk_pad, &e))
-      throw Fail{ACCORD_E_CUDA, "tensor map: " + e};
     c->plan_a_x = true;
   }
   float* rA = c->dalloc<float>(std::max<int64_t>(c->pk, 1));
@@ -2045,10 +2081,16 @@ double lambda_max_impl(accord_ctx* c) {
   CK(cudaMemsetAsync(eptr, 0, (c->pk + 1) * 8, S));
   CK(cudaMemsetAsync(dmax, 0, 4, S));
   c->launches += launch_row_ab(c->pk, c->ldk, (const float*)xrows, rA, rB, S, c->x_drop);
-  // I8_FILTER: the int8 X^T rows with their block scales (quant_i8.cu)
-  GradOverride ov{2, c->i8 ? c->xr_A : rA, c->i8 ? c->xr_B : rB, c->i8 ? c->xr_s : nullptr,
-                  OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax,
-                  c->world == 1 && !c->sharded && c->r0 == 0 && c->pk == c->p &&
+  // int8 operands: the rank's X^T rows quantised per row into the spare int8
+  // Y buffer (the int8 buffers are re-quantised before every GEMM); the
+  // columns are the permuted int8 X^T, so no symmetric schedule
+  const int qb = 1 - c->cur;
+  if (c->i8)
+    c->launches += launch_quant_y_i8(c->pk, c->n, c->ldk, (const float*)xrows, c->Yq[qb],
+                                     c->yq_s[qb], c->yq_A[qb], c->yq_B[qb], S);
+  GradOverride ov{c->i8 ? qb : 2, c->i8 ? c->yq_A[qb] : rA, c->i8 ? c->yq_B[qb] : rB,
+                  c->i8 ? c->yq_s[qb] : nullptr, OmegaView{eptr, c->om_col, c->om_val}, 0.0, dmax,
+                  !c->i8 && c->world == 1 && !c->sharded && c->r0 == 0 && c->pk == c->p &&
                       !std::getenv("ACCORD_GEMM_NOSYM")};
   accord_iter_stats st{};
   build_candidates(c, st, &ov);                      // pass 1: certified lower bound

@@ -466,10 +466,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               for (int c = 0; c < 32; ++c) {
                 const int64_t k = c0 + c;
                 if (k < col_end) {
-                  // kMode 2: the accumulator in the units of n G (a_i b_K acc)
+                  // kMode 2: the accumulator in the units of n G (a_i b_K acc),
+                  // at the variable's own column
                   const float a = kMode == 2 ? (float)((double)(int)v[c] * sc)
                                              : __uint_as_float(v[c]);
-                  ep.audit_acc[r * ep.audit_ld + k] = a;
+                  const int64_t kv = (kMode == 2 && ep.col_perm) ? (int64_t)ep.col_perm[k] : k;
+                  ep.audit_acc[r * ep.audit_ld + kv] = a;
                   if (mir && k >= ep.r0 && k < ep.r0 + ep.pk)
                     ep.audit_acc[(k - ep.r0) * ep.audit_ld + gi] = a;
                 }
@@ -484,7 +486,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                 int mi = 0;
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                  if (c0 + c < col_end && c0 + c != gi) mi = max(mi, abs((int)v[c]));
+                  if (c0 + c < col_end &&
+                      (ep.col_perm ? (int64_t)ep.col_perm[c0 + c] : (int64_t)(c0 + c)) != gi)
+                    mi = max(mi, abs((int)v[c]));
                 wmax = fmaxf(wmax, __double2float_rd((double)mi * sc - ndel));
               } else {
                 float mm = 0.f;
@@ -619,7 +623,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
               m &= m - 1;
               if (writable) {
                 pool.row[pos] = (int32_t)r;
-                pool.col[pos] = c0 + c;
+                pool.col[pos] = (kMode == 2 && ep.col_perm) ? ep.col_perm[c0 + c] : c0 + c;
               }
               ++pos;
               if (mir_local) {
@@ -678,15 +682,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
 }
 
 // per-256-column-block maxima of the filter's column constants
+// (perm: column k' of the tile order holds variable perm[k'])
 __global__ void blk_max_kernel(const float2* __restrict__ col_sd, int64_t p, int nblk,
-                               float2* __restrict__ out) {
+                               const int32_t* __restrict__ perm, float2* __restrict__ out) {
   const int b = blockIdx.x;
   float mx = 0.f, my = 0.f;
   for (int j = threadIdx.x; j < BN; j += blockDim.x) {
     const int64_t k = (int64_t)b * BN + j;
     if (k < p) {
-      mx = fmaxf(mx, col_sd[k].x);
-      my = fmaxf(my, col_sd[k].y);
+      const float2 v = col_sd[perm ? perm[k] : k];
+      mx = fmaxf(mx, v.x);
+      my = fmaxf(my, v.y);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -844,9 +850,9 @@ bool tc_plan_set_a_i8(TcGemmPlan* p, int idx, const int8_t* q, int64_t rows_pad,
 }
 
 int tc_plan_set_col_norms(TcGemmPlan* p, const float2* col_sd, int64_t pcols, cudaStream_t st,
-                          bool i8) {
+                          bool i8, const int32_t* perm) {
   const int nblk = (int)(p->p_pad / BN);
-  blk_max_kernel<<<nblk, 256, 0, st>>>(col_sd, pcols, nblk, i8 ? p->blk_q : p->blk_sdmax);
+  blk_max_kernel<<<nblk, 256, 0, st>>>(col_sd, pcols, nblk, perm, i8 ? p->blk_q : p->blk_sdmax);
   return 1;
 }
 
