@@ -2013,12 +2013,18 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   st.ms_total = ev_ms(c, 0, 7);
   TR_flush(c);
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
-  // AUTO's operand switch (global |C|, so every rank takes the same
-  // decision): int8 once the bf16 filter's |C| / p is small, back to bf16 if
-  // the int8 filter's grows large
-  if (c->i8 && !c->i8_force && !c->refit)
-    c->i8_on = c->i8_on ? (double)st.n_cand <= c->i8_off * (double)c->p
-                        : (double)st.n_cand <= c->i8_at * (double)c->p;
+  // AUTO's operand switch (global |C| and nnz, so every rank takes the same
+  // decision): int8 once the bf16 filter's |C| / p is small, or once the new
+  // iterate's support is (nnz / p <= i8_at: the next C is mostly supp Omega
+  // plus the filter's slack; c5: |C| / p = 385, 243, 36 at iterations 1-3,
+  // nnz / p = 242, 35, 10 after them), provided |C| / p <= 8 i8_at; back to
+  // bf16 if the int8 filter's |C| / p exceeds i8_off
+  if (c->i8 && !c->i8_force && !c->refit) {
+    const double pp = (double)c->p;
+    c->i8_on = c->i8_on ? (double)st.n_cand <= c->i8_off * pp
+                        : ((double)st.n_cand <= c->i8_at * pp ||
+                           ((double)st.nnz <= c->i8_at * pp && (double)st.n_cand <= 8 * c->i8_at * pp));
+  }
   if (c->plan && c->col_sd && !c->sharded && !c->i8 &&
       (double)st.n_cand <= c->x_drop_at * (double)c->p) {
     if (c->x_drop != c->x_drop_target) set_x_width(c, c->x_drop_target);

@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <cfloat>
 #include <climits>
 #include <vector>
@@ -721,8 +722,44 @@ __device__ __forceinline__ double warp_dot_f64(const T* ys, const T* __restrict_
   return warp_sum(s);
 }
 
+// <y, x> as above with y already in float64 (staged once per work item):
+// one F2F per product instead of two (the XU pipe's F2F.F64.F32 was the
+// refine's limit); the same products in the same order, so bitwise equal
+__device__ __forceinline__ double warp_dot_f64_yd(const double* ysd, const float* __restrict__ xr,
+                                                  int64_t ldk, int lane) {
+  constexpr int V = 4;
+  constexpr int kStep = 32 * V;
+  double s = 0.0;
+  int64_t m = lane * V;
+  for (; m + 7 * kStep < ldk; m += 8 * kStep) {
+    float4 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(xr + m + u * kStep));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2 y0 = *reinterpret_cast<const double2*>(ysd + m + u * kStep);
+      const double2 y1 = *reinterpret_cast<const double2*>(ysd + m + u * kStep + 2);
+      s = fma(y0.x, (double)x[u].x, s);
+      s = fma(y0.y, (double)x[u].y, s);
+      s = fma(y1.x, (double)x[u].z, s);
+      s = fma(y1.y, (double)x[u].w, s);
+    }
+  }
+  for (; m < ldk; m += kStep) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(xr + m));
+    const double2 y0 = *reinterpret_cast<const double2*>(ysd + m);
+    const double2 y1 = *reinterpret_cast<const double2*>(ysd + m + 2);
+    s = fma(y0.x, (double)x.x, s);
+    s = fma(y0.y, (double)x.y, s);
+    s = fma(y1.x, (double)x.z, s);
+    s = fma(y1.y, (double)x.w, s);
+  }
+  return warp_sum(s);
+}
+
 // kArith: 0 = float64 products (both operands converted by F2F), 1 =
-// float-float (A-B variant, slower; ACCORD_REFINE=ff)
+// float-float (A-B variant, slower; ACCORD_REFINE=ff), 2 = Y_i staged in
+// shared memory as float64 (one F2F per product; T = float, default)
 // sym (Omega = I on one rank, C = C^T): only the entries with k >= i; the
 // others are copied from their twins afterwards (sym_mirror_kernel)
 template <typename T, int kArith = 0>
@@ -759,6 +796,14 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
   if (beg == end) return;
   if (y_global) {
     ys = Y + r * ldk;
+  } else if constexpr (kArith == 2) {
+    double* yd = reinterpret_cast<double*>(ys_raw);
+    for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V) {
+      const VT v = *reinterpret_cast<const VT*>(Y + r * ldk + m);
+#pragma unroll
+      for (int u = 0; u < V; ++u) yd[m + u] = (double)vget(v, u);
+    }
+    __syncthreads();
   } else {
     T* yw = reinterpret_cast<T*>(ys_raw);
     for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V)
@@ -799,7 +844,13 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
       if (lane == 0) c_g[e] = (T)(s * inv_n);
       continue;
     }
-    const double s = warp_dot_f64<T>(ys, xr, ldk, lane);
+    double s;
+    if constexpr (kArith == 2) {
+      if (y_global) s = warp_dot_f64<T>(ys, xr, ldk, lane);
+      else s = warp_dot_f64_yd(reinterpret_cast<const double*>(ys_raw), (const float*)xr, ldk, lane);
+    } else {
+      s = warp_dot_f64<T>(ys, xr, ldk, lane);
+    }
     if (lane == 0) c_g[e] = (T)(s * inv_n);
   }
 }
@@ -1475,7 +1526,13 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                   int64_t n_items, int64_t L, const int32_t* item_row, int ff, int sym) {
   const unsigned grid = (unsigned)(itm_ptr ? n_items : pk);
   if (pk == 0) return 0;
-  size_t smem = (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
+  // f32: Y_i staged as float64 (kArith 2) unless ACCORD_REFINE=f32 (A-B)
+  static const bool yd = [] {
+    const char* e = std::getenv("ACCORD_REFINE");
+    return !(e && std::strcmp(e, "f32") == 0);
+  }();
+  const bool stage_d = dtype != ACCORD_F64 && ff != 1 && yd;
+  size_t smem = (size_t)ldk * ((dtype == ACCORD_F64 || stage_d) ? 8 : 4);
   const int y_global = smem > 200 * 1024 ? 1 : 0;
   if (y_global) smem = 0;
   // threads per block (warps share the item's candidates): ACCORD_REFINE_THREADS (A-B);
@@ -1493,6 +1550,8 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                          200 * 1024);
     cudaFuncSetAttribute(refine_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
+    cudaFuncSetAttribute(refine_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr_done(attr_seen);
   }
   if (dtype == ACCORD_F64)
@@ -1502,6 +1561,11 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
                                                    y_global, sym);
   else if (ff == 1)
     refine_kernel<float, 1><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
+                                                        (const float*)Y, (const float*)Xt,
+                                                        (float*)c_g, v0, v1, itm_ptr, L, item_row,
+                                                        y_global, sym);
+  else if (stage_d)
+    refine_kernel<float, 2><<<grid, thr, smem, st>>>(pk, n, ldk, c_ptr, c_col,
                                                         (const float*)Y, (const float*)Xt,
                                                         (float*)c_g, v0, v1, itm_ptr, L, item_row,
                                                         y_global, sym);
