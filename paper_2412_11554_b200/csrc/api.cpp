@@ -211,6 +211,9 @@ struct accord_ctx {
   bool i8_on = false;                      // the next GEMM in int8
   bool i8_last = false;                    // the last GEMM ran in int8 (filter audit)
   double i8_at = 48.0, i8_off = 384.0;     // AUTO: on at |C|/p <= i8_at (bf16), off above i8_off
+  double i8_excess = 5e-4;                 // AUTO: off for good if int8 adds > i8_excess p^2 to |C|
+  int64_t bf16_cand = -1;                  // |C| of the last bf16-filter GEMM (global)
+  bool i8_banned = false;
   int64_t gemm_launches_i8 = 0;
   float2* col_sd_q = nullptr;              // int8 column constants of the bound
   float2* blk_q = nullptr;                 // their 256-column tile maxima
@@ -1065,6 +1068,7 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   }
   if (const char* e = std::getenv("ACCORD_I8_AT")) c->i8_at = std::atof(e);     // tuning
   if (const char* e = std::getenv("ACCORD_I8_OFF")) c->i8_off = std::atof(e);
+  if (const char* e = std::getenv("ACCORD_I8_EXCESS")) c->i8_excess = std::atof(e);
   const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
   if (tc && !tc_ok) throw Fail{ACCORD_E_UNSUPPORTED, "tcgen05 GEMM needs an sm_100 device"};
   if (tc && prm->x_sharded && prm->world > 1 && prm->row_begin % kRowPad != 0)
@@ -2019,11 +2023,25 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   // plus the filter's slack; c5: |C| / p = 385, 243, 36 at iterations 1-3,
   // nnz / p = 242, 35, 10 after them), provided |C| / p <= 8 i8_at; back to
   // bf16 if the int8 filter's |C| / p exceeds i8_off
+  //
+  // Cost check after the first int8 GEMM: int8 saves ~40 % of a GEMM pass,
+  // i.e. ~0.8 p n / peak per row, and each extra candidate costs a 4n-byte
+  // gather in the refine, so the break-even is ~1e-3 p extra candidates per
+  // row (c5: ~1000; c3, p = 20,000: ~20). If int8 added more than
+  // i8_excess p^2 to |C| over the last bf16 GEMM's, it stays off for the solve
+  // (c3: 68 -> 227 per row; c5: 12.5 -> 60; c4: 6 -> 41). Counts only, so the
+  // decision is deterministic and the same on every rank.
   if (c->i8 && !c->i8_force && !c->refit) {
     const double pp = (double)c->p;
-    c->i8_on = c->i8_on ? (double)st.n_cand <= c->i8_off * pp
-                        : ((double)st.n_cand <= c->i8_at * pp ||
-                           ((double)st.nnz <= c->i8_at * pp && (double)st.n_cand <= 8 * c->i8_at * pp));
+    if (st.gemm_i8 && !c->i8_banned && c->bf16_cand >= 0 &&
+        (double)(st.n_cand - c->bf16_cand) > c->i8_excess * pp * pp)
+      c->i8_banned = true;
+    if (!st.gemm_i8) c->bf16_cand = st.n_cand;
+    c->i8_on = !c->i8_banned &&
+               (c->i8_on ? (double)st.n_cand <= c->i8_off * pp
+                         : ((double)st.n_cand <= c->i8_at * pp ||
+                            ((double)st.nnz <= c->i8_at * pp &&
+                             (double)st.n_cand <= 8 * c->i8_at * pp)));
   }
   if (c->plan && c->col_sd && !c->sharded && !c->i8 &&
       (double)st.n_cand <= c->x_drop_at * (double)c->p) {
@@ -2515,6 +2533,9 @@ accord_status accord_set_lambda(accord_ctx* c, double lambda) {
   }
   return guard(c, [&] {
     c->lam = lambda;
+    // AUTO's int8 cost check starts over (the candidate density depends on lambda)
+    c->i8_banned = false;
+    c->bf16_cand = -1;
     refresh_objective(c);
   });
 }

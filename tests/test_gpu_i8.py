@@ -167,3 +167,28 @@ def test_i8_ragged_shapes_and_workspace():
         st = s.step(12)
         W = s.export_csr().to_dense(p)
     compare_full(Xt, lam, 12, inv_L, W, st, "f32")
+
+
+def test_auto_switch_and_cost_check_config3():
+    """AUTO at config 3 (p = 20,000, lambda = 0.1 = 3.2 null sd: the int8 bound
+    admits ~3x the bf16 filter's candidates, more than its GEMM saving is
+    worth at this p): bf16 until the support is small, one int8 iteration,
+    then bf16 for good; the iterate equals the bf16-only
+    run's."""
+    _cuda()
+    pr = make_problem(3)
+    lam = pr.cfg.lambdas[0]
+    out = {}
+    for g in (A.GEMM_AUTO, A.GEMM_BF16_FILTER):
+        with A.AccordSolver(torch.from_numpy(pr.Xt).cuda(), lam, inv_L=0.0, gemm=g) as s:
+            st = s.step(10)
+            out[g] = (s.export_csr(), st, s.info())
+    flags = [x["gemm_i8"] for x in out[A.GEMM_AUTO][1]]
+    assert flags[0] == 0 and sum(flags) == 1, flags          # exactly one int8 trial
+    k = flags.index(1)
+    assert all(f == 0 for f in flags[k + 1:])
+    assert out[A.GEMM_AUTO][2]["gemm_launches_i8"] == 1
+    a, b = out[A.GEMM_AUTO], out[A.GEMM_BF16_FILTER]
+    assert [x["tau"] for x in a[1]] == [x["tau"] for x in b[1]]
+    assert np.array_equal(a[0].col, b[0].col)
+    assert np.abs(a[0].val - b[0].val).max() <= 1e-6 * np.abs(b[0].val).max()

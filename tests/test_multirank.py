@@ -142,7 +142,7 @@ def run_ranks(Xt, lam, T, inv_L, P, gemm, align=256, infos=None):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gemm", [A.GEMM_SIMT, A.GEMM_BF16_FILTER])
+@pytest.mark.parametrize("gemm", [A.GEMM_SIMT, A.GEMM_BF16_FILTER, A.GEMM_I8_FILTER, A.GEMM_AUTO])
 def test_p_invariance_one_gpu(gemm):
     import torch
     if not torch.cuda.is_available():
