@@ -214,6 +214,9 @@ struct accord_ctx {
   double i8_excess = 5e-4;                 // AUTO: off for good if int8 adds > i8_excess p^2 to |C|
   int64_t bf16_cand = -1;                  // |C| of the last bf16-filter GEMM (global)
   bool i8_banned = false;
+  // Y_hi / row_A / row_B of each Y buffer match its Y (the SpMM skips the bf16
+  // operand while the int8 GEMM is on; a bf16 GEMM re-derives it first)
+  bool yhi_ok[2] = {true, true};
   int64_t gemm_launches_i8 = 0;
   float2* col_sd_q = nullptr;              // int8 column constants of the bound
   float2* blk_q = nullptr;                 // their 256-column tile maxima
@@ -545,22 +548,47 @@ SpmmItems items_view(accord_ctx* c) {
                    c->row_done, kItemEntries};
 }
 
+// Does the next GEMM need Y's bf16 operand? Not while the int8 GEMM is on
+// (it quantises Y itself); the SpMM then writes Y alone (ACCORD_SPMM_BF16=1:
+// always write it, A-B).
+bool want_yhi(accord_ctx* c) {
+  static const bool always = [] {
+    const char* e = std::getenv("ACCORD_SPMM_BF16");
+    return e && e[0] == '1';
+  }();
+  return !(c->i8 && c->i8_on && c->y_drop == 0 && !c->sharded && !always);
+}
+
+// Y_hi, row_A, row_B of buffer b from its Y (after SpMM passes that skipped
+// them), before a bf16 GEMM
+void ensure_yhi(accord_ctx* c, int b) {
+  if (c->yhi_ok[b] || !c->Yhi[b]) return;
+  c->launches += launch_split_bf16((const float*)c->Y[b], c->pk_pad * c->ldk, c->Yhi[b], nullptr,
+                                   c->st);
+  c->launches += launch_row_ab(c->pk, c->ldk, (const float*)c->Y[b], c->row_A[b], c->row_B[b],
+                               c->st, 0);
+  c->yhi_ok[b] = true;
+}
+
 // SpMM Y+ = W X^T (and D = (W - Wold) X^T) over all of X: one launch, or a
 // ring pass accumulating in float64 when X is sharded.
 void spmm_all(accord_ctx* c, const int64_t* ptr, const int32_t* col, const void* wn,
               const void* wo, int yb, double* row_D2, double* row_Y2) {
+  const bool hi = want_yhi(c) && c->Yhi[yb];
+  c->yhi_ok[yb] = hi || !c->Yhi[yb];
   if (!c->sharded && c->tma_spmm) {
     if (c->items_of != ptr) build_items(c, ptr);
     c->launches += launch_spmm_tma(c->pk, c->ldk, ptr, col, (const float*)wn, (const float*)wo,
-                                   (const float*)c->Xt, (float*)c->Y[yb], c->Yhi[yb], c->Ylo[yb],
+                                   (const float*)c->Xt, (float*)c->Y[yb],
+                                   hi ? c->Yhi[yb] : nullptr, hi ? c->Ylo[yb] : nullptr,
                                    c->row_A[yb], c->row_B[yb], row_D2, row_Y2, items_view(c),
                                    c->sm_count, c->st, nullptr, nullptr, c->y_drop);
     return;
   }
   if (!c->sharded) {
     c->launches += launch_spmm(c->dtype, c->pk, c->n, c->ldk, ptr, col, wn, wo, c->Xt, c->Y[yb],
-                               c->Yhi[yb], c->Ylo[yb], c->row_A[yb], c->row_B[yb], row_D2,
-                               row_Y2, c->st, nullptr, c->y_drop);
+                               hi ? c->Yhi[yb] : nullptr, hi ? c->Ylo[yb] : nullptr, c->row_A[yb],
+                               c->row_B[yb], row_D2, row_Y2, c->st, nullptr, c->y_drop);
     return;
   }
   ring_pass(c, false, [&](const void* slab, int, int64_t v0, int64_t v1, bool first, bool last) {
@@ -1625,6 +1653,7 @@ void build_candidates(accord_ctx* c, accord_iter_stats& st, const GradOverride* 
   // lambda_max at Omega = I -- whenever int8 operands exist): the int8 copy of
   // the current Y and its bound constants (a read of Y per GEMM: ~1 ms at c5)
   const bool use_i8 = c->i8 && (ov ? true : c->i8_on);
+  if (!use_i8 && !ov) ensure_yhi(c, c->cur);   // a bf16 GEMM after int8 ones
   const bool sym2 = !use_i8 && !ov && !c->audit_acc && c->sym2_ok && c->omega_identity &&
                     c->gemm == ACCORD_GEMM_BF16_FILTER && !std::getenv("ACCORD_GEMM_NOSYM");
   bool exchanged = false;
@@ -1909,9 +1938,11 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
                                        c->diag_zz, c->row_Y2, c->row_D2, c->diag_a, S);
     } else if (paired) {
       if (c->items_of != c->c_ptr) build_items(c, c->c_ptr);
+      const bool hi = want_yhi(c) && c->Yhi[nb];
+      c->yhi_ok[nb] = hi || !c->Yhi[nb];
       c->launches += launch_spmm_tma(c->pk, c->ldk, c->c_ptr, c->c_col, (const float*)c->c_wn,
-                                     (const float*)c->c_w, (const float*)c->Xt,
-                                     (float*)c->Y[nb], c->Yhi[nb], c->Ylo[nb], c->row_A[nb],
+                                     (const float*)c->c_w, (const float*)c->Xt, (float*)c->Y[nb],
+                                     hi ? c->Yhi[nb] : nullptr, hi ? c->Ylo[nb] : nullptr, c->row_A[nb],
                                      c->row_B[nb], c->row_D2, c->row_Y2, items_view(c),
                                      c->sm_count, S, (const float*)c->c_wn2, c->row_D2b,
                                      c->y_drop);
@@ -1982,10 +2013,12 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
     tau *= c->beta;
   }
   // ---------------- accept: Omega <- Omega+, Y <- Y+ ----------------
-  if (diag_ls)
+  if (diag_ls) {
     c->launches += launch_diag_apply(c->pk, c->ldk, xrow0, (const float*)c->Xt, (float*)c->Y[nb],
                                      c->Yhi[nb], c->diag_a, tau, c->row_A[nb], c->row_B[nb], S,
                                      c->y_drop);
+    c->yhi_ok[nb] = true;
+  }
   c->launches += launch_scan_i32(c->row_nnz, c->om_ptr, c->pk, c->scan_tmp, c->scan_tmp_sz, S);
   c->launches += launch_compact(c->dtype, c->pk, c->r0, c->c_ptr, c->c_col, c->c_wn, c->om_ptr,
                                 c->om_col, c->om_val, S);
