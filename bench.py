@@ -474,6 +474,23 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
     # was taken at MEASURED_PEAKS' median clock under load)
     ref_mhz = (pk_.get("clocks_under_load") or {}).get("sm_mhz_median")
     peak_clk = peak * clocks["sm_mhz"] / ref_mhz if (ref_mhz and clocks.get("sm_mhz")) else None
+    lib_i8 = None
+    if i8:
+        # the int8 GEMM runs at another power-capped clock than the bf16 one the
+        # measured peak was taken at, so the clock-scaled figure does not apply;
+        # beside the nominal-ratio peak: cuBLAS int8's own sustained rate under
+        # the same cap (tools/int8_probe.py, measured on this pool)
+        peak_clk = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02b", "library_gemm_probe.jsonl")) as f:
+                for line in f:
+                    j = json.loads(line)
+                    if j.get("dtype") == "int8" and j.get("tops"):
+                        lib_i8 = {"tops": j["tops"], "sm_mhz": j.get("sm_mhz"),
+                                  "source": "torch._int_mm 8192^3 back to back, 6 s "
+                                            "(profiles/r02b/library_gemm_probe.jsonl)"}
+        except Exception:
+            lib_i8 = None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "gemm_traffic_i8.json" if i8 else "gemm_traffic.json")
     if os.path.exists(tf):
@@ -512,6 +529,8 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
                                      f"bf16_tflops_sustained, {pdata}"),
                      "peak_at_run_clock": peak_clk,
                      "frac_at_run_clock": achieved / peak_clk if peak_clk else None,
+                     "library_int8_sustained": lib_i8,
+                     "frac_of_library_int8": achieved / lib_i8["tops"] if lib_i8 else None,
                      "algorithmic": f"2*p_k*p*n = {2.0 * pk0 * p * n:.3e} FLOP per launch",
                      "ms_per_launch": ms_gemm_max},
         "step_split_ms": {k: float(np.mean([s[k] for s in stats])) for k in
