@@ -61,10 +61,13 @@ __device__ __forceinline__ double wsum(double v) {
 // kCols: output columns per consumer thread (8: two float4 per staged row;
 // 4: one float4, twice the consumer warps per block and a third of the
 // accumulator registers -- more warps in flight per SM)
-template <bool kPair, int kCols>
+// kMinB: resident blocks the register budget is sized for (0 = the default:
+// 3 for the paired kernel, whose 128-register cap spills ~176 B; 2 = no
+// spills, fewer warps: ACCORD_SPMM_MINB=2, A-B)
+template <bool kPair, int kCols, int kMinB = 0>
 __global__ void __launch_bounds__(kCols == 4 ? 32 + kSpmmTmaMaxConsumers
                                   : (kPair ? 32 + kSpmmPairMaxConsumers : 32 + kSpmmTmaMaxConsumers),
-                                  kCols == 4 ? (kPair ? 2 : 3) : (kPair ? 3 : 2))
+                                  kMinB ? kMinB : (kCols == 4 ? (kPair ? 2 : 3) : (kPair ? 3 : 2)))
 spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__ ptr,
                 const int32_t* __restrict__ col, const float* __restrict__ wn,
                 const float* __restrict__ wo, const float* __restrict__ Xt, float* __restrict__ Yout,
@@ -148,11 +151,17 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
           w = 0.0; d = 0.0; d2 = 0.0; cc = 0;
         }
       };
-      double nw_ = 0.0, nd_ = 0.0, nd2_ = 0.0;
-      int32_t nc_ = 0;
+      // lookahead of two items: the first 32 entries of items k+1 (set a)
+      // and k+2 (set b) are in flight while item k is emitted (items have
+      // ~10 entries in the steady state, so one item of lookahead left the
+      // producer waiting on these loads: ncu, int8-filter c5 run)
+      double nw_ = 0.0, nd_ = 0.0, nd2_ = 0.0, bw_ = 0.0, bd_ = 0.0, bd2_ = 0.0;
+      int32_t nc_ = 0, bc_ = 0;
       {
         const int64_t b0 = __shfl_sync(0xffffffffu, begj, 0), e0_ = __shfl_sync(0xffffffffu, endj, 0);
         load(b0 + lane, e0_, nw_, nd_, nd2_, nc_);
+        const int64_t b1 = __shfl_sync(0xffffffffu, begj, 1), e1_ = __shfl_sync(0xffffffffu, endj, 1);
+        if (nv > 1) load(b1 + lane, e1_, bw_, bd_, bd2_, bc_);
       }
       for (int k = 0; k < nv; ++k) {
         const int64_t r = __shfl_sync(0xffffffffu, rj, k);
@@ -162,10 +171,12 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         const int64_t end = __shfl_sync(0xffffffffu, endj, k);
         double w = nw_, d = nd_, d2 = nd2_;
         int32_t cc = nc_;
-        if (k + 1 < nv) {   // lookahead: first batch of the next item
-          const int64_t bn = __shfl_sync(0xffffffffu, begj, k + 1);
-          const int64_t en = __shfl_sync(0xffffffffu, endj, k + 1);
-          load(bn + lane, en, nw_, nd_, nd2_, nc_);
+        nw_ = bw_; nd_ = bd_; nd2_ = bd2_; nc_ = bc_;
+        {
+          const int kn = k + 2 < 32 ? k + 2 : 31;
+          const int64_t bn = __shfl_sync(0xffffffffu, begj, kn);
+          const int64_t en = __shfl_sync(0xffffffffu, endj, kn);
+          if (k + 2 < nv) load(bn + lane, en, bw_, bd_, bd2_, bc_);
         }
         // one entry of lookahead so that the item's last nonzero carries kFlagLast
         bool pend = false;
@@ -477,6 +488,8 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
                          100 * 1024);
     cudaFuncSetAttribute(spmm_tma_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          100 * 1024);
+    cudaFuncSetAttribute(spmm_tma_kernel<true, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         100 * 1024);
     attr_done(attr_seen);
   }
   // 8 columns per consumer thread; 4 (twice the consumer warps, a third of the
@@ -501,7 +514,12 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
     if (wn2) launch(spmm_tma_kernel<true, 4>);
     else launch(spmm_tma_kernel<false, 4>);
   } else {
-    if (wn2) launch(spmm_tma_kernel<true, 8>);
+    static const bool minb2 = [] {
+      const char* e = std::getenv("ACCORD_SPMM_MINB");
+      return e && std::atoi(e) == 2;
+    }();
+    if (wn2 && minb2) launch(spmm_tma_kernel<true, 8, 2>);
+    else if (wn2) launch(spmm_tma_kernel<true, 8>);
     else launch(spmm_tma_kernel<false, 8>);
   }
   return 1;
