@@ -212,6 +212,7 @@ struct accord_ctx {
   bool i8_last = false;                    // the last GEMM ran in int8 (filter audit)
   double i8_at = 48.0, i8_off = 384.0;     // AUTO: on at |C|/p <= i8_at (bf16), off above i8_off
   double i8_excess = 5e-4;                 // AUTO: off for good if int8 adds > i8_excess p^2 to |C|
+  double i8_nnz = 256.0, i8_ccap = 512.0;  // AUTO: on at nnz/p <= i8_nnz with |C|/p <= i8_ccap
   int64_t bf16_cand = -1;                  // |C| of the last bf16-filter GEMM (global)
   bool i8_banned = false;
   // Y_hi / row_A / row_B of each Y buffer match its Y (the SpMM skips the bf16
@@ -1097,6 +1098,8 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   if (const char* e = std::getenv("ACCORD_I8_AT")) c->i8_at = std::atof(e);     // tuning
   if (const char* e = std::getenv("ACCORD_I8_OFF")) c->i8_off = std::atof(e);
   if (const char* e = std::getenv("ACCORD_I8_EXCESS")) c->i8_excess = std::atof(e);
+  if (const char* e = std::getenv("ACCORD_I8_NNZ")) c->i8_nnz = std::atof(e);
+  if (const char* e = std::getenv("ACCORD_I8_CCAP")) c->i8_ccap = std::atof(e);
   const bool tc = c->gemm == ACCORD_GEMM_BF16X3 || c->gemm == ACCORD_GEMM_BF16_FILTER;
   if (tc && !tc_ok) throw Fail{ACCORD_E_UNSUPPORTED, "tcgen05 GEMM needs an sm_100 device"};
   if (tc && prm->x_sharded && prm->world > 1 && prm->row_begin % kRowPad != 0)
@@ -2052,10 +2055,12 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   if (!std::isfinite(c->f)) throw Fail{ACCORD_E_NUMERIC, "non-finite objective"};
   // AUTO's operand switch (global |C| and nnz, so every rank takes the same
   // decision): int8 once the bf16 filter's |C| / p is small, or once the new
-  // iterate's support is (nnz / p <= i8_at: the next C is mostly supp Omega
-  // plus the filter's slack; c5: |C| / p = 385, 243, 36 at iterations 1-3,
-  // nnz / p = 242, 35, 10 after them), provided |C| / p <= 8 i8_at; back to
-  // bf16 if the int8 filter's |C| / p exceeds i8_off
+  // iterate's support is (nnz / p <= i8_nnz = 256: the next C is mostly
+  // supp Omega plus the filter's slack; c5: |C| / p = 385, 243, 36 at
+  // iterations 1-3, nnz / p = 242, 35, 10 after them), provided
+  // |C| / p <= i8_ccap = 512 (not from Omega = I's G = S, whose int8 C is
+  // ~5x the bf16 one); back to bf16 if the int8 filter's |C| / p exceeds
+  // i8_off
   //
   // Cost check after the first int8 GEMM: int8 saves ~40 % of a GEMM pass,
   // i.e. ~0.8 p n / peak per row, and each extra candidate costs a 4n-byte
@@ -2073,8 +2078,8 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
     c->i8_on = !c->i8_banned &&
                (c->i8_on ? (double)st.n_cand <= c->i8_off * pp
                          : ((double)st.n_cand <= c->i8_at * pp ||
-                            ((double)st.nnz <= c->i8_at * pp &&
-                             (double)st.n_cand <= 8 * c->i8_at * pp)));
+                            ((double)st.nnz <= c->i8_nnz * pp &&
+                             (double)st.n_cand <= c->i8_ccap * pp)));
   }
   if (c->plan && c->col_sd && !c->sharded && !c->i8 &&
       (double)st.n_cand <= c->x_drop_at * (double)c->p) {

@@ -129,10 +129,21 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     // the current one is being emitted, so the producer's global-memory
     // latencies overlap the copies in flight.
     const int64_t G = gridDim.x;
+    // the item -> row map of the next batch of 32 items is loaded one batch
+    // ahead (one dependent global latency per batch instead of two)
+    int32_t row_next = 0;
+    {
+      const int64_t itj0 = blockIdx.x + (int64_t)lane * G;
+      if (itj0 < n_items) row_next = items.item_row[itj0];
+    }
     for (int64_t base = blockIdx.x; base < n_items; base += 32 * G) {
       const int64_t itj = base + (int64_t)lane * G;
       const bool vj = itj < n_items;
-      const int64_t rj = vj ? (int64_t)items.item_row[itj] : 0;
+      const int64_t rj = vj ? (int64_t)row_next : 0;
+      {
+        const int64_t itn = itj + 32 * G;
+        row_next = itn < n_items ? items.item_row[itn] : 0;
+      }
       const int64_t i0 = items.itm_ptr[rj], i1 = items.itm_ptr[rj + 1];
       const int64_t p0 = ptr[rj], p1 = ptr[rj + 1];
       const int chj = (int)(itj - i0), nchj = (int)(i1 - i0);
@@ -140,28 +151,40 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       const int64_t endj = min(p1, begj + items.L);
       const int nv = __popc(__ballot_sync(0xffffffffu, vj));
       // entries of the first item
-      auto load = [&](int64_t e, int64_t end, double& w, double& d, double& d2, int32_t& cc) {
+      // raw loads (no use of the values: the warp does not wait for them
+      // here) and the conversion where the values are consumed
+      struct Raw { float w, o, w2; int32_t cc; };
+      auto load_raw = [&](int64_t e, int64_t end, Raw& q) {
         if (e < end) {
-          w = (double)__ldg(wn + e);
-          const double o = wo ? (double)__ldg(wo + e) : 0.0;
-          d = wo ? w - o : 0.0;
-          d2 = kPair ? (double)__ldg(wn2 + e) - o : 0.0;
-          cc = __ldg(col + e);
+          q.w = __ldg(wn + e);
+          q.o = wo ? __ldg(wo + e) : 0.f;
+          q.w2 = kPair ? __ldg(wn2 + e) : 0.f;
+          q.cc = __ldg(col + e);
         } else {
-          w = 0.0; d = 0.0; d2 = 0.0; cc = 0;
+          q.w = 0.f; q.o = 0.f; q.w2 = 0.f; q.cc = 0;
         }
+      };
+      auto cvt = [&](const Raw& q, double& w, double& d, double& d2, int32_t& cc) {
+        w = (double)q.w;
+        d = wo ? w - (double)q.o : 0.0;
+        d2 = kPair ? (double)q.w2 - (double)q.o : 0.0;
+        cc = q.cc;
+      };
+      auto load = [&](int64_t e, int64_t end, double& w, double& d, double& d2, int32_t& cc) {
+        Raw q;
+        load_raw(e, end, q);
+        cvt(q, w, d, d2, cc);
       };
       // lookahead of two items: the first 32 entries of items k+1 (set a)
       // and k+2 (set b) are in flight while item k is emitted (items have
       // ~10 entries in the steady state, so one item of lookahead left the
       // producer waiting on these loads: ncu, int8-filter c5 run)
-      double nw_ = 0.0, nd_ = 0.0, nd2_ = 0.0, bw_ = 0.0, bd_ = 0.0, bd2_ = 0.0;
-      int32_t nc_ = 0, bc_ = 0;
+      Raw qa{0.f, 0.f, 0.f, 0}, qb{0.f, 0.f, 0.f, 0};
       {
         const int64_t b0 = __shfl_sync(0xffffffffu, begj, 0), e0_ = __shfl_sync(0xffffffffu, endj, 0);
-        load(b0 + lane, e0_, nw_, nd_, nd2_, nc_);
+        load_raw(b0 + lane, e0_, qa);
         const int64_t b1 = __shfl_sync(0xffffffffu, begj, 1), e1_ = __shfl_sync(0xffffffffu, endj, 1);
-        if (nv > 1) load(b1 + lane, e1_, bw_, bd_, bd2_, bc_);
+        if (nv > 1) load_raw(b1 + lane, e1_, qb);
       }
       for (int k = 0; k < nv; ++k) {
         const int64_t r = __shfl_sync(0xffffffffu, rj, k);
@@ -169,14 +192,15 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         const int nch = __shfl_sync(0xffffffffu, nchj, k);
         const int64_t beg = __shfl_sync(0xffffffffu, begj, k);
         const int64_t end = __shfl_sync(0xffffffffu, endj, k);
-        double w = nw_, d = nd_, d2 = nd2_;
-        int32_t cc = nc_;
-        nw_ = bw_; nd_ = bd_; nd2_ = bd2_; nc_ = bc_;
+        double w, d, d2;
+        int32_t cc;
+        cvt(qa, w, d, d2, cc);
+        qa = qb;
         {
           const int kn = k + 2 < 32 ? k + 2 : 31;
           const int64_t bn = __shfl_sync(0xffffffffu, begj, kn);
           const int64_t en = __shfl_sync(0xffffffffu, endj, kn);
-          if (k + 2 < nv) load(bn + lane, en, bw_, bd_, bd2_, bc_);
+          if (k + 2 < nv) load_raw(bn + lane, en, qb);
         }
         // one entry of lookahead so that the item's last nonzero carries kFlagLast
         bool pend = false;
