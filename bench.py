@@ -431,7 +431,9 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
         s2 = A.AccordSolver(Xh, lam, tau0=cfg.tau0, beta=cfg.beta, inv_L=0.0, row_begin=r0,
                             row_end=r1, rank=rank, world=world, comm=comm, nccl_id=nid,
                             stream=stream, device=dev, **skw)
-        s2.step(args.steps)
+        torch.cuda.synchronize()
+        t_create = time.perf_counter() - t0
+        e2e_stats = s2.step(args.steps)
         csr = s2.export_csr()
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
@@ -442,6 +444,8 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
             te = float(tt[0])
         d2h = csr.row_ptr.nbytes + csr.col.nbytes + csr.val.nbytes
         e2e = {"value": args.steps / te, "unit": "iterations/s",
+               "create_s": t_create,
+               "ms_per_iteration": [float(x["ms_total"]) for x in e2e_stats],
                "h2d_bytes_per_step": int(Xh_all.nbytes // args.steps),
                "d2h_bytes_per_step": int(d2h // args.steps),
                "note": "one solve through the C ABI from pinned host X: create (H2D copy, "

@@ -213,7 +213,6 @@ struct accord_ctx {
   double i8_at = 48.0, i8_off = 384.0;     // AUTO: on at |C|/p <= i8_at (bf16), off above i8_off
   double i8_excess = 5e-4;                 // AUTO: off for good if int8 adds > i8_excess p^2 to |C|
   double i8_nnz = 256.0, i8_ccap = 512.0;  // AUTO: on at nnz/p <= i8_nnz with |C|/p <= i8_ccap
-  int64_t bf16_cand = -1;                  // |C| of the last bf16-filter GEMM (global)
   bool i8_banned = false;
   // Y_hi / row_A / row_B of each Y buffer match its Y (the SpMM skips the bf16
   // operand while the int8 GEMM is on; a bf16 GEMM re-derives it first)
@@ -2035,6 +2034,7 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   CK(cudaEventRecord(c->ev[7], S));
   CK(cudaEventSynchronize(c->ev[7]));
   c->nnz_local = nnz_loc;
+  const int64_t nnz_before = c->nnz_global;   // the support the GEMM ran at
   c->nnz_global = (int64_t)r[5];
   c->parts[0] = -r[2];
   c->parts[1] = r[3] / (2.0 * (double)c->n);
@@ -2062,19 +2062,19 @@ void step_one(accord_ctx* c, accord_iter_stats* s) {
   // ~5x the bf16 one); back to bf16 if the int8 filter's |C| / p exceeds
   // i8_off
   //
-  // Cost check after the first int8 GEMM: int8 saves ~40 % of a GEMM pass,
-  // i.e. ~0.8 p n / peak per row, and each extra candidate costs a 4n-byte
-  // gather in the refine, so the break-even is ~1e-3 p extra candidates per
-  // row (c5: ~1000; c3, p = 20,000: ~20). If int8 added more than
-  // i8_excess p^2 to |C| over the last bf16 GEMM's, it stays off for the solve
-  // (c3: 68 -> 227 per row; c5: 12.5 -> 60; c4: 6 -> 41). Counts only, so the
-  // decision is deterministic and the same on every rank.
+  // Cost check after every int8 GEMM: int8 saves ~40 % of a GEMM pass, i.e.
+  // ~0.8 p n / peak per row, and each candidate beyond the support costs a
+  // 4n-byte gather in the refine, so the break-even is ~1e-3 p candidates
+  // per row beyond supp Omega (c5: ~1000; c3, p = 20,000: ~20). If the int8
+  // C held more than i8_excess p^2 entries beyond the support it was computed
+  // at, int8 stays off for the solve (c3: 227 - 43 per row; c5: 60 - 9; c4:
+  // 41 - 5; c5 iteration 2: 357 - 242). Counts only, so the decision is
+  // deterministic and the same on every rank.
   if (c->i8 && !c->i8_force && !c->refit) {
     const double pp = (double)c->p;
-    if (st.gemm_i8 && !c->i8_banned && c->bf16_cand >= 0 &&
-        (double)(st.n_cand - c->bf16_cand) > c->i8_excess * pp * pp)
+    if (st.gemm_i8 && !c->i8_banned &&
+        (double)(st.n_cand - nnz_before) > c->i8_excess * pp * pp)
       c->i8_banned = true;
-    if (!st.gemm_i8) c->bf16_cand = st.n_cand;
     c->i8_on = !c->i8_banned &&
                (c->i8_on ? (double)st.n_cand <= c->i8_off * pp
                          : ((double)st.n_cand <= c->i8_at * pp ||
@@ -2573,7 +2573,6 @@ accord_status accord_set_lambda(accord_ctx* c, double lambda) {
     c->lam = lambda;
     // AUTO's int8 cost check starts over (the candidate density depends on lambda)
     c->i8_banned = false;
-    c->bf16_cand = -1;
     refresh_objective(c);
   });
 }
