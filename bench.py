@@ -510,6 +510,16 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
     if world == 1 and not args.no_cpu_baseline:
         with all_host_cores():
             cpu = cpu_baseline_leg(Xt, cfg, lam, list(ws) + list(stats), len(ws), args)
+    # the refine (exact float64 SDDMM of every candidate) is the largest sparse
+    # kernel: |C| gathered X^T rows of 4n bytes per step, against the
+    # random-row gather ceiling measured on B200 (profiles/r02/gather_bench.txt)
+    ref_b = float(np.mean([s_["n_cand"] for s_ in stats])) * 4.0 * n
+    ref_ms = float(np.mean([s_["ms_refine"] for s_ in stats]))
+    ref_gbs = ref_b / (ref_ms * 1e-3) / 1e9 if ref_ms > 0 else None
+    refine_rf = {"bound": "hbm (random 4n-byte row gathers)", "algorithmic_bytes": ref_b,
+                 "ms": ref_ms, "achieved_GBps": ref_gbs, "ceiling_GBps": 7230.0,
+                 "frac": ref_gbs / 7230.0 if ref_gbs else None,
+                 "ceiling_source": "gather microbenchmark, profiles/r02/gather_bench.txt"}
     out = {
         "metric": metric_name(cfg), "value": value, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -537,6 +547,7 @@ def run_ours(args, rank, world, local_rank, local_world, barrier):
                      "frac_of_library_int8": achieved / lib_i8["tops"] if lib_i8 else None,
                      "algorithmic": f"2*p_k*p*n = {2.0 * pk0 * p * n:.3e} FLOP per launch",
                      "ms_per_launch": ms_gemm_max},
+        "refine_roofline": refine_rf,
         "step_split_ms": {k: float(np.mean([s[k] for s in stats])) for k in
                           ("ms_gemm", "ms_finalize", "ms_refine", "ms_prox", "ms_spmm",
                            "ms_reduce", "ms_total")},
