@@ -83,6 +83,11 @@ constexpr int kEpiWarp0 = 4;
 template <int kMode, int kStagesT> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
   static constexpr int kBKe = kMode == 2 ? 2 * BK : BK;                  // elements per 128-B row
+  // epilogue warps: int8 halves the MMA time per tile, so two warps share a
+  // TMEM lane quarter (each half of the 256 columns); with four the int8
+  // GEMM ran 19 % faster with its epilogue switched off (ACCORD_DEBUG_GEMM=1)
+  static constexpr int kEpiW = kMode == 2 ? 8 : 4;
+  static constexpr int kThreads = 128 + 32 * kEpiW;
   static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 64 / 32 KB
   static constexpr int kStages = kStagesT;
   static constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
@@ -195,7 +200,7 @@ struct TileIt {
 // reduction (no emission: a certified lower bound on n max_{i!=k} |G_ik|
 // into *ep.max_out, the lambda_max of a path)
 template <int kMode, int kStagesT, bool kFast, int kDiag = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<kMode, kStagesT>::kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
                const __grid_constant__ CUtensorMap mB_hi,
@@ -234,7 +239,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     }
     for (int a = 0; a < kAccStages; ++a) {
       tc::mbar_init(tc::smem_u32(&tfull[a]), 1);
-      tc::mbar_init(tc::smem_u32(&tempty[a]), 8);   // 4 epilogue warps x 2 CTAs
+      tc::mbar_init(tc::smem_u32(&tempty[a]), 2 * Cfg<kMode, kStagesT>::kEpiW);   // x 2 CTAs
     }
     tc::fence_mbar_init();
   }
@@ -336,7 +341,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     __syncwarp();
   } else if (warp >= kEpiWarp0) {
     // ============================ epilogue (both CTAs) ====================
-    const int q = warp - kEpiWarp0;                 // TMEM lane quarter (= warp % 4)
+    constexpr int kEpiW = Cfg<kMode, kStagesT>::kEpiW;
+    constexpr int kCols = BN / (kEpiW / 4);          // columns of the tile this warp tests
+    const int q = (warp - kEpiWarp0) & 3;            // TMEM lane quarter (= warp % 4)
+    const int cb = ((warp - kEpiWarp0) >> 2) * kCols;   // first column of this warp's part
     const float thr = (float)(ep.lam_cand / ep.inv_n);   // n * lambda
     const double thr_d = ep.lam_cand / ep.inv_n;
     const float inv_nf = (float)ep.inv_n;
@@ -424,13 +432,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
         if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
         continue;
       }
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      const uint32_t tbase =
+          tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN) + (uint32_t)cb;
       // TMEM -> registers 32 columns at a time, one load ahead: the next
       // 32 columns are in flight while these are tested
       uint32_t va[32], vb[32];
       tc::tmem_ld32(tbase, va);
 #pragma unroll 1
-      for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
+      for (int ch2 = 0; ch2 < kCols / 64; ++ch2) {
         tc::tmem_ld_wait();                                   // va = columns 64 ch2 + [0, 32)
         tc::tmem_ld32(tbase + ch2 * 64 + 32, vb);             // in flight: 64 ch2 + [32, 64)
         if (dbg >= 3) {   // diagnostics: 3 = TMEM reads only, 4 = reads + max test only
@@ -446,18 +455,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           } else if (va[0] == 0xffffffffu && vb[31] == 0xffffffffu) {
             pool.row[0] = 0;                  // keep the loads alive (never true)
           }
-          if (ch2 + 1 < BN / 64) tc::tmem_ld32(tbase + (ch2 + 1) * 64, va);
+          if (ch2 + 1 < kCols / 64) tc::tmem_ld32(tbase + (ch2 + 1) * 64, va);
           continue;
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1) {
             tc::tmem_ld_wait();                               // vb ready
-            if (ch2 + 1 < BN / 64)                            // in flight: next 64 ch2 + [0, 32)
+            if (ch2 + 1 < kCols / 64)                         // in flight: next 64 ch2 + [0, 32)
               tc::tmem_ld32(tbase + (ch2 + 1) * 64, va);
           }
           const uint32_t* v = h ? vb : va;
-          const int c0 = n0 + ch2 * 64 + h * 32;
+          const int c0 = n0 + cb + ch2 * 64 + h * 32;
           const int64_t sp0 = sp;
           if constexpr (kDiag == 1) {   // audit: the raw accumulator of every computed entry
             if (row_ok) {
@@ -911,13 +920,17 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   if (i8) {
     if (bsel != 0) return -1;   // no sharded-X ring in int8
     if (ep.audit_acc)
-      gemm_tc_kernel<2, 6, true, 1><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+      gemm_tc_kernel<2, 6, true, 1><<<grid, Cfg<2, 6>::kThreads, Cfg<2, 6>::kSmemBytes, st>>>(
+          ACCORD_TC_ARGS_I8);
     else if (ep.max_out)
-      gemm_tc_kernel<2, 6, true, 2><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+      gemm_tc_kernel<2, 6, true, 2><<<grid, Cfg<2, 6>::kThreads, Cfg<2, 6>::kSmemBytes, st>>>(
+          ACCORD_TC_ARGS_I8);
     else if (ep.sym == 2)
-      gemm_tc_kernel<2, 6, true, 3><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+      gemm_tc_kernel<2, 6, true, 3><<<grid, Cfg<2, 6>::kThreads, Cfg<2, 6>::kSmemBytes, st>>>(
+          ACCORD_TC_ARGS_I8);
     else
-      gemm_tc_kernel<2, 6, true><<<grid, kThreads, Cfg<2, 6>::kSmemBytes, st>>>(ACCORD_TC_ARGS_I8);
+      gemm_tc_kernel<2, 6, true><<<grid, Cfg<2, 6>::kThreads, Cfg<2, 6>::kSmemBytes, st>>>(
+          ACCORD_TC_ARGS_I8);
   } else if (mode == ACCORD_GEMM_BF16X3)
     gemm_tc_kernel<0, 3, true><<<grid, kThreads, Cfg<0, 3>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_lo[bsel]));

@@ -722,6 +722,16 @@ __device__ __forceinline__ double warp_dot_f64(const T* ys, const T* __restrict_
   return warp_sum(s);
 }
 
+// Shared-memory slot of element e of Y_i staged as float64 for the refine:
+// element e belongs to lane (e >> 2) & 31 of 128-element block e >> 7; the
+// lanes' first double2 (elements 0-1 of their four) are stored contiguously,
+// then their second (elements 2-3), so each of the two 16-byte loads of a
+// warp reads 512 contiguous bytes (4 wavefronts, no bank conflict; with the
+// plain layout the lanes were 32 B apart and each load took 8)
+__device__ __forceinline__ int64_t yd_slot(int64_t e) {
+  return ((((e >> 7) * 2 + ((e >> 1) & 1)) * 32 + ((e >> 2) & 31)) << 1) + (e & 1);
+}
+
 // <y, x> as above with y already in float64 (staged once per work item):
 // one F2F per product instead of two (the XU pipe's F2F.F64.F32 was the
 // refine's limit); the same products in the same order, so bitwise equal
@@ -729,16 +739,18 @@ __device__ __forceinline__ double warp_dot_f64_yd(const double* ysd, const float
                                                   int64_t ldk, int lane) {
   constexpr int V = 4;
   constexpr int kStep = 32 * V;
+  const double2* y2 = reinterpret_cast<const double2*>(ysd);
   double s = 0.0;
   int64_t m = lane * V;
   for (; m + 7 * kStep < ldk; m += 8 * kStep) {
     float4 x[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(xr + m + u * kStep));
+    const int64_t U0 = (m - lane * V) >> 7;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const double2 y0 = *reinterpret_cast<const double2*>(ysd + m + u * kStep);
-      const double2 y1 = *reinterpret_cast<const double2*>(ysd + m + u * kStep + 2);
+      const double2 y0 = y2[((U0 + u) * 2) * 32 + lane];
+      const double2 y1 = y2[((U0 + u) * 2 + 1) * 32 + lane];
       s = fma(y0.x, (double)x[u].x, s);
       s = fma(y0.y, (double)x[u].y, s);
       s = fma(y1.x, (double)x[u].z, s);
@@ -747,8 +759,9 @@ __device__ __forceinline__ double warp_dot_f64_yd(const double* ysd, const float
   }
   for (; m < ldk; m += kStep) {
     const float4 x = __ldg(reinterpret_cast<const float4*>(xr + m));
-    const double2 y0 = *reinterpret_cast<const double2*>(ysd + m);
-    const double2 y1 = *reinterpret_cast<const double2*>(ysd + m + 2);
+    const int64_t U = (m - lane * V) >> 7;
+    const double2 y0 = y2[(U * 2) * 32 + lane];
+    const double2 y1 = y2[(U * 2 + 1) * 32 + lane];
     s = fma(y0.x, (double)x.x, s);
     s = fma(y0.y, (double)x.y, s);
     s = fma(y1.x, (double)x.z, s);
@@ -801,7 +814,7 @@ __global__ void __launch_bounds__(256) refine_kernel(int64_t pk, int64_t n, int6
     for (int64_t m = threadIdx.x * V; m < ldk; m += blockDim.x * V) {
       const VT v = *reinterpret_cast<const VT*>(Y + r * ldk + m);
 #pragma unroll
-      for (int u = 0; u < V; ++u) yd[m + u] = (double)vget(v, u);
+      for (int u = 0; u < V; ++u) yd[yd_slot(m + u)] = (double)vget(v, u);
     }
     __syncthreads();
   } else {
@@ -1532,7 +1545,9 @@ int launch_refine(int dtype, int64_t pk, int64_t n, int64_t ldk, const int64_t* 
     return !(e && std::strcmp(e, "f32") == 0);
   }();
   const bool stage_d = dtype != ACCORD_F64 && ff != 1 && yd;
-  size_t smem = (size_t)ldk * ((dtype == ACCORD_F64 || stage_d) ? 8 : 4);
+  // (the float64 staging's conflict-free layout fills whole 128-element blocks)
+  size_t smem = stage_d ? (size_t)((ldk + 127) / 128 * 128) * 8
+                        : (size_t)ldk * (dtype == ACCORD_F64 ? 8 : 4);
   const int y_global = smem > 200 * 1024 ? 1 : 0;
   if (y_global) smem = 0;
   // threads per block (warps share the item's candidates): ACCORD_REFINE_THREADS (A-B);
