@@ -80,13 +80,13 @@ constexpr uint32_t kTileB = BNH * BK * 2;       // 16 KB
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
-template <int kMode, int kStagesT> struct Cfg {
+template <int kMode, int kStagesT, int kEpiWT = 0> struct Cfg {
   static constexpr int kOps = kMode == 0 ? 2 : 1;                        // hi (+lo)
   static constexpr int kBKe = kMode == 2 ? 2 * BK : BK;                  // elements per 128-B row
   // epilogue warps: int8 halves the MMA time per tile, so two warps share a
   // TMEM lane quarter (each half of the 256 columns); with four the int8
   // GEMM ran 19 % faster with its epilogue switched off (ACCORD_DEBUG_GEMM=1)
-  static constexpr int kEpiW = kMode == 2 ? 8 : 4;
+  static constexpr int kEpiW = kEpiWT ? kEpiWT : (kMode == 2 ? 8 : 4);
   static constexpr int kThreads = 128 + 32 * kEpiW;
   static constexpr uint32_t kStageBytes = kOps * (kTileA + kTileB);      // 64 / 32 KB
   static constexpr int kStages = kStagesT;
@@ -199,8 +199,8 @@ struct TileIt {
 // accumulator to ep.audit_acc, for the filter certification test); 2 = max
 // reduction (no emission: a certified lower bound on n max_{i!=k} |G_ik|
 // into *ep.max_out, the lambda_max of a path)
-template <int kMode, int kStagesT, bool kFast, int kDiag = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<kMode, kStagesT>::kThreads, 1)
+template <int kMode, int kStagesT, bool kFast, int kDiag = 0, int kEpiWT = 0>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<kMode, kStagesT, kEpiWT>::kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                const __grid_constant__ CUtensorMap mA_lo,
                const __grid_constant__ CUtensorMap mB_hi,
@@ -209,8 +209,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
                int group_n, int unit_n, int dbg, int l2hint, EpiParams ep,
                const float2* __restrict__ blk_sdmax, OmegaView om,
                PoolView pool) {
-  constexpr int kStages = Cfg<kMode, kStagesT>::kStages;
-  constexpr uint32_t kStageBytes = Cfg<kMode, kStagesT>::kStageBytes;
+  constexpr int kStages = Cfg<kMode, kStagesT, kEpiWT>::kStages;
+  constexpr uint32_t kStageBytes = Cfg<kMode, kStagesT, kEpiWT>::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + kStages * kStageBytes);
@@ -239,7 +239,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     }
     for (int a = 0; a < kAccStages; ++a) {
       tc::mbar_init(tc::smem_u32(&tfull[a]), 1);
-      tc::mbar_init(tc::smem_u32(&tempty[a]), 2 * Cfg<kMode, kStagesT>::kEpiW);   // x 2 CTAs
+      tc::mbar_init(tc::smem_u32(&tempty[a]), 2 * Cfg<kMode, kStagesT, kEpiWT>::kEpiW);   // x 2 CTAs
     }
     tc::fence_mbar_init();
   }
@@ -264,7 +264,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
           uint8_t* s = smem + stage * kStageBytes;
           const uint32_t fb_local = tc::smem_u32(&full[stage]);
           const uint32_t fb = tc::mapa_shared(fb_local, 0);                  // leader's barrier
-          const int kx = kb * Cfg<kMode, kStagesT>::kBKe;
+          const int kx = kb * Cfg<kMode, kStagesT, kEpiWT>::kBKe;
           if (tc::elect_one()) {
             if (leader) tc::mbar_arrive_expect_tx(fb_local, 2 * kStageBytes);   // both CTAs' bytes
             // stage layout: A_hi | B_hi | (A_lo | B_lo)
@@ -341,7 +341,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mA_hi,
     __syncwarp();
   } else if (warp >= kEpiWarp0) {
     // ============================ epilogue (both CTAs) ====================
-    constexpr int kEpiW = Cfg<kMode, kStagesT>::kEpiW;
+    constexpr int kEpiW = Cfg<kMode, kStagesT, kEpiWT>::kEpiW;
     constexpr int kCols = BN / (kEpiW / 4);          // columns of the tile this warp tests
     const int q = (warp - kEpiWarp0) & 3;            // TMEM lane quarter (= warp % 4)
     const int cb = ((warp - kEpiWarp0) >> 2) * kCols;   // first column of this warp's part
@@ -820,6 +820,10 @@ TcGemmPlan* tc_plan_create(const __nv_bfloat16* Yhi0, const __nv_bfloat16* Ylo0,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg<2, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, 6, true, 0, 8>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1, 6>::kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true, 0, 16>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2, 6>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true, 1>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2, 6>::kSmemBytes);
     cudaFuncSetAttribute(gemm_tc_kernel<2, 6, true, 2>,
@@ -905,7 +909,8 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
   const char* dbg_env = std::getenv("ACCORD_DEBUG_GEMM");
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   // ACCORD_GEMM_VARIANT (tuning / A-B diagnostics, results identical):
-  // 0 = 6-stage ring + FMNMX3 fast path (default), 1 = 7 stages, 2 = no fast path
+  // 0 = 6-stage ring + FMNMX3 fast path (default), 1 = 7 stages, 2 = no fast path,
+  // 3 = bf16 with 8 epilogue warps (the int8 kernel's split), 4 = int8 with 16
   int var = 0;
   if (const char* e = std::getenv("ACCORD_GEMM_VARIANT")) var = std::atoi(e);
   // ACCORD_GEMM_L2HINT (tuning): 1 = TMA loads of X^T with evict_last, 2 = evict_first
@@ -928,6 +933,9 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
     else if (ep.sym == 2)
       gemm_tc_kernel<2, 6, true, 3><<<grid, Cfg<2, 6>::kThreads, Cfg<2, 6>::kSmemBytes, st>>>(
           ACCORD_TC_ARGS_I8);
+    else if (var == 4)   // A-B: 16 epilogue warps (64 columns each)
+      gemm_tc_kernel<2, 6, true, 0, 16><<<grid, Cfg<2, 6, 16>::kThreads, Cfg<2, 6>::kSmemBytes,
+                                          st>>>(ACCORD_TC_ARGS_I8);
     else
       gemm_tc_kernel<2, 6, true><<<grid, Cfg<2, 6>::kThreads, Cfg<2, 6>::kSmemBytes, st>>>(
           ACCORD_TC_ARGS_I8);
@@ -948,6 +956,9 @@ int launch_gemm_tc(TcGemmPlan* plan, int mode, int ybuf, int bsel, int sm_count,
         ACCORD_TC_ARGS(plan->b_hi[bsel]));
   else if (var == 2)
     gemm_tc_kernel<1, 6, false><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
+        ACCORD_TC_ARGS(plan->b_hi[bsel]));
+  else if (var == 3)
+    gemm_tc_kernel<1, 6, true, 0, 8><<<grid, Cfg<1, 6, 8>::kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
         ACCORD_TC_ARGS(plan->b_hi[bsel]));
   else
     gemm_tc_kernel<1, 6, true><<<grid, kThreads, Cfg<1, 6>::kSmemBytes, st>>>(
