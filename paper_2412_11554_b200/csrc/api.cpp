@@ -792,10 +792,12 @@ void validate(const accord_init_params* prm) {
 }
 
 // Default candidate-pool capacity (entries): the first iteration (G = S) has
-// the most candidates (config 5: ~380 per row), so size for ~512 per row.
+// the most candidates (config 5: ~380 per row), so size for ~512 per row; at
+// least 2 M entries (104 MB), which small problems whose int8 filter admits
+// more than 512 per row need (config 2 at lambda = 0.1: ~1.3 M)
 int64_t default_capacity(int64_t pk, int64_t p) {
   const int64_t dense = pk * p;
-  int64_t cap = std::min<int64_t>(dense, std::max<int64_t>(pk * 512, 1 << 20));
+  int64_t cap = std::min<int64_t>(dense, std::max<int64_t>(pk * 512, 1 << 21));
   return std::max<int64_t>(cap, std::min<int64_t>(dense, pk * 16));
 }
 

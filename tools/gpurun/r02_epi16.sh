@@ -10,3 +10,4 @@ done; done
 for v in 0 3; do
   ACCORD_AUTO_GEMM=bf16 ACCORD_GEMM_VARIANT=$v timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/e16_bf16_v$v.json 2> gpurun_out/e16_bf16_v$v.log; echo bfv$v=$?
 done
+timeout 900 python -m pytest -x -q -m gpu tests/test_gpu_workspace.py > gpurun_out/e16_pytest_ws.log 2>&1; echo ws=$?
