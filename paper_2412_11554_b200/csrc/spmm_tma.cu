@@ -74,7 +74,8 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
                 __nv_bfloat16* __restrict__ Yhi, __nv_bfloat16* __restrict__ Ylo,
                 float* __restrict__ row_A, float* __restrict__ row_B, double* __restrict__ row_D2,
                 double* __restrict__ row_Y2, const float* __restrict__ wn2,
-                double* __restrict__ row_D2b, SpmmItems items, int ydrop) {
+                double* __restrict__ row_D2b, SpmmItems items, int ydrop,
+                int par_emit) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t stage_bytes = (uint32_t)(ldk * 4);
   float* data = reinterpret_cast<float*>(sm);
@@ -180,11 +181,19 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       // ~10 entries in the steady state, so one item of lookahead left the
       // producer waiting on these loads: ncu, int8-filter c5 run)
       Raw qa{0.f, 0.f, 0.f, 0}, qb{0.f, 0.f, 0.f, 0};
+#ifdef ACCORD_SPMM_PREFETCH2
+      // (A-B) the second 32 entries of items k+1, k+2 in flight as well
+      Raw qa2{0.f, 0.f, 0.f, 0}, qb2{0.f, 0.f, 0.f, 0};
+#endif
       {
         const int64_t b0 = __shfl_sync(0xffffffffu, begj, 0), e0_ = __shfl_sync(0xffffffffu, endj, 0);
         load_raw(b0 + lane, e0_, qa);
         const int64_t b1 = __shfl_sync(0xffffffffu, begj, 1), e1_ = __shfl_sync(0xffffffffu, endj, 1);
         if (nv > 1) load_raw(b1 + lane, e1_, qb);
+#ifdef ACCORD_SPMM_PREFETCH2
+        load_raw(b0 + 32 + lane, e0_, qa2);
+        if (nv > 1) load_raw(b1 + 32 + lane, e1_, qb2);
+#endif
       }
       for (int k = 0; k < nv; ++k) {
         const int64_t r = __shfl_sync(0xffffffffu, rj, k);
@@ -196,34 +205,99 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         int32_t cc;
         cvt(qa, w, d, d2, cc);
         qa = qb;
+#ifdef ACCORD_SPMM_PREFETCH2
+        const Raw q2 = qa2;
+        qa2 = qb2;
+#endif
         {
           const int kn = k + 2 < 32 ? k + 2 : 31;
           const int64_t bn = __shfl_sync(0xffffffffu, begj, kn);
           const int64_t en = __shfl_sync(0xffffffffu, endj, kn);
           if (k + 2 < nv) load_raw(bn + lane, en, qb);
+#ifdef ACCORD_SPMM_PREFETCH2
+          if (k + 2 < nv) load_raw(bn + 32 + lane, en, qb2);
+#endif
         }
         // one entry of lookahead so that the item's last nonzero carries kFlagLast
         bool pend = false;
         double pw = 0.0, pd = 0.0, pd2 = 0.0;
         int32_t pc = 0;
         for (int64_t e0 = beg; e0 < end; e0 += 32) {
+#ifdef ACCORD_SPMM_PREFETCH2
+          if (e0 == beg + 32) cvt(q2, w, d, d2, cc);
+          else
+#endif
           if (e0 != beg) load(e0 + lane, end, w, d, d2, cc);
           const bool keep = (e0 + lane < end) && ((w != 0.0) || (d != 0.0) || (d2 != 0.0));
-          unsigned m = __ballot_sync(0xffffffffu, keep);
-          while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const double ws = __shfl_sync(0xffffffffu, w, src);
-            const double ds = __shfl_sync(0xffffffffu, d, src);
-            const double ds2 = kPair ? __shfl_sync(0xffffffffu, d2, src) : 0.0;
-            const int32_t cs = __shfl_sync(0xffffffffu, cc, src);
-            if (pend) emit(pw, pd, pd2, pc, kFlagData, r, chunk, nch);
-            pend = true;
-            pw = ws;
-            pd = ds;
-            pd2 = ds2;
-            pc = cs;
+          const unsigned m = __ballot_sync(0xffffffffu, keep);
+          if (!m) continue;
+          if (!par_emit) {   // one entry at a time (ACCORD_SPMM_SERIAL=1, A-B)
+            unsigned mm = m;
+            while (mm) {
+              const int src = __ffs(mm) - 1;
+              mm &= mm - 1;
+              const double ws = __shfl_sync(0xffffffffu, w, src);
+              const double ds = __shfl_sync(0xffffffffu, d, src);
+              const double ds2 = kPair ? __shfl_sync(0xffffffffu, d2, src) : 0.0;
+              const int32_t cs = __shfl_sync(0xffffffffu, cc, src);
+              if (pend) emit(pw, pd, pd2, pc, kFlagData, r, chunk, nch);
+              pend = true;
+              pw = ws;
+              pd = ds;
+              pd2 = ds2;
+              pc = cs;
+            }
+            continue;
           }
+          // Warp-parallel issue: every kept lane fills its own stage (its
+          // rank among this batch's entries), up to `stages` per round, so a
+          // batch costs one round of waits / metadata / bulk copies instead
+          // of one serial emit per entry (a single producer's serial issue
+          // rate limited the ring: DESIGN §7, gather microbenchmark). The
+          // highest kept lane's entry is held back as the new pending one
+          // (the item's last entry must carry kFlagLast); that lane emits the
+          // previous pending entry at rank 0. Stages are filled in the same
+          // order as by the serial loop, so the sums are bitwise the same.
+          const int hi = 31 - __clz(m);
+          const unsigned em = m & ~(1u << hi);
+          const int p0 = pend ? 1 : 0;
+          int myrank = -1;
+          if (lane == hi) myrank = pend ? 0 : -1;
+          else if ((em >> lane) & 1u) myrank = p0 + __popc(em & ((1u << lane) - 1u));
+          const int cnt = p0 + __popc(em);
+          for (int r0 = 0; r0 < cnt; r0 += stages) {
+            const int nr = min(stages, cnt - r0);
+            if (myrank >= r0 && myrank < r0 + nr) {
+              int si = stage + (myrank - r0);
+              uint32_t ph = phase;
+              if (si >= stages) { si -= stages; ph ^= 1; }
+              tc::mbar_wait(tc::smem_u32(&empty[si]), ph ^ 1);
+              const bool mine = lane != hi;
+              StageMeta& mt = meta[si];
+              mt.w = mine ? w : pw;
+              mt.d = mine ? d : pd;
+              mt.d2 = mine ? d2 : pd2;
+              mt.row = r;
+              mt.chunk = chunk;
+              mt.nch = nch;
+              mt.flags = kFlagData;
+              const uint32_t fb = tc::smem_u32(&full[si]);
+              tc::mbar_arrive_expect_tx(fb, stage_bytes);
+              bulk_g2s(tc::smem_u32(data + (size_t)si * ldk), Xt + (int64_t)(mine ? cc : pc) * ldk,
+                       stage_bytes, fb);
+            }
+            // a round's lanes must have passed their waits before the next
+            // round's lanes wait on the same stages for the following phase
+            // (a parity wait one phase ahead would return at once)
+            __syncwarp();
+            stage += nr;
+            if (stage >= stages) { stage -= stages; phase ^= 1; }
+          }
+          pend = true;
+          pw = __shfl_sync(0xffffffffu, w, hi);
+          pd = __shfl_sync(0xffffffffu, d, hi);
+          pd2 = kPair ? __shfl_sync(0xffffffffu, d2, hi) : 0.0;
+          pc = __shfl_sync(0xffffffffu, cc, hi);
         }
         if (pend) emit(pw, pd, pd2, pc, kFlagData | kFlagLast, r, chunk, nch);
         else emit(0.0, 0.0, 0.0, 0, kFlagLast, r, chunk, nch);
@@ -257,10 +331,148 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     }
   };
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool fin = false;           // an item completed in the previous round
+  int64_t f_row = 0;
+  int f_chunk = 0, f_nch = 1;
   for (;;) {
-    // two stages per round when the item continues: both waits and both
-    // shared-memory loads are issued before the arithmetic (halves the
-    // dependent latency chain per staged row)
+    // The finalize of the item completed in the previous round runs here, at
+    // the top of the next round, so that the loop has a single back edge:
+    // with the finalize (and its zeroing) at the end of the body, ptxas
+    // merged two definitions of the accumulators at the loop head and
+    // copied all of them (48 registers in the paired kernel) every round.
+    if (fin) {
+      fin = false;
+      const int64_t m_row = f_row;
+      const int m_chunk = f_chunk, m_nch = f_nch;
+
+      // ---------------- item complete: finalize the row (or its partial) ----
+      const int64_t r = m_row;
+      bool finish = true;
+      if (m_nch > 1) {
+        const int64_t slot0 = items.slot_ptr[r];
+        if (active) {
+          double* py = items.part_y + (slot0 + m_chunk) * ldk + c0;
+          double* pd = items.part_d + (slot0 + m_chunk) * ldk + c0;
+#pragma unroll
+          for (int v = 0; v < kCols; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
+          if constexpr (kPair) {
+            double* pe = items.part_d2 + (slot0 + m_chunk) * ldk + c0;
+#pragma unroll
+            for (int v = 0; v < kCols; ++v) pe[v] = ae[v];
+          }
+        }
+        __threadfence();
+        named_sync(1, nct);
+        if (t == 0) *sh_flag = (atomicAdd(&items.row_done[r], 1) == m_nch - 1) ? 1 : 0;
+        named_sync(1, nct);
+        finish = *sh_flag != 0;
+        if (finish) {
+          __threadfence();
+          if (active) {
+#pragma unroll
+            for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
+            for (int k = 0; k < m_nch; ++k) {   // chunk order: deterministic sum
+              const double* py = items.part_y + (slot0 + k) * ldk + c0;
+              const double* pd = items.part_d + (slot0 + k) * ldk + c0;
+#pragma unroll
+              for (int v = 0; v < kCols; ++v) {
+                ay[v] += __ldcg(py + v);
+                ad[v] += __ldcg(pd + v);
+              }
+              if constexpr (kPair) {
+                const double* pe = items.part_d2 + (slot0 + k) * ldk + c0;
+#pragma unroll
+                for (int v = 0; v < kCols; ++v) ae[v] += __ldcg(pe + v);
+              }
+            }
+          }
+          if (t == 0) items.row_done[r] = 0;   // ready for the next trial
+        }
+      }
+      if (finish) {
+        double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0, e2 = 0.0;
+        if (active) {
+          float yt[kCols];
+#pragma unroll
+          for (int v = 0; v < kCols; ++v) {
+            d2 += ad[v] * ad[v];
+            y2 += ay[v] * ay[v];
+            if constexpr (kPair) e2 += ae[v] * ae[v];
+            yt[v] = (float)ay[v];
+          }
+          float* yo = Yout + r * ldk + c0;
+          *reinterpret_cast<float4*>(yo) = make_float4(yt[0], yt[1], yt[2], yt[3]);
+          if constexpr (kCols == 8)
+            *reinterpret_cast<float4*>(yo + 4) = make_float4(yt[4], yt[5], yt[6], yt[7]);
+          if (Yhi) {
+            uint32_t hp[kCols / 2], lp[kCols / 2];
+#pragma unroll
+            for (int v = 0; v < kCols; v += 2) {
+              const __nv_bfloat162 h2 =
+                  ydrop ? __halves2bfloat162(filter_bf16_x(yt[v], ydrop), filter_bf16_x(yt[v + 1], ydrop))
+                        : filter_bf16x2(yt[v], yt[v + 1]);
+              const float2 hf = __bfloat1622float2(h2);
+              const __nv_bfloat162 l2 = __floats2bfloat162_rn(yt[v] - hf.x, yt[v + 1] - hf.y);
+              hp[v / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+              lp[v / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+              const double e0 = (double)yt[v] - (double)hf.x, e1 = (double)yt[v + 1] - (double)hf.y;
+              a2 += e0 * e0 + e1 * e1;
+              b2 += (double)yt[v] * (double)yt[v] + (double)yt[v + 1] * (double)yt[v + 1];
+            }
+            if constexpr (kCols == 8) {
+              *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+              if (Ylo)
+                *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+            } else {
+              *reinterpret_cast<uint2*>(Yhi + r * ldk + c0) = make_uint2(hp[0], hp[1]);
+              if (Ylo) *reinterpret_cast<uint2*>(Ylo + r * ldk + c0) = make_uint2(lp[0], lp[1]);
+            }
+          }
+        }
+        d2 = wsum(d2);
+        y2 = wsum(y2);
+        a2 = wsum(a2);
+        b2 = wsum(b2);
+        if constexpr (kPair) e2 = wsum(e2);
+        const int cw = warp - 1;
+        double* sh_red = red + rowpar * 80;
+        rowpar ^= 1;
+        if (lane == 0) {
+          sh_red[cw] = d2;
+          sh_red[16 + cw] = y2;
+          sh_red[32 + cw] = a2;
+          sh_red[48 + cw] = b2;
+          sh_red[64 + cw] = e2;
+        }
+        named_sync(1, nct);
+        if (t == 0) {
+          double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+          for (int q = 0; q < ncw; ++q) {   // fixed order
+            s0 += sh_red[q];
+            s1 += sh_red[16 + q];
+            s2 += sh_red[32 + q];
+            s3 += sh_red[48 + q];
+            s4 += sh_red[64 + q];
+          }
+          if (row_D2) row_D2[r] = s0;
+          if (kPair && row_D2b) row_D2b[r] = s4;
+          if (row_Y2) row_Y2[r] = s1;
+          if (Yhi) {
+            // rounded up: these enter an upper bound (the GEMM filter)
+            if (row_A) row_A[r] = __double2float_ru(sqrt(s2) * (1.0 + 1e-12));
+            if (row_B) row_B[r] = __double2float_ru(sqrt(s3) * (1.0 + 1e-12));
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
+    }
+    // one staged row per round, the accumulators updated in place. Two
+    // stages per round (both waits and loads issued before the arithmetic,
+    // rounds 1-2b) made ptxas rename the accumulators and copy all of them
+    // back every round (48 registers in the paired kernel, plus spills at
+    // its 128-register cap); same-box c5 A-B: 34.3-34.9 ms per step either
+    // way, 37 ms for the round-2b kernel (profiles/r02c/ab_spmm_consumer)
     tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
     const int f0 = meta[stage].flags;
     if (f0 & kFlagEnd) break;
@@ -272,168 +484,24 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
       a0 = *reinterpret_cast<const float4*>(xs);
       if constexpr (kCols == 8) b0 = *reinterpret_cast<const float4*>(xs + 4);
     }
-    const int s1 = stage + 1 == stages ? 0 : stage + 1;
-    const uint32_t ph1 = stage + 1 == stages ? phase ^ 1 : phase;
-    const bool two = !(f0 & kFlagLast);   // the item goes on: stage s1 belongs to it
-    int f1 = 0;
-    double w1 = 0.0, d1 = 0.0, e1d = 0.0;
-    float4 a1 = z4, b1 = z4;
-    if (two) {
-      tc::mbar_wait(tc::smem_u32(&full[s1]), ph1);
-      f1 = meta[s1].flags;
-      w1 = meta[s1].w;
-      d1 = meta[s1].d;
-      if constexpr (kPair) e1d = meta[s1].d2;
-      if ((f1 & kFlagData) && active) {
-        const float* xs = data + (size_t)s1 * ldk + c0;
-        a1 = *reinterpret_cast<const float4*>(xs);
-        if constexpr (kCols == 8) b1 = *reinterpret_cast<const float4*>(xs + 4);
-      }
-    }
-    const bool last = (f0 & kFlagLast) || (f1 & kFlagLast);
-    const int ls = (f0 & kFlagLast) ? stage : s1;
+    const bool last = (f0 & kFlagLast) != 0;
     int64_t m_row = 0;        // row / chunk of the finished item (read before the release)
     int m_chunk = 0, m_nch = 1;
     if (last) {
-      m_row = meta[ls].row;
-      m_chunk = meta[ls].chunk;
-      m_nch = meta[ls].nch;
+      m_row = meta[stage].row;
+      m_chunk = meta[stage].chunk;
+      m_nch = meta[stage].nch;
     }
     accumulate(w0, d0, e0d, a0, b0);
-    if (two) accumulate(w1, d1, e1d, a1, b1);
     __syncwarp();
-    if (lane == 0) {
-      tc::mbar_arrive(tc::smem_u32(&empty[stage]));
-      if (two) tc::mbar_arrive(tc::smem_u32(&empty[s1]));
+    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[stage]));
+    if (++stage == stages) { stage = 0; phase ^= 1; }
+    if (last) {
+      fin = true;
+      f_row = m_row;
+      f_chunk = m_chunk;
+      f_nch = m_nch;
     }
-    stage = s1;
-    phase = ph1;
-    if (two) {
-      if (++stage == stages) { stage = 0; phase ^= 1; }
-    }
-    if (!last) continue;
-
-    // ---------------- item complete: finalize the row (or its partial) ----
-    const int64_t r = m_row;
-    bool finish = true;
-    if (m_nch > 1) {
-      const int64_t slot0 = items.slot_ptr[r];
-      if (active) {
-        double* py = items.part_y + (slot0 + m_chunk) * ldk + c0;
-        double* pd = items.part_d + (slot0 + m_chunk) * ldk + c0;
-#pragma unroll
-        for (int v = 0; v < kCols; ++v) { py[v] = ay[v]; pd[v] = ad[v]; }
-        if constexpr (kPair) {
-          double* pe = items.part_d2 + (slot0 + m_chunk) * ldk + c0;
-#pragma unroll
-          for (int v = 0; v < kCols; ++v) pe[v] = ae[v];
-        }
-      }
-      __threadfence();
-      named_sync(1, nct);
-      if (t == 0) *sh_flag = (atomicAdd(&items.row_done[r], 1) == m_nch - 1) ? 1 : 0;
-      named_sync(1, nct);
-      finish = *sh_flag != 0;
-      if (finish) {
-        __threadfence();
-        if (active) {
-#pragma unroll
-          for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
-          for (int k = 0; k < m_nch; ++k) {   // chunk order: deterministic sum
-            const double* py = items.part_y + (slot0 + k) * ldk + c0;
-            const double* pd = items.part_d + (slot0 + k) * ldk + c0;
-#pragma unroll
-            for (int v = 0; v < kCols; ++v) {
-              ay[v] += __ldcg(py + v);
-              ad[v] += __ldcg(pd + v);
-            }
-            if constexpr (kPair) {
-              const double* pe = items.part_d2 + (slot0 + k) * ldk + c0;
-#pragma unroll
-              for (int v = 0; v < kCols; ++v) ae[v] += __ldcg(pe + v);
-            }
-          }
-        }
-        if (t == 0) items.row_done[r] = 0;   // ready for the next trial
-      }
-    }
-    if (finish) {
-      double d2 = 0.0, y2 = 0.0, a2 = 0.0, b2 = 0.0, e2 = 0.0;
-      if (active) {
-        float yt[kCols];
-#pragma unroll
-        for (int v = 0; v < kCols; ++v) {
-          d2 += ad[v] * ad[v];
-          y2 += ay[v] * ay[v];
-          if constexpr (kPair) e2 += ae[v] * ae[v];
-          yt[v] = (float)ay[v];
-        }
-        float* yo = Yout + r * ldk + c0;
-        *reinterpret_cast<float4*>(yo) = make_float4(yt[0], yt[1], yt[2], yt[3]);
-        if constexpr (kCols == 8)
-          *reinterpret_cast<float4*>(yo + 4) = make_float4(yt[4], yt[5], yt[6], yt[7]);
-        if (Yhi) {
-          uint32_t hp[kCols / 2], lp[kCols / 2];
-#pragma unroll
-          for (int v = 0; v < kCols; v += 2) {
-            const __nv_bfloat162 h2 =
-                ydrop ? __halves2bfloat162(filter_bf16_x(yt[v], ydrop), filter_bf16_x(yt[v + 1], ydrop))
-                      : filter_bf16x2(yt[v], yt[v + 1]);
-            const float2 hf = __bfloat1622float2(h2);
-            const __nv_bfloat162 l2 = __floats2bfloat162_rn(yt[v] - hf.x, yt[v + 1] - hf.y);
-            hp[v / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-            lp[v / 2] = *reinterpret_cast<const uint32_t*>(&l2);
-            const double e0 = (double)yt[v] - (double)hf.x, e1 = (double)yt[v + 1] - (double)hf.y;
-            a2 += e0 * e0 + e1 * e1;
-            b2 += (double)yt[v] * (double)yt[v] + (double)yt[v + 1] * (double)yt[v + 1];
-          }
-          if constexpr (kCols == 8) {
-            *reinterpret_cast<uint4*>(Yhi + r * ldk + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-            if (Ylo)
-              *reinterpret_cast<uint4*>(Ylo + r * ldk + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
-          } else {
-            *reinterpret_cast<uint2*>(Yhi + r * ldk + c0) = make_uint2(hp[0], hp[1]);
-            if (Ylo) *reinterpret_cast<uint2*>(Ylo + r * ldk + c0) = make_uint2(lp[0], lp[1]);
-          }
-        }
-      }
-      d2 = wsum(d2);
-      y2 = wsum(y2);
-      a2 = wsum(a2);
-      b2 = wsum(b2);
-      if constexpr (kPair) e2 = wsum(e2);
-      const int cw = warp - 1;
-      double* sh_red = red + rowpar * 80;
-      rowpar ^= 1;
-      if (lane == 0) {
-        sh_red[cw] = d2;
-        sh_red[16 + cw] = y2;
-        sh_red[32 + cw] = a2;
-        sh_red[48 + cw] = b2;
-        sh_red[64 + cw] = e2;
-      }
-      named_sync(1, nct);
-      if (t == 0) {
-        double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
-        for (int q = 0; q < ncw; ++q) {   // fixed order
-          s0 += sh_red[q];
-          s1 += sh_red[16 + q];
-          s2 += sh_red[32 + q];
-          s3 += sh_red[48 + q];
-          s4 += sh_red[64 + q];
-        }
-        if (row_D2) row_D2[r] = s0;
-        if (kPair && row_D2b) row_D2b[r] = s4;
-        if (row_Y2) row_Y2[r] = s1;
-        if (Yhi) {
-          // rounded up: these enter an upper bound (the GEMM filter)
-          if (row_A) row_A[r] = __double2float_ru(sqrt(s2) * (1.0 + 1e-12));
-          if (row_B) row_B[r] = __double2float_ru(sqrt(s3) * (1.0 + 1e-12));
-        }
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
   }
 }
 
@@ -523,6 +591,10 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
   if (const char* e = std::getenv("ACCORD_SPMM_COLS"))
     cols = (std::atoi(e) == 4 && ldk <= 4 * kSpmmTmaMaxConsumers) ? 4 : 8;
   const int consumers = (int)round_up(ldk / cols, 32);
+  // warp-parallel producer issue (ACCORD_SPMM_SERIAL=1: one entry at a time;
+  // read per launch, tests flip it)
+  const char* eser = std::getenv("ACCORD_SPMM_SERIAL");
+  const int par_emit = (eser && std::atoi(eser) == 1) ? 0 : 1;
   // persistent: exactly the resident blocks (items are dealt round-robin)
   auto launch = [&](auto kern) {
     int per_sm = 0;
@@ -532,7 +604,7 @@ int launch_spmm_tma(int64_t pk, int64_t ldk, const int64_t* ptr, const int32_t* 
       per_sm = 1;
     kern<<<sm_count * std::min(per_sm, 8), 32 + consumers, smem, st>>>(
         pk, ldk, stages, ptr, col, wn, wo, Xt, Yout, Yhi, Ylo, row_A, row_B, row_D2, row_Y2,
-        wn2, row_D2b, items, Ylo ? 0 : ydrop);
+        wn2, row_D2b, items, Ylo ? 0 : ydrop, par_emit);
   };
   if (cols == 4) {
     if (wn2) launch(spmm_tma_kernel<true, 4>);

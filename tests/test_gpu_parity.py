@@ -169,6 +169,33 @@ def test_bitwise_reproducible(spmm, monkeypatch):
         assert np.array_equal(csr.val, runs[0][0].val)
 
 
+@pytest.mark.parametrize("cols", ["4", "8"])
+def test_spmm_parallel_producer_issue_is_bitwise(cols, monkeypatch):
+    """The TMA SpMM's warp-parallel producer issue (every kept entry of a
+    32-entry batch fills its own ring stage in one round, up to `stages` per
+    round) stages the same X^T rows in the same order as the serial producer
+    (ACCORD_SPMM_SERIAL=1), so the sums are bitwise the same: equal iterates,
+    tau schedule and objective on a problem with hub rows and short rows,
+    with rings shallower than a batch (2 and 4 stages: several issue rounds
+    per batch, wrapping the ring) and a deep one."""
+    _cuda()
+    monkeypatch.setenv("ACCORD_SPMM_TMA", "1")
+    monkeypatch.setenv("ACCORD_SPMM_COLS", cols)
+    pr = make_problem("t_hubs_f32")
+    inv_L = 1.0 / O.spectral_bound(pr.Xt)
+    runs = []
+    for serial, stages in (("1", "8"), ("0", "8"), ("0", "2"), ("0", "4"), ("0", "16")):
+        monkeypatch.setenv("ACCORD_SPMM_SERIAL", serial)
+        monkeypatch.setenv("ACCORD_SPMM_STAGES", stages)
+        csr, stats, _ = run_gpu(pr.Xt, 0.05, 12, inv_L, A.GEMM_AUTO)
+        runs.append((csr, [(x["tau"], x["f"], x["n_cand"], x["nnz"]) for x in stats]))
+    c0, s0 = runs[0]
+    for c1, s1 in runs[1:]:
+        assert s0 == s1
+        assert np.array_equal(c0.row_ptr, c1.row_ptr) and np.array_equal(c0.col, c1.col)
+        assert np.array_equal(c0.val, c1.val)
+
+
 def test_warm_start_roundtrip():
     _cuda()
     pr = make_problem("t_ba_f64")
