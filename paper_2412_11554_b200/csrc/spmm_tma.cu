@@ -46,6 +46,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -331,20 +340,43 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     }
   };
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  bool fin = false;           // an item completed in the previous round
-  int64_t f_row = 0;
-  int f_chunk = 0, f_nch = 1;
+  const uint32_t data_u32 = tc::smem_u32(data) + (uint32_t)c0 * 4u;   // this thread's columns, stage 0
+  // Two nested loops: the inner one walks the staged rows of one item with the
+  // accumulators updated in place (a single back edge, one definition of each
+  // accumulator at its head: with the finalize inside a single loop ptxas
+  // merged two definitions and copied all 48 accumulator registers of the
+  // paired kernel every round), the outer one zeroes them and finalizes.
   for (;;) {
-    // The finalize of the item completed in the previous round runs here, at
-    // the top of the next round, so that the loop has a single back edge:
-    // with the finalize (and its zeroing) at the end of the body, ptxas
-    // merged two definitions of the accumulators at the loop head and
-    // copied all of them (48 registers in the paired kernel) every round.
-    if (fin) {
-      fin = false;
-      const int64_t m_row = f_row;
-      const int m_chunk = f_chunk, m_nch = f_nch;
-
+#pragma unroll
+    for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
+    int64_t m_row = 0;        // row / chunk of the finished item (read before the release)
+    int m_chunk = 0, m_nch = 1;
+    for (;;) {
+      tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
+      const int f0 = meta[stage].flags;
+      if (f0 & kFlagEnd) return;   // the end marker follows the last item
+      const bool last = (f0 & kFlagLast) != 0;
+      if (last) {
+        m_row = meta[stage].row;
+        m_chunk = meta[stage].chunk;
+        m_nch = meta[stage].nch;
+      }
+      if ((f0 & kFlagData) && active) {   // an empty item's only stage carries no data
+        const double w0 = meta[stage].w, d0 = meta[stage].d;
+        const double e0d = kPair ? meta[stage].d2 : 0.0;
+        // 32-bit shared addresses (the generic pointer made the compiler
+        // rebuild the shared window base from SR_CgaCtaId every round)
+        const uint32_t xs = data_u32 + (uint32_t)stage * stage_bytes;
+        const float4 a0 = lds128(xs);
+        const float4 b0 = kCols == 8 ? lds128(xs + 16) : z4;
+        accumulate(w0, d0, e0d, a0, b0);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[stage]));
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+      if (last) break;
+    }
+    {
       // ---------------- item complete: finalize the row (or its partial) ----
       const int64_t r = m_row;
       bool finish = true;
@@ -431,8 +463,10 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         }
         d2 = wsum(d2);
         y2 = wsum(y2);
-        a2 = wsum(a2);
-        b2 = wsum(b2);
+        if (Yhi) {   // the operand-split norms exist only with the bf16 copy (block-uniform)
+          a2 = wsum(a2);
+          b2 = wsum(b2);
+        }
         if constexpr (kPair) e2 = wsum(e2);
         const int cw = warp - 1;
         double* sh_red = red + rowpar * 80;
@@ -464,43 +498,6 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
           }
         }
       }
-#pragma unroll
-      for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
-    }
-    // one staged row per round, the accumulators updated in place. Two
-    // stages per round (both waits and loads issued before the arithmetic,
-    // rounds 1-2b) made ptxas rename the accumulators and copy all of them
-    // back every round (48 registers in the paired kernel, plus spills at
-    // its 128-register cap); same-box c5 A-B: 34.3-34.9 ms per step either
-    // way, 37 ms for the round-2b kernel (profiles/r02c/ab_spmm_consumer)
-    tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
-    const int f0 = meta[stage].flags;
-    if (f0 & kFlagEnd) break;
-    const double w0 = meta[stage].w, d0 = meta[stage].d;
-    const double e0d = kPair ? meta[stage].d2 : 0.0;
-    float4 a0 = z4, b0 = z4;
-    if ((f0 & kFlagData) && active) {
-      const float* xs = data + (size_t)stage * ldk + c0;
-      a0 = *reinterpret_cast<const float4*>(xs);
-      if constexpr (kCols == 8) b0 = *reinterpret_cast<const float4*>(xs + 4);
-    }
-    const bool last = (f0 & kFlagLast) != 0;
-    int64_t m_row = 0;        // row / chunk of the finished item (read before the release)
-    int m_chunk = 0, m_nch = 1;
-    if (last) {
-      m_row = meta[stage].row;
-      m_chunk = meta[stage].chunk;
-      m_nch = meta[stage].nch;
-    }
-    accumulate(w0, d0, e0d, a0, b0);
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[stage]));
-    if (++stage == stages) { stage = 0; phase ^= 1; }
-    if (last) {
-      fin = true;
-      f_row = m_row;
-      f_chunk = m_chunk;
-      f_nch = m_nch;
     }
   }
 }
