@@ -121,14 +121,14 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         m.chunk = chunk;
         m.nch = nch;
         m.flags = flags;
+        // every stage carries a row: a dataless one (an item whose entries
+        // were all dropped, the end marker) gets X^T row 0 with zero weights,
+        // which adds exact zeros (X is finite, checked at create), so the
+        // consumer loop has no data / no-data branch
         const uint32_t fb = tc::smem_u32(&full[stage]);
-        if (flags & kFlagData) {
-          tc::mbar_arrive_expect_tx(fb, stage_bytes);
-          bulk_g2s(tc::smem_u32(data + (size_t)stage * ldk), Xt + (int64_t)c * ldk, stage_bytes,
-                   fb);
-        } else {
-          tc::mbar_arrive(fb);
-        }
+        tc::mbar_arrive_expect_tx(fb, stage_bytes);
+        bulk_g2s(tc::smem_u32(data + (size_t)stage * ldk),
+                 Xt + (int64_t)((flags & kFlagData) ? c : 0) * ldk, stage_bytes, fb);
       }
       __syncwarp();
       if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -180,29 +180,22 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         d2 = kPair ? (double)q.w2 - (double)q.o : 0.0;
         cc = q.cc;
       };
-      auto load = [&](int64_t e, int64_t end, double& w, double& d, double& d2, int32_t& cc) {
-        Raw q;
-        load_raw(e, end, q);
-        cvt(q, w, d, d2, cc);
-      };
       // lookahead of two items: the first 32 entries of items k+1 (set a)
       // and k+2 (set b) are in flight while item k is emitted (items have
       // ~10 entries in the steady state, so one item of lookahead left the
       // producer waiting on these loads: ncu, int8-filter c5 run)
       Raw qa{0.f, 0.f, 0.f, 0}, qb{0.f, 0.f, 0.f, 0};
-#ifdef ACCORD_SPMM_PREFETCH2
-      // (A-B) the second 32 entries of items k+1, k+2 in flight as well
+      // the second 32 entries of items k+1, k+2 are in flight as well (the
+      // int8 filter leaves ~60 candidates per row at c5, i.e. two batches per
+      // item: round 2c A-B, 27.9 -> 26.7 ms per step)
       Raw qa2{0.f, 0.f, 0.f, 0}, qb2{0.f, 0.f, 0.f, 0};
-#endif
       {
         const int64_t b0 = __shfl_sync(0xffffffffu, begj, 0), e0_ = __shfl_sync(0xffffffffu, endj, 0);
         load_raw(b0 + lane, e0_, qa);
         const int64_t b1 = __shfl_sync(0xffffffffu, begj, 1), e1_ = __shfl_sync(0xffffffffu, endj, 1);
         if (nv > 1) load_raw(b1 + lane, e1_, qb);
-#ifdef ACCORD_SPMM_PREFETCH2
         load_raw(b0 + 32 + lane, e0_, qa2);
         if (nv > 1) load_raw(b1 + 32 + lane, e1_, qb2);
-#endif
       }
       for (int k = 0; k < nv; ++k) {
         const int64_t r = __shfl_sync(0xffffffffu, rj, k);
@@ -214,29 +207,27 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         int32_t cc;
         cvt(qa, w, d, d2, cc);
         qa = qb;
-#ifdef ACCORD_SPMM_PREFETCH2
         const Raw q2 = qa2;
         qa2 = qb2;
-#endif
         {
           const int kn = k + 2 < 32 ? k + 2 : 31;
           const int64_t bn = __shfl_sync(0xffffffffu, begj, kn);
           const int64_t en = __shfl_sync(0xffffffffu, endj, kn);
           if (k + 2 < nv) load_raw(bn + lane, en, qb);
-#ifdef ACCORD_SPMM_PREFETCH2
           if (k + 2 < nv) load_raw(bn + 32 + lane, en, qb2);
-#endif
         }
         // one entry of lookahead so that the item's last nonzero carries kFlagLast
         bool pend = false;
         double pw = 0.0, pd = 0.0, pd2 = 0.0;
         int32_t pc = 0;
+        Raw qn{0.f, 0.f, 0.f, 0};
         for (int64_t e0 = beg; e0 < end; e0 += 32) {
-#ifdef ACCORD_SPMM_PREFETCH2
+          // batch 0 came with the item lookahead (qa), batch 1 too (q2); from
+          // batch 2 on (long rows: the first iterations, hub rows) each batch
+          // is requested while the previous one is being emitted
           if (e0 == beg + 32) cvt(q2, w, d, d2, cc);
-          else
-#endif
-          if (e0 != beg) load(e0 + lane, end, w, d, d2, cc);
+          else if (e0 != beg) cvt(qn, w, d, d2, cc);
+          if (e0 != beg && e0 + 32 < end) load_raw(e0 + 32 + lane, end, qn);
           const bool keep = (e0 + lane < end) && ((w != 0.0) || (d != 0.0) || (d2 != 0.0));
           const unsigned m = __ballot_sync(0xffffffffu, keep);
           if (!m) continue;
@@ -312,7 +303,7 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
         else emit(0.0, 0.0, 0.0, 0, kFlagLast, r, chunk, nch);
       }
     }
-    emit(0.0, 0.0, 0.0, 0, kFlagEnd, 0, 0, 0);
+    emit(0.0, 0.0, 0.0, 0, kFlagEnd | kFlagLast, 0, 0, 0);
     return;
   }
 
@@ -340,7 +331,10 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
     }
   };
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const uint32_t data_u32 = tc::smem_u32(data) + (uint32_t)c0 * 4u;   // this thread's columns, stage 0
+  // this thread's columns in stage 0 (32-bit shared address; threads past the
+  // row end read column 0 and discard it)
+  const uint32_t data_u32 = tc::smem_u32(data) + (active ? (uint32_t)c0 * 4u : 0u);
+  const uint32_t meta_u32 = tc::smem_u32(meta);
   // Two nested loops: the inner one walks the staged rows of one item with the
   // accumulators updated in place (a single back edge, one definition of each
   // accumulator at its head: with the finalize inside a single loop ptxas
@@ -350,32 +344,40 @@ spmm_tma_kernel(int64_t pk, int64_t ldk, int stages, const int64_t* __restrict__
 #pragma unroll
     for (int v = 0; v < kCols; ++v) { ay[v] = 0.0; ad[v] = 0.0; ae[v] = 0.0; }
     int64_t m_row = 0;        // row / chunk of the finished item (read before the release)
-    int m_chunk = 0, m_nch = 1;
+    int m_chunk = 0, m_nch = 1, m_flags = 0;
     for (;;) {
       tc::mbar_wait(tc::smem_u32(&full[stage]), phase);
-      const int f0 = meta[stage].flags;
-      if (f0 & kFlagEnd) return;   // the end marker follows the last item
+      // the stage's metadata (three 16-byte loads) and this thread's columns
+      // are requested together: one shared-memory latency per round, and no
+      // branch before the arithmetic
+      const uint32_t ms = meta_u32 + (uint32_t)stage * (uint32_t)sizeof(StageMeta);
+      const uint32_t xs = data_u32 + (uint32_t)stage * stage_bytes;
+      double w0, d0, e0d;
+      int64_t mrow;
+      int mchunk, mnch, f0, mpad;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(mchunk), "=r"(mnch), "=r"(f0), "=r"(mpad)
+                   : "r"(ms + 32)
+                   : "memory");
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w0), "=d"(d0) : "r"(ms) : "memory");
+      asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=d"(e0d), "=l"(mrow) : "r"(ms + 16) : "memory");
+      const float4 a0 = lds128(xs);
+      const float4 b0 = kCols == 8 ? lds128(xs + 16) : z4;
+      // unconditional: dataless stages carry zero weights and a finite row
+      accumulate(w0, d0, kPair ? e0d : 0.0, a0, b0);
       const bool last = (f0 & kFlagLast) != 0;
       if (last) {
-        m_row = meta[stage].row;
-        m_chunk = meta[stage].chunk;
-        m_nch = meta[stage].nch;
-      }
-      if ((f0 & kFlagData) && active) {   // an empty item's only stage carries no data
-        const double w0 = meta[stage].w, d0 = meta[stage].d;
-        const double e0d = kPair ? meta[stage].d2 : 0.0;
-        // 32-bit shared addresses (the generic pointer made the compiler
-        // rebuild the shared window base from SR_CgaCtaId every round)
-        const uint32_t xs = data_u32 + (uint32_t)stage * stage_bytes;
-        const float4 a0 = lds128(xs);
-        const float4 b0 = kCols == 8 ? lds128(xs + 16) : z4;
-        accumulate(w0, d0, e0d, a0, b0);
+        m_row = mrow;
+        m_chunk = mchunk;
+        m_nch = mnch;
+        m_flags = f0;
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[stage]));
       if (++stage == stages) { stage = 0; phase ^= 1; }
       if (last) break;
     }
+    if (m_flags & kFlagEnd) return;   // the end marker follows the last item
     {
       // ---------------- item complete: finalize the row (or its partial) ----
       const int64_t r = m_row;
@@ -537,7 +539,10 @@ int launch_item_rows(int64_t rows, const int64_t* itm_ptr, int32_t* item_row, cu
 
 size_t spmm_tma_smem(int64_t ldk, int* stages) {
   const int64_t sb = ldk * 4;
-  int want = 8;   // stages (4 KB each at n = 1000); ACCORD_SPMM_STAGES: tuning
+  // stages (4 KB each at n = 1000); 16 absorb the row finalize and the item
+  // boundaries better than 8 (round 2c A-B: 26.7 -> 25.4 ms per step at c5);
+  // ACCORD_SPMM_STAGES: tuning
+  int want = 16;
   if (const char* e = std::getenv("ACCORD_SPMM_STAGES")) want = std::max(2, std::atoi(e));
   int s = (int)std::min<int64_t>(want, std::max<int64_t>(2, (want * 4096) / sb));
   *stages = s;
