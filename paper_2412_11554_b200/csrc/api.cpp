@@ -916,7 +916,8 @@ Footprint footprint(const accord_init_params* prm) {
   // work items of C: <= p_k + cap / L items; split-row slots reserved
   const int64_t items = pk + cap / kItemEntries + 1024;
   a += 3 * R(items * 8) + 2 * R(items * 4);
-  const bool tma = !sharded && spmm_tma_supported(prm->dtype, ldk) && pk >= 65536;
+  const bool tma = !sharded && spmm_tma_supported(prm->dtype, ldk) && pk >= 65536 &&
+                   ldk % 256 == 0;   // mirrors create_impl's choice
   if (tma || std::getenv("ACCORD_SPMM_TMA")) a += 3 * R((size_t)(64 + pk / 64) * ldk * 8);
   f.transient = tr;
   f.total = a + tr;
@@ -1393,7 +1394,12 @@ void create_impl(accord_ctx* c, const accord_init_params* prm) {
   // producer/consumer pipeline has too few items per block to hide its
   // per-item latency and the block-per-row kernel is faster (config 3:
   // 0.8 vs 0.4 ms per trial; config 4: 1.8 vs 3.4 ms)
+  // ... and only when every consumer warp is full (ldk a multiple of 256): with
+  // lanes past the row end the row finalize diverges, and at config 6 (n = 365,
+  // one candidate per row) the block-per-row kernel is twice as fast (0.58 vs
+  // 1.15 ms per step, profiles/r02c/c6ab)
   c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk) && c->pk >= 65536 &&
+                c->ldk % 256 == 0 &&
                 std::getenv("ACCORD_SPMM_PLAIN") == nullptr;   // env: A-B diagnostic
   if (std::getenv("ACCORD_SPMM_TMA"))   // env: force (tests of the TMA path at small sizes)
     c->tma_spmm = !c->sharded && spmm_tma_supported(c->dtype, c->ldk);
